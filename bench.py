@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""bench.py -- SparseVILA decode-stage hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {svl,reference}]
+
+Step = one fresh-retrieval decode step of a 28-layer stack (NVILA-8B /
+Qwen2-7B depth) on the long-video workload (BASELINE.json configs[2]: 32768
+retained visual tokens, 512 + 256 text rows at the last of 256 generated
+tokens, k = keep_budget(32768, 0.90) = 3277, batch 1, 28 q / 4 KV heads,
+d = 128): per layer svl_retrieve (a1-a3) then svl_sparse_decode_attn (a4-a5)
+through the C ABI, replayed as one CUDA graph.  28 distinct layer KV caches
+(1.9 GB) rotate, so the working set is > L2 every step.
+
+value  = algorithmic HBM bytes of the step (scored visual
+         K + selected K/V + text K/V once + q + out + idx) / step time, summed
+         over ranks (weak scaling: every rank serves its own request).
+e2e    = the same through the public API with host buffers: per step the
+         new token's q and K/V rows go H2D from pinned memory, the graph
+         replays, and the attention outputs come back D2H.
+--impl reference = the fp64 CPU oracle (oracle/), the paper-method baseline
+         of this tier, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAYERS = 28
+WORKLOAD = "long-video"
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def step_bytes(wl, n_q=1):
+    """Algorithmic bytes of one layer's fresh-retrieval step:
+    scored visual K + selected K,V + text K,V (text K counted once) + q + out + idx."""
+    T = wl.vb + wl.t_after                   # text rows attended at this step
+    row = wl.d * 2
+    kvis = wl.B * wl.Hkv * wl.nv * row
+    sel = wl.B * wl.Hkv * wl.k * 2 * row
+    text = wl.B * wl.Hkv * T * 2 * row
+    q = wl.B * n_q * wl.H * row
+    out = wl.B * wl.H * wl.d * 4
+    idx = wl.B * wl.Hkv * wl.k * 4
+    return {"score": kvis + wl.B * wl.Hkv * T * row + q,   # what the scoring kernel must read
+            "total": kvis + sel + text + q + out + idx}
+
+
+def kv_cache_bytes(entries, layers, kv_heads, d, elem_bytes):
+    """SPEC.md:331 cache_stats byte accounting: entries * 2 (K and V) * d * heads * layers * width."""
+    return entries * 2 * d * kv_heads * layers * elem_bytes
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.strip().splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- CPU oracle
+
+
+def cpu_oracle_sample(wl, budget_s=12.0, nthreads=None):
+    """Time the fp64 oracle (as it stands) on whole layers of the workload
+    until ~budget_s of CPU work; returns (bytes/s, layers, threads, seconds)."""
+    import oracle
+    import torch
+    from paper_2510_17777_b200 import inputs as gen
+    nthreads = nthreads or os.cpu_count() or 1
+    x = gen.make_decode_inputs(wl, seed=0)
+    nb = step_bytes(wl)["total"]
+    layers, t_total = 0, 0.0
+    while t_total < budget_s and layers < LAYERS:
+        t0 = time.perf_counter()
+        idx, _, _ = oracle.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k,
+                                    nthreads=nthreads)
+        oracle.sparse_decode(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx,
+                             nthreads=nthreads)
+        t_total += time.perf_counter() - t0
+        layers += 1
+    _ = torch
+    return nb * layers / t_total, layers, nthreads, t_total
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2510_17777_b200 import inputs as gen
+    wl = gen.CONFIGS[WORKLOAD]
+    per_layer = step_bytes(wl)["total"]
+    # each step = a bounded sample (2 layers) of the 28-layer step
+    import oracle
+    x = gen.make_decode_inputs(wl, seed=0)
+    nth = os.cpu_count() or 1
+    sample_layers = 2
+
+    def one():
+        for _ in range(sample_layers):
+            idx, _, _ = oracle.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k,
+                                        nthreads=nth)
+            oracle.sparse_decode(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx,
+                                 nthreads=nth)
+
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = time.perf_counter() - t0
+    sec_per_layer = dt / (args.steps * sample_layers)
+    value = per_layer / sec_per_layer / 1e9
+    line = {
+        "impl": "reference", "metric": "decode step HBM GB/s (retrieve+sparse attn) @32k visual tok",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec_per_layer * LAYERS * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(wl),
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nth, "kind": "oracle",
+                         "sample": f"{sample_layers} of {LAYERS} layers per step (fp64 C oracle, "
+                                   f"OpenMP over units), ms_per_step extrapolated to {LAYERS} layers"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def config_dict(wl):
+    return {"workload": f"{WORKLOAD}: {LAYERS}-layer fresh-retrieval decode step",
+            "B": wl.B, "H": wl.H, "Hkv": wl.Hkv, "d": wl.d, "visual_tokens": wl.nv,
+            "text_rows": wl.vb + wl.t_after, "k": wl.k, "decode_sparsity": 0.90, "layers": LAYERS,
+            "l2": "inputs > L2: 28 rotating layer KV caches (1.9 GB) per step"}
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="svl", choices=["svl", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON checks)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_17777_b200 import inputs as gen
+    from paper_2510_17777_b200 import svl
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    svl.lib()
+
+    wl = gen.CONFIGS[WORKLOAD]
+    nbytes = step_bytes(wl)
+    # ---- 28 distinct layers (rank-dependent seeds: independent requests per rank)
+    Ks, Vs, qs, qds = [], [], [], []
+    for layer in range(LAYERS):
+        x = gen.make_decode_inputs(wl, seed=1000 * rank + layer, device=dev)
+        Ks.append(x["K"])
+        Vs.append(x["V"])
+        qs.append(x["q"])
+        qds.append(x["q_dec"])
+        seq = x["seq_len"]
+    idxs = [torch.empty(wl.B, wl.Hkv, wl.k, dtype=torch.int32, device=dev) for _ in range(LAYERS)]
+    outs = [torch.empty(wl.B, wl.H, wl.d, dtype=torch.float32, device=dev) for _ in range(LAYERS)]
+    ws_r, ws_d = svl.Workspace(dev), svl.Workspace(dev)
+    ws_r.get(svl.retrieve_workspace_size(wl.B, 1, wl.H, wl.Hkv, wl.d, wl.nv))
+    ws_d.get(svl.sparse_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
+
+    def layer_retrieve(l, flags=0):
+        svl.retrieve(qs[l], Ks[l], seq, wl.vb, wl.nv, wl.k, flags=flags, idx_out=idxs[l], ws=ws_r)
+
+    def layer_decode(l):
+        svl.sparse_decode_attn(qds[l], Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l], out=outs[l],
+                               ws=ws_d)
+
+    def full_step():
+        for l in range(LAYERS):
+            layer_retrieve(l)
+            layer_decode(l)
+
+    def graph_of(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                fn()
+        torch.cuda.synchronize()
+        return g
+
+    g_step = graph_of(full_step)
+    g_score = graph_of(lambda: [layer_retrieve(l, svl.SVL_RETRIEVE_SCORE_ONLY) for l in range(LAYERS)])
+    g_select = graph_of(lambda: [layer_retrieve(l, svl.SVL_RETRIEVE_SELECT_ONLY) for l in range(LAYERS)])
+    g_decode = graph_of(lambda: [layer_decode(l) for l in range(LAYERS)])
+
+    if args.profile:
+        for _ in range(max(args.warmup, 1)):
+            g_step.replay()
+        for _ in range(args.steps):
+            g_step.replay()
+        torch.cuda.synchronize()
+        return 0
+
+    def timed(g, steps, warmup):
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return e0.elapsed_time(e1) / steps  # ms per replay
+
+    # ---- headline: the full 28-layer step, clocks sampled during the timed region
+    with ClockSampler(local) as clk:
+        ms_step = timed(g_step, args.steps, args.warmup)
+    clocks = clk.summary()
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = t.item()
+    total_bytes = nbytes["total"] * LAYERS * world
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    # ---- breakdown (same stream, CUDA events): score / select / decode graphs
+    sub = max(200, args.steps // 4)
+    ms_score = timed(g_score, sub, 10)
+    ms_select = timed(g_select, sub, 10)
+    ms_decode = timed(g_decode, sub, 10)
+
+    # ---- e2e through the public API with host buffers (pinned)
+    q_host = torch.stack(qs).cpu().pin_memory()
+    qd_host = torch.stack(qds).cpu().pin_memory()
+    newkv_host = torch.zeros(LAYERS, 2, wl.B, wl.Hkv, wl.d, dtype=torch.bfloat16).pin_memory()
+    out_host = torch.empty(LAYERS, wl.B, wl.H, wl.d, dtype=torch.float32).pin_memory()
+    q_dev = torch.stack(qs)
+    qd_dev = torch.stack(qds)
+    newkv_dev = torch.empty(LAYERS, 2, wl.B, wl.Hkv, wl.d, dtype=torch.bfloat16, device=dev)
+    last = wl.seq_len - 1
+    for l in range(LAYERS):
+        newkv_host[l, 0] = Ks[l][:, :, last].cpu()
+        newkv_host[l, 1] = Vs[l][:, :, last].cpu()
+    qs_e = [q_dev[l] for l in range(LAYERS)]
+    qds_e = [qd_dev[l] for l in range(LAYERS)]
+
+    def e2e_step():
+        for l in range(LAYERS):
+            Ks[l][:, :, last].copy_(newkv_dev[l, 0])      # append the current token's K/V
+            Vs[l][:, :, last].copy_(newkv_dev[l, 1])
+            svl.retrieve(qs_e[l], Ks[l], seq, wl.vb, wl.nv, wl.k, idx_out=idxs[l], ws=ws_r)
+            svl.sparse_decode_attn(qds_e[l], Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l],
+                                   out=outs[l], ws=ws_d)
+
+    g_e2e = graph_of(e2e_step)
+    out_stack = torch.stack(outs)  # placeholder to size
+    h2d = q_host.numel() * 2 + qd_host.numel() * 2 + newkv_host.numel() * 2
+    d2h = out_host.numel() * 4
+    e2e_steps = max(50, args.steps // 10)
+
+    def e2e_once():
+        q_dev.copy_(q_host, non_blocking=True)
+        qd_dev.copy_(qd_host, non_blocking=True)
+        newkv_dev.copy_(newkv_host, non_blocking=True)
+        g_e2e.replay()
+        for l in range(LAYERS):
+            out_host[l].copy_(outs[l], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(5):
+        e2e_once()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_once()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    _ = out_stack
+
+    # ---- roofline of the dominant kernel (retrieval scoring)
+    peak, peak_src = peaks()
+    score_us = ms_score * 1e3 / LAYERS
+    achieved = nbytes["score"] / (score_us * 1e-6) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_score_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, layers, th, secs = cpu_oracle_sample(wl)
+        cpu = {"value": v / 1e9, "unit": "GB/s", "cores": th, "kind": "oracle",
+               "sample": f"{layers} whole layers of the long-video step (retrieve + sparse decode),"
+                         f" {secs:.1f} s of fp64 oracle work, OpenMP over (b, KV-group) units"}
+
+    launches = LAYERS * 4 * args.steps  # score + select + decode + merge per layer
+    if rank == 0:
+        line = {
+            "metric": "decode step HBM GB/s (retrieve+sparse attn) @32k visual tok",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded generator, paper_2510_17777_b200/inputs.py)",
+            "config": config_dict(wl),
+            "us_per_layer": ms_step * 1e3 / LAYERS,
+            "tokens_per_s": wl.B * world / (ms_step * 1e-3),
+            "hbm_frac_of_measured": value / world / peak,
+            "breakdown_us_per_layer": {"score": score_us, "select": ms_select * 1e3 / LAYERS,
+                                       "decode+merge": ms_decode * 1e3 / LAYERS},
+            "bytes_per_layer": nbytes["total"],
+            "roofline": {"bound": "hbm", "kernel": "score_kernel (svl_retrieve phase 1)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": nbytes["score"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": nbytes["total"] * LAYERS * world / (e2e_ms * 1e-3) / 1e9,
+                    "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "how": "pinned H2D of q + new K/V rows, CUDA-graph replay of the 56 C-ABI "
+                           "calls, D2H of the 28 layer outputs, host wall clock"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,228 @@
+/*
+ * sparsevila.h -- C ABI of libsparsevila.so, the B200 (sm_100a) decode-stage
+ * hot path of SparseVILA (arXiv 2510.17777, "Decoupling Visual Sparsity for
+ * Efficient VLM Inference").
+ *
+ * Calling rules:
+ *  - Plain C types only; every pointer is caller-owned.  "device" pointers
+ *    are CUDA global-memory addresses on the current device, "host" pointers
+ *    are ordinary CPU memory.  The library never allocates or frees memory.
+ *  - Every compute call is stream-ordered and asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).  Host
+ *    argument validation is synchronous: on any non-SVL_OK status nothing was
+ *    launched.  No call synchronises the device except
+ *    svl_read_device_flags (debug/test only).
+ *  - Stateless and re-entrant.  The only globals are a thread-local
+ *    last-error string and an immutable per-device attribute cache.
+ *  - Scratch comes from a caller-supplied device `workspace` of at least
+ *    svl_*_workspace_size(...) bytes, 256-byte aligned, which must be zero
+ *    filled once before its first use (svl_workspace_init); every call leaves
+ *    its counters at zero again.  A workspace serves one call at a time.
+ *  - bf16 tensors are IEEE bfloat16 bit patterns (uint16).  Row pointers and
+ *    row strides must be 16-byte aligned.  Head dims d in {64, 128}.
+ *
+ * Citations: PAPER.md / SPEC.md line numbers refer to the paper text and the
+ * spec written from it (DESIGN.md lists every reading taken where the paper
+ * is silent; "reading Ax" below).
+ */
+#ifndef SPARSEVILA_H_
+#define SPARSEVILA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+typedef enum {
+    SVL_OK = 0,
+    SVL_ERR_INVALID_ARGUMENT = 1, /* k > N_v, sparsity outside [0,1), NULL pointer, bad flags */
+    SVL_ERR_SHAPE = 2,            /* H % Hkv != 0, empty visual span, span outside capacity   */
+    SVL_ERR_ALIGNMENT = 3,        /* pointer / stride not 16-byte aligned                     */
+    SVL_ERR_WORKSPACE = 4,        /* workspace NULL, misaligned or smaller than required      */
+    SVL_ERR_UNSUPPORTED = 5,      /* d not in {64,128}, g or n_q*g too large, N_v too large, no sm_100 device */
+    SVL_ERR_CUDA = 6              /* a CUDA runtime call or kernel launch failed               */
+} svl_status;
+
+/* Device-side precondition bits, OR-ed into the workspace flag word
+ * (svl_read_device_flags).  Offending elements are skipped / treated as the
+ * lowest key so kernels never fault. */
+#define SVL_DEVFLAG_INDEX 1u      /* vis_idx out of [0,N_v) or not strictly ascending */
+#define SVL_DEVFLAG_NONFINITE 2u  /* NaN relevance / saliency; NaN ranks lowest          */
+#define SVL_DEVFLAG_SPAN 4u       /* seq_len[b] < visual_begin + visual_len + n_q, or > capacity       */
+
+/* ------------------------------------------------------------------ flags */
+#define SVL_NORM_VISUAL_ONLY 1u /* softmax over visual rows only (default: full causal prefix, reading A2) */
+#define SVL_SELECT_SHARED 2u    /* one selection per batch row, relevance summed over KV groups (reading A4) */
+/* svl_retrieve phase split (profiling / overlap): SCORE_ONLY runs phase 1
+ * (logits + chunk log-sum-exp partials into the workspace); SELECT_ONLY runs
+ * phase 2 (normalise, aggregate, top-k) from a workspace filled by a
+ * SCORE_ONLY call with identical arguments.  Neither bit = both phases. */
+#define SVL_RETRIEVE_SCORE_ONLY 0x100u
+#define SVL_RETRIEVE_SELECT_ONLY 0x200u
+
+/* Salience modes */
+#define SVL_SAL_SUMMARY 0       /* S == 1 summary token (CLIP)               */
+#define SVL_SAL_MULTI_SUMMARY 1 /* S >= 2 summary tokens (RADIO)             */
+#define SVL_SAL_INTRA_VISUAL 2  /* S == 0, mean intra-visual attention (SigLIP, QwenVL) */
+
+/* ------------------------------------------------------------------ types */
+/* A bf16 KV-cache view for one decoder layer: element (b, kv_head, row, c)
+ * lives at data + b*stride_b + kv_head*stride_h + row*stride_t + c
+ * (strides in elements, last dim contiguous).  `capacity` = rows allocated
+ * per (b, kv_head).  Device memory. */
+typedef struct {
+    const void* data;
+    int64_t stride_b, stride_h, stride_t;
+    int32_t capacity;
+} svl_kv;
+
+/* Sequence layout per batch row b:
+ * rows [0, visual_begin) are system text, [visual_begin, visual_begin +
+ * visual_len) the retained visual tokens, [visual_begin + visual_len,
+ * seq_len[b]) question / answer / generated text, the current token last.
+ * seq_len is a DEVICE int32 [B] array (it changes every decode step). */
+typedef struct {
+    int32_t visual_begin;
+    int32_t visual_len;
+    const int32_t* seq_len;
+} svl_span;
+
+/* -------------------------------------------------------------- retrieve */
+/*
+ * svl_retrieve -- query-aware visual-token retrieval (section
+ * 3.2 "Query-Aware Token Selection").
+ *
+ * For each unit (b, G) -- G a KV group, h in [G*g, G*g+g), g = H/Hkv
+ * (kv = h / g, reading A5) -- or each b with SVL_SELECT_SHARED:
+ *   s[r,h,j]  = scale * q[b,r,h,:] . K[b,G,j,:]
+ *   LSE[r,h]  = lse_in[b,r,h] if lse_in != NULL, else the natural-log
+ *               log-sum-exp of s over the causal prefix j <= seq_len-n_q+r
+ *               (visual rows only with SVL_NORM_VISUAL_ONLY)
+ *   score[j]  = sum_r sum_h exp(s[r,h,j] - LSE[r,h])     (visual j)
+ *   idx       = the k visual rows with the largest score, ties to the lower
+ *               index, written ascending, relative to visual_begin.
+ *
+ * q        device bf16 [B][n_q][H][d] contiguous (post-RoPE; reading A10).
+ *          n_q*g <= 32 in this version.
+ * K        device KV view (see svl_kv).
+ * span     visual span + device seq_len[B]; visual_len <= 131072.
+ * lse_in   device fp32 [B][n_q][H] or NULL.
+ * k        0 <= k <= visual_len (SVL_ERR_INVALID_ARGUMENT otherwise).
+ * scale    softmax scale, normally 1/sqrt(d) (reading A6).
+ * idx_out  device int32 [B][U][k], U = Hkv (or 1 with SVL_SELECT_SHARED).
+ * scores_out  device fp32 [B][U][visual_len] or NULL.
+ * Errors: host-checkable shape/argument errors return before launching;
+ * NaN scores set SVL_DEVFLAG_NONFINITE; a bad seq_len sets SVL_DEVFLAG_SPAN.
+ */
+svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv,
+                        int32_t d, svl_kv K, svl_span span, const float* lse_in, int32_t k,
+                        float scale, uint32_t flags, int32_t* idx_out, float* scores_out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+size_t svl_retrieve_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                   int32_t visual_len, uint32_t flags);
+
+/* ---------------------------------------------------- sparse decode attn */
+/*
+ * svl_sparse_decode_attn -- decode attention over the active set
+ * (SPEC.md:143-151, 315-323).
+ *
+ * For (b, h), G = h / g: attended rows, ascending,
+ *   [0, vb)  U  { vb + vis_idx[b][G][m] : m < k }  U  [vb + N_v, seq_len[b])
+ * (G replaced by 0 with SVL_SELECT_SHARED).  The caller appends the current
+ * token's K/V before the call (reading A9).
+ *   out[b,h,:] = sum_j softmax(scale * q.K_j)_j V_j   (fp32, reading A18)
+ *   lse[b,h]   = natural-log log-sum-exp of the attended logits
+ * Split-K flash-decoding with a log-sum-exp merge across splits; the merge
+ * order is fixed, results are bitwise reproducible.
+ *
+ * q        device bf16 [B][H][d] contiguous; g = H/Hkv <= 16.
+ * K, V     device KV views with identical capacity.
+ * vis_idx  device int32 [B][U][k], strictly ascending, in [0, N_v)
+ *          (violations set SVL_DEVFLAG_INDEX; offending rows are skipped).
+ *          k = 0 is allowed (text only).
+ * out      device fp32 [B][H][d]; lse_out device fp32 [B][H] or NULL.
+ */
+svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                  svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
+                                  int32_t k, uint32_t flags, float scale, float* out,
+                                  float* lse_out, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
+                                        int32_t visual_len, int32_t capacity, uint32_t flags);
+
+/* ----------------------------------------------------- prefill companion */
+/*
+ * svl_prefill_prune -- query-agnostic per-frame pruning (PAPER.md:113,
+ * 199-200).  For each b and frame f = [o_f, o_{f+1}):
+ * k_f = svl_keep_budget(N_f, prefill_sparsity); keep the k_f highest
+ * saliency tokens (ties to the lower index); frames concatenated in order;
+ * ascending global indices.  Bit-exact with the fp32 comparisons.
+ *
+ * saliency       device fp32 [B][N] (NaN ranks lowest, sets SVL_DEVFLAG_NONFINITE;
+ *                -0.0 == +0.0).
+ * frame_offsets  HOST int32 [n_frames+1], 0 = o_0 <= ... <= o_n = N, each
+ *                frame <= 131072 tokens; NULL = one global frame (N <= 131072).
+ * kept_idx       device int32 [B][kept_capacity].
+ * kept_total     HOST out: sum_f k_f (computed synchronously on the host
+ *                before launching; SVL_ERR_INVALID_ARGUMENT if > kept_capacity).
+ */
+svl_status svl_prefill_prune(const float* saliency, int32_t B, int32_t N,
+                             const int32_t* frame_offsets, int32_t n_frames,
+                             double prefill_sparsity, int32_t* kept_idx, int32_t kept_capacity,
+                             int32_t* kept_total, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+size_t svl_prune_workspace_size(int32_t B, int32_t N, int32_t n_frames);
+
+/*
+ * svl_salience -- encoder-attention salience per visual token (PAPER.md:113,
+ * 116 "streams softmax normalization and salience accumulation without
+ * explicitly forming the full attention matrix").
+ * Per frame f and encoder head h, P = softmax(scale * Q K^T) over all S+N_f
+ * columns (never materialised; two streaming passes):
+ *   SUMMARY        (S == 1): sal_j = mean_h P[0, S+j]
+ *   MULTI_SUMMARY  (S >= 2): sal_j = mean_h (1/S) sum_{s<S} P[s, S+j]
+ *   INTRA_VISUAL   (S == 0): sal_j = mean_h (1/N_f) sum_{i<N_f} P[i, j]
+ * Qe, Ke   device bf16 [F][S+N_f][H_e][d_e] contiguous, d_e <= 128, d_e % 8 == 0.
+ * saliency device fp32 [F][N_f].
+ * Mode/summary-count mismatch -> SVL_ERR_INVALID_ARGUMENT.
+ */
+svl_status svl_salience(const void* Qe, const void* Ke, int32_t F, int32_t S, int32_t N_f,
+                        int32_t H_e, int32_t d_e, int32_t mode, float scale, float* saliency,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+size_t svl_salience_workspace_size(int32_t F, int32_t S, int32_t N_f, int32_t H_e, int32_t d_e,
+                                   int32_t mode);
+
+/* --------------------------------------------------------------- helpers */
+/* keep_budget(n, s) = max(1, floor(n*(1-s) + 0.5)) for n > 0, 0 for n == 0,
+ * evaluated in IEEE double (reading A7); -1 if n < 0 or
+ * s outside [0, 1). */
+int64_t svl_keep_budget(int64_t n, double s);
+
+/* Zero-fill a workspace (stream-ordered). */
+svl_status svl_workspace_init(void* workspace, size_t workspace_bytes, void* stream);
+
+const char* svl_status_string(svl_status s);
+
+/* Thread-local description of the last non-OK status returned on this
+ * thread (includes the cudaError_t name for SVL_ERR_CUDA). */
+const char* svl_last_error_message(void);
+
+/* Synchronises `stream` and reads the device flag word (debug/test only). */
+svl_status svl_read_device_flags(void* workspace, void* stream, uint32_t* flags);
+svl_status svl_reset_device_flags(void* workspace, void* stream);
+
+/* Library build identifier ("sm_100a ..."). */
+const char* svl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSEVILA_H_ */

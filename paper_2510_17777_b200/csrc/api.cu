@@ -1,0 +1,437 @@
+// api.cu -- C-ABI host layer of libsparsevila.so (include/sparsevila.h).
+//
+// Host-side validation (synchronous; nothing launches on error), workspace
+// sizing and carving, launch heuristics (chunks / splits / cluster size from
+// the device's SM count), error strings.  No allocation, no synchronisation.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "../../include/sparsevila.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svl {
+
+static thread_local char g_err[512] = "";
+
+static svl_status fail(svl_status s, const char* fmt, const char* a = nullptr) {
+    snprintf(g_err, sizeof g_err, fmt, a ? a : "");
+    return s;
+}
+
+static svl_status cuda_fail(cudaError_t e, const char* where) {
+    snprintf(g_err, sizeof g_err, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+    return SVL_ERR_CUDA;
+}
+
+struct DevAttr {
+    int sms = 0, major = 0, minor = 0;
+};
+
+static DevAttr dev_attr() {
+    static DevAttr cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DevAttr{};
+    if (cache[dev].sms == 0) {
+        DevAttr a;
+        cudaDeviceGetAttribute(&a.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&a.major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&a.minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cache[dev] = a;
+    }
+    return cache[dev];
+}
+
+int device_sm_count() {
+    const int s = dev_attr().sms;
+    return s > 0 ? s : 148;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ retrieve
+struct ScorePlan {
+    int NT, NCP, C, rows_per_chunk;
+};
+
+// Chunks per unit: minimise the critical path ceil(units*C/SMs) * ceil(nv/C)
+// (persistent grid of SM-count CTAs), chunks of >= 64 rows.
+static ScorePlan plan_score(int units, int n_q, int g, int nv, int sms) {
+    ScorePlan pl;
+    pl.NT = (n_q * g + 7) / 8;
+    pl.NCP = pl.NT * 8;
+    long best = -1;
+    int bestC = 1;
+    const int cmax = std::max(1, std::min(4096, (nv + 63) / 64));
+    for (int C = 1; C <= cmax; ++C) {
+        const long rpc = ((nv + C - 1) / C + 15) / 16 * 16;
+        const int Ceff = (int)((nv + rpc - 1) / rpc);
+        if (Ceff != C) continue;
+        const long waves = ((long)units * C + sms - 1) / sms;
+        const long cost = waves * (rpc + 48);  // + per-item overhead in row units
+        if (best < 0 || cost < best) {
+            best = cost;
+            bestC = C;
+        }
+    }
+    pl.C = bestC;
+    pl.rows_per_chunk = ((nv + bestC - 1) / bestC + 15) / 16 * 16;
+    return pl;
+}
+
+struct RetrieveLayout {
+    size_t logits, part, total;
+};
+
+static RetrieveLayout retrieve_layout(int B, int Hkv, int nv, const ScorePlan& pl) {
+    RetrieveLayout l;
+    const size_t units = (size_t)B * Hkv;
+    l.logits = kWsHeader;
+    l.part = round_up(l.logits + units * nv * pl.NCP * sizeof(float), 256);
+    l.total = round_up(l.part + units * pl.C * pl.NCP * sizeof(float2), 256);
+    return l;
+}
+
+// --------------------------------------------------------------- decode plan
+static int plan_splits(int units, int n_att_max, int sms) {
+    int S = std::max(1, (n_att_max + kDecodeRowsMax - 1) / kDecodeRowsMax);
+    const int fill = (sms + units - 1) / units;  // at least one CTA per SM
+    S = std::max(S, fill);
+    S = std::min(S, std::max(1, n_att_max));
+    return S;
+}
+
+}  // namespace svl
+
+using namespace svl;
+
+extern "C" {
+
+const char* svl_version(void) { return "libsparsevila 0.1 sm_100a (tensor-core mma.sync swap-AB, cluster radix select)"; }
+
+const char* svl_status_string(svl_status s) {
+    switch (s) {
+        case SVL_OK: return "SVL_OK";
+        case SVL_ERR_INVALID_ARGUMENT: return "SVL_ERR_INVALID_ARGUMENT";
+        case SVL_ERR_SHAPE: return "SVL_ERR_SHAPE";
+        case SVL_ERR_ALIGNMENT: return "SVL_ERR_ALIGNMENT";
+        case SVL_ERR_WORKSPACE: return "SVL_ERR_WORKSPACE";
+        case SVL_ERR_UNSUPPORTED: return "SVL_ERR_UNSUPPORTED";
+        case SVL_ERR_CUDA: return "SVL_ERR_CUDA";
+    }
+    return "SVL_ERR_UNKNOWN";
+}
+
+const char* svl_last_error_message(void) { return g_err; }
+
+int64_t svl_keep_budget(int64_t n, double s) {
+    if (n < 0 || !(s >= 0.0 && s < 1.0)) return -1;
+    if (n == 0) return 0;
+    int64_t k = (int64_t)floor((double)n * (1.0 - s) + 0.5);
+    if (k < 1) k = 1;
+    if (k > n) k = n;
+    return k;
+}
+
+svl_status svl_workspace_init(void* ws, size_t bytes, void* stream) {
+    if (!ws) return fail(SVL_ERR_WORKSPACE, "workspace is NULL");
+    cudaError_t e = cudaMemsetAsync(ws, 0, bytes, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_workspace_init");
+    return SVL_OK;
+}
+
+svl_status svl_read_device_flags(void* ws, void* stream, uint32_t* flags) {
+    if (!ws || !flags) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaMemcpy(flags, ws, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_read_device_flags");
+    return SVL_OK;
+}
+
+svl_status svl_reset_device_flags(void* ws, void* stream) {
+    if (!ws) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL workspace");
+    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_reset_device_flags");
+    return SVL_OK;
+}
+
+static svl_status check_device() {
+    DevAttr a = dev_attr();
+    if (a.major != 10 || a.minor != 0)
+        return fail(SVL_ERR_UNSUPPORTED, "libsparsevila needs an sm_100 (B200) device%s");
+    return SVL_OK;
+}
+
+static svl_status check_kv(const svl_kv& kv, int B, int Hkv, int d, const char* name) {
+    if (!kv.data) return fail(SVL_ERR_INVALID_ARGUMENT, "%s.data is NULL", name);
+    if (!aligned16(kv.data)) return fail(SVL_ERR_ALIGNMENT, "%s.data not 16-byte aligned", name);
+    if ((kv.stride_t * 2) % 16 || (kv.stride_h * 2) % 16 || (kv.stride_b * 2) % 16)
+        return fail(SVL_ERR_ALIGNMENT, "%s strides must be multiples of 8 elements", name);
+    if (kv.stride_t < d || kv.capacity < 1)
+        return fail(SVL_ERR_SHAPE, "%s stride_t < d or capacity < 1", name);
+    (void)B;
+    (void)Hkv;
+    return SVL_OK;
+}
+
+size_t svl_retrieve_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                   int32_t visual_len, uint32_t flags) {
+    (void)d;
+    (void)flags;
+    if (B < 1 || n_q < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
+    const int g = H / Hkv;
+    ScorePlan pl = plan_score(B * Hkv, n_q, g, visual_len, device_sm_count());
+    return retrieve_layout(B, Hkv, visual_len, pl).total;
+}
+
+svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                        svl_kv K, svl_span span, const float* lse_in, int32_t k, float scale,
+                        uint32_t flags, int32_t* idx_out, float* scores_out, void* ws,
+                        size_t ws_bytes, void* stream) {
+    if (!q || !idx_out || !span.seq_len) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags & ~(SVL_NORM_VISUAL_ONLY | SVL_SELECT_SHARED | SVL_RETRIEVE_SCORE_ONLY |
+                  SVL_RETRIEVE_SELECT_ONLY))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if ((flags & SVL_RETRIEVE_SCORE_ONLY) && (flags & SVL_RETRIEVE_SELECT_ONLY))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "SCORE_ONLY and SELECT_ONLY are exclusive%s");
+    if (B < 1 || n_q < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, n_q, H, Hkv must be >= 1%s");
+    if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
+    if (span.visual_len < 1) return fail(SVL_ERR_SHAPE, "no visual rows to retrieve from%s");
+    if (span.visual_begin < 0 ||
+        (int64_t)span.visual_begin + span.visual_len + n_q > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span + query rows outside the KV capacity%s");
+    if (k < 0 || k > span.visual_len) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, visual_len]%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    const int g = H / Hkv;
+    if (n_q * g > 32) return fail(SVL_ERR_UNSUPPORTED, "n_q * g must be <= 32 in this version%s");
+    const int shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
+    if (shared && n_q * g * Hkv > 128) return fail(SVL_ERR_UNSUPPORTED, "SHARED needs n_q*H <= 128%s");
+    if (span.visual_len > 16 * kSelectThreads * kSelectMaxPerThread)
+        return fail(SVL_ERR_UNSUPPORTED, "visual_len > 131072%s");
+    if (!aligned16(q)) return fail(SVL_ERR_ALIGNMENT, "q not 16-byte aligned%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+
+    const int units = B * Hkv;
+    ScorePlan pl = plan_score(units, n_q, g, span.visual_len, device_sm_count());
+    RetrieveLayout lay = retrieve_layout(B, Hkv, span.visual_len, pl);
+    if (ws_bytes < lay.total) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    cudaStream_t s = (cudaStream_t)stream;
+
+    ScoreParams sp;
+    sp.q = static_cast<const uint16_t*>(q);
+    sp.K = static_cast<const uint16_t*>(K.data);
+    sp.sb = K.stride_b; sp.sh = K.stride_h; sp.st = K.stride_t;
+    sp.seq_len = span.seq_len;
+    sp.B = B; sp.n_q = n_q; sp.H = H; sp.Hkv = Hkv; sp.g = g;
+    sp.NC = n_q * g; sp.NCP = pl.NCP;
+    sp.vb = span.visual_begin; sp.nv = span.visual_len; sp.capacity = K.capacity;
+    sp.C = pl.C; sp.rows_per_chunk = pl.rows_per_chunk;
+    sp.need_partials = lse_in ? 0 : 1;
+    sp.use_text = (!lse_in && !(flags & SVL_NORM_VISUAL_ONLY)) ? 1 : 0;
+    sp.scale2 = scale * kLog2e;
+    sp.logits = reinterpret_cast<float*>(w + lay.logits);
+    sp.part = reinterpret_cast<float2*>(w + lay.part);
+    sp.flags = reinterpret_cast<uint32_t*>(w);
+    cudaError_t e = cudaSuccess;
+    if (!(flags & SVL_RETRIEVE_SELECT_ONLY)) {
+        e = launch_score(sp, d, pl.NT, s);
+        if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve/score");
+    }
+    if (flags & SVL_RETRIEVE_SCORE_ONLY) return SVL_OK;
+
+    SelectParams se = {};
+    se.mode = 0;
+    se.logits = sp.logits;
+    se.part = sp.part;
+    se.lse_in = lse_in;
+    se.C = pl.C; se.NC = sp.NC; se.NCP = pl.NCP; se.g = g; se.n_q = n_q; se.H = H; se.Hkv = Hkv;
+    se.shared = shared;
+    se.nv = span.visual_len; se.k = k;
+    se.idx_out = idx_out;
+    se.scores_out = scores_out;
+    se.flags = sp.flags;
+    se.CS = select_cluster_size(span.visual_len);
+    e = launch_select(se, shared ? B : units, s);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve/select");
+    return SVL_OK;
+}
+
+// ------------------------------------------------------------ sparse decode
+size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
+                                        int32_t visual_len, int32_t capacity, uint32_t flags) {
+    (void)flags;
+    if (B < 1 || Hkv < 1 || H % Hkv || capacity < 1) return 0;
+    const int units = B * Hkv, g = H / Hkv;
+    const int vb_max = capacity - visual_len;  // conservative: rows outside the visual span
+    const int n_att_max = std::max(1, k + std::max(0, vb_max));
+    const int S = plan_splits(units, n_att_max, device_sm_count());
+    return round_up(kWsHeader + (size_t)units * S * g * (d + 2) * sizeof(float), 256);
+}
+
+svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                  svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
+                                  int32_t k, uint32_t flags, float scale, float* out,
+                                  float* lse_out, void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !out || !span.seq_len || (k > 0 && !vis_idx))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags & ~(SVL_SELECT_SHARED)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
+    if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
+    if (span.visual_begin < 0 || span.visual_len < 0 ||
+        (int64_t)span.visual_begin + span.visual_len > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span outside the KV capacity%s");
+    if (K.capacity != V.capacity) return fail(SVL_ERR_SHAPE, "K and V capacities differ%s");
+    if (k < 0 || k > span.visual_len) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, visual_len]%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    const int g = H / Hkv;
+    if (g > 16) return fail(SVL_ERR_UNSUPPORTED, "g = H/Hkv must be <= 16 in this version%s");
+    if (!aligned16(q)) return fail(SVL_ERR_ALIGNMENT, "q not 16-byte aligned%s");
+    if (!aligned16(out)) return fail(SVL_ERR_ALIGNMENT, "out not 16-byte aligned%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st != SVL_OK) return st;
+    st = check_kv(V, B, Hkv, d, "V");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+
+    const int units = B * Hkv;
+    const int n_att_max = std::max(1, k + std::max(0, K.capacity - span.visual_len));
+    const int S = plan_splits(units, n_att_max, device_sm_count());
+    const size_t need = round_up(kWsHeader + (size_t)units * S * g * (d + 2) * sizeof(float), 256);
+    if (ws_bytes < need) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+
+    DecodeParams p;
+    p.q = static_cast<const uint16_t*>(q);
+    p.K = static_cast<const uint16_t*>(K.data);
+    p.ksb = K.stride_b; p.ksh = K.stride_h; p.kst = K.stride_t;
+    p.V = static_cast<const uint16_t*>(V.data);
+    p.vsb = V.stride_b; p.vsh = V.stride_h; p.vst = V.stride_t;
+    p.seq_len = span.seq_len;
+    p.idx = vis_idx;
+    p.B = B; p.H = H; p.Hkv = Hkv; p.g = g;
+    p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k;
+    p.shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
+    p.capacity = K.capacity;
+    p.S = S;
+    p.scale2 = scale * kLog2e;
+    p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kWsHeader);
+    p.out = out;
+    p.lse_out = lse_out;
+    p.flags = static_cast<uint32_t*>(ws);
+    cudaError_t e = launch_decode(p, d, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_sparse_decode_attn");
+    return SVL_OK;
+}
+
+// ---------------------------------------------------------------- prune
+size_t svl_prune_workspace_size(int32_t B, int32_t N, int32_t n_frames) {
+    (void)B;
+    (void)N;
+    (void)n_frames;
+    return kWsHeader;
+}
+
+svl_status svl_prefill_prune(const float* saliency, int32_t B, int32_t N,
+                             const int32_t* frame_offsets, int32_t n_frames,
+                             double prefill_sparsity, int32_t* kept_idx, int32_t kept_capacity,
+                             int32_t* kept_total, void* ws, size_t ws_bytes, void* stream) {
+    if (!saliency || !kept_idx || !kept_total) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (B < 1 || N < 1) return fail(SVL_ERR_SHAPE, "B and N must be >= 1%s");
+    if (!(prefill_sparsity >= 0.0 && prefill_sparsity < 1.0))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "prefill_sparsity outside [0, 1)%s");
+    const int nf = frame_offsets ? n_frames : 1;
+    if (nf < 1) return fail(SVL_ERR_SHAPE, "n_frames must be >= 1%s");
+    if (nf > kMaxFrames) return fail(SVL_ERR_UNSUPPORTED, "more than 2047 frames per call%s");
+    PruneTable tab;
+    int64_t total = 0;
+    int max_n = 0;
+    for (int f = 0; f < nf; ++f) {
+        const int o0 = frame_offsets ? frame_offsets[f] : 0;
+        const int o1 = frame_offsets ? frame_offsets[f + 1] : N;
+        if (o1 < o0 || o0 < 0 || o1 > N) return fail(SVL_ERR_SHAPE, "frame_offsets not ascending within [0, N]%s");
+        if (f == 0 && o0 != 0) return fail(SVL_ERR_SHAPE, "frame_offsets[0] must be 0%s");
+        if (f == nf - 1 && o1 != N) return fail(SVL_ERR_SHAPE, "frame_offsets[n_frames] must be N%s");
+        const int n = o1 - o0;
+        if (n > 16 * kSelectThreads * kSelectMaxPerThread)
+            return fail(SVL_ERR_UNSUPPORTED, "frame larger than 131072 tokens%s");
+        max_n = std::max(max_n, n);
+        tab.fr[f] = make_int2(o0, (int)total);
+        total += svl_keep_budget(n, prefill_sparsity);
+    }
+    tab.fr[nf] = make_int2(N, (int)total);
+    if (total > kept_capacity) return fail(SVL_ERR_INVALID_ARGUMENT, "kept_capacity < sum of frame budgets%s");
+    *kept_total = (int32_t)total;
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    if (ws_bytes < kWsHeader) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    if (!aligned16(saliency)) return fail(SVL_ERR_ALIGNMENT, "saliency not 16-byte aligned%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    SelectParams se = {};
+    se.mode = 1;
+    se.scores_in = saliency;
+    se.N = N;
+    se.nf = nf;
+    se.kept_cap = kept_capacity;
+    se.idx_out = kept_idx;
+    se.flags = static_cast<uint32_t*>(ws);
+    se.CS = select_cluster_size(max_n);
+    cudaError_t e = launch_prune_select(se, tab, B * nf, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_prefill_prune");
+    return SVL_OK;
+}
+
+// --------------------------------------------------------------- salience
+size_t svl_salience_workspace_size(int32_t F, int32_t S, int32_t N_f, int32_t H_e, int32_t d_e,
+                                   int32_t mode) {
+    (void)d_e;
+    if (F < 1 || N_f < 1 || H_e < 1) return 0;
+    const int rows = (mode == SVL_SAL_INTRA_VISUAL) ? N_f : S;
+    return round_up(kWsHeader + (size_t)F * H_e * std::max(rows, 1) * sizeof(float), 256) +
+           round_up((size_t)F * H_e * N_f * sizeof(float), 256);
+}
+
+svl_status svl_salience(const void* Qe, const void* Ke, int32_t F, int32_t S, int32_t N_f,
+                        int32_t H_e, int32_t d_e, int32_t mode, float scale, float* saliency,
+                        void* ws, size_t ws_bytes, void* stream) {
+    if (!Qe || !Ke || !saliency) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (F < 1 || N_f < 1 || H_e < 1 || S < 0) return fail(SVL_ERR_SHAPE, "bad F / N_f / H_e / S%s");
+    if ((mode == SVL_SAL_SUMMARY && S != 1) || (mode == SVL_SAL_MULTI_SUMMARY && S < 2) ||
+        (mode == SVL_SAL_INTRA_VISUAL && S != 0) || mode < 0 || mode > 2)
+        return fail(SVL_ERR_INVALID_ARGUMENT, "salience mode does not match the summary-token count%s");
+    if (d_e < 8 || d_e > 128 || d_e % 8) return fail(SVL_ERR_UNSUPPORTED, "d_e must be a multiple of 8 in [8, 128]%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (!aligned16(Qe) || !aligned16(Ke)) return fail(SVL_ERR_ALIGNMENT, "Qe/Ke not 16-byte aligned%s");
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    if (ws_bytes < svl_salience_workspace_size(F, S, N_f, H_e, d_e, mode))
+        return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    const int rows = (mode == SVL_SAL_INTRA_VISUAL) ? N_f : S;
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    SalienceParams p;
+    p.Qe = static_cast<const uint16_t*>(Qe);
+    p.Ke = static_cast<const uint16_t*>(Ke);
+    p.F = F; p.S = S; p.Nf = N_f; p.He = H_e; p.de = d_e; p.mode = mode;
+    p.scale2 = scale * kLog2e;
+    p.lse = reinterpret_cast<float*>(w + kWsHeader);
+    p.acc = reinterpret_cast<float*>(w + round_up(kWsHeader + (size_t)F * H_e * std::max(rows, 1) * sizeof(float), 256));
+    p.sal = saliency;
+    p.flags = reinterpret_cast<uint32_t*>(w);
+    cudaError_t e = launch_salience(p, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_salience");
+    return SVL_OK;
+}
+
+}  // extern "C"

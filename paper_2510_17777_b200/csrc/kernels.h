@@ -1,0 +1,97 @@
+// kernels.h -- internal launcher interface between the C-ABI host layer
+// (api.cu) and the kernels.  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace svl {
+
+// ---------------------------------------------------------------- retrieve
+struct ScoreParams {
+    const uint16_t* q;  // [B][n_q][H][d]
+    const uint16_t* K;  // KV view
+    int64_t sb, sh, st;
+    const int32_t* seq_len;
+    int B, n_q, H, Hkv, g, NC, NCP;  // NC = n_q*g columns, NCP = padded (8*NT)
+    int vb, nv, capacity;
+    int C;               // chunks per unit
+    int rows_per_chunk;  // visual rows per chunk (multiple of 16)
+    int use_text;        // normalise over text rows too (FULL_PREFIX and no lse_in)
+    int need_partials;   // 0 when lse_in supplies the normaliser
+    float scale2;        // scale * log2(e)
+    float* logits;       // [units][nv][NCP] base-2 logits
+    float2* part;        // [units][C][NCP] chunk (max, sum) in base 2
+    uint32_t* flags;
+};
+
+struct SelectParams {
+    int mode;  // 0 = retrieve (logits + LSE), 1 = prune (float scores)
+    // retrieve source
+    const float* logits;
+    const float2* part;
+    const float* lse_in;  // natural log [B][n_q][H] or null
+    int C, NC, NCP, g, n_q, H, Hkv, shared;
+    // prune source
+    const float* scores_in;
+    int N, nf, kept_cap;  // prune: per b, frames f in [0, nf) of the row [b*N, b*N+N)
+    // retrieve: uniform n = nv, k, out = u*k
+    int nv, k;
+    int32_t* idx_out;
+    float* scores_out;  // retrieve only, nullable
+    uint32_t* flags;
+    int CS;  // cluster size (CTAs per selection unit)
+};
+
+// Prune frame table, passed by value as a kernel parameter (no host->device
+// copy, no stream sync): fr[f] = (offset o_f, prefix sum of k over frames < f),
+// f in [0, nf]; k_f = fr[f+1].y - fr[f].y.
+constexpr int kMaxFrames = 2047;
+struct PruneTable {
+    int2 fr[kMaxFrames + 1];
+};
+
+struct DecodeParams {
+    const uint16_t* q;  // [B][H][d]
+    const uint16_t* K;
+    int64_t ksb, ksh, kst;
+    const uint16_t* V;
+    int64_t vsb, vsh, vst;
+    const int32_t* seq_len;
+    const int32_t* idx;  // [B][U][k]
+    int B, H, Hkv, g, vb, nv, k, shared, capacity;
+    int S;         // splits per unit
+    float scale2;  // scale * log2(e)
+    float* part;   // [units][S][g][d+2] : o (unnormalised), m (base 2), l
+    float* out;    // [B][H][d]
+    float* lse_out;
+    uint32_t* flags;
+};
+
+struct SalienceParams {
+    const uint16_t* Qe;
+    const uint16_t* Ke;
+    int F, S, Nf, He, de, mode;
+    float scale2;
+    float* lse;  // [F][He][rows] base-2 row LSE (pass 1)
+    float* sal;  // [F][Nf]
+    float* acc;  // [F][He][Nf] per-head column sums (pass 2) -- fp32
+    uint32_t* flags;
+};
+
+constexpr int kScoreThreads = 512;
+constexpr int kSelectThreads = 512;
+constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA
+constexpr int kDecodeThreads = 128;
+constexpr int kDecodeRowsMax = 128;  // rows staged per decode CTA
+
+cudaError_t launch_score(const ScoreParams& p, int d, int NT, cudaStream_t s);
+cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s);
+cudaError_t launch_prune_select(const SelectParams& p, const PruneTable& tab, int n_units, cudaStream_t s);
+cudaError_t launch_decode(const DecodeParams& p, int d, cudaStream_t s);
+cudaError_t launch_salience(const SalienceParams& p, cudaStream_t s);
+
+int device_sm_count();
+int select_cluster_size(int n);  // CTAs per selection unit for n keys
+
+}  // namespace svl

@@ -1,0 +1,290 @@
+"""Thin ctypes binding of libsparsevila.so (include/sparsevila.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI.  Tensors are torch CUDA tensors (PyTorch provides
+device memory and streams).  There is no CPU fallback: if the library is
+missing or a tensor is not on a CUDA device, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Optional
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsparsevila.so")
+
+SVL_OK = 0
+SVL_NORM_VISUAL_ONLY = 1
+SVL_SELECT_SHARED = 2
+SVL_RETRIEVE_SCORE_ONLY = 0x100
+SVL_RETRIEVE_SELECT_ONLY = 0x200
+SVL_SAL_SUMMARY, SVL_SAL_MULTI_SUMMARY, SVL_SAL_INTRA_VISUAL = 0, 1, 2
+SVL_DEVFLAG_INDEX, SVL_DEVFLAG_NONFINITE, SVL_DEVFLAG_SPAN = 1, 2, 4
+
+STATUS = {0: "SVL_OK", 1: "SVL_ERR_INVALID_ARGUMENT", 2: "SVL_ERR_SHAPE", 3: "SVL_ERR_ALIGNMENT",
+          4: "SVL_ERR_WORKSPACE", 5: "SVL_ERR_UNSUPPORTED", 6: "SVL_ERR_CUDA"}
+
+EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_attn",
+           "svl_sparse_decode_workspace_size", "svl_prefill_prune", "svl_prune_workspace_size",
+           "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
+           "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
+           "svl_reset_device_flags", "svl_version"]
+
+
+class SvlError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class svl_kv(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("stride_b", ctypes.c_int64),
+                ("stride_h", ctypes.c_int64), ("stride_t", ctypes.c_int64),
+                ("capacity", ctypes.c_int32)]
+
+
+class svl_span(ctypes.Structure):
+    _fields_ = [("visual_begin", ctypes.c_int32), ("visual_len", ctypes.c_int32),
+                ("seq_len", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsparsevila.so (fails loudly; no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2510_17777_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, F, D, U32, SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                      ctypes.c_float, ctypes.c_double, ctypes.c_uint32,
+                                      ctypes.c_size_t)
+        L.svl_retrieve.restype = ctypes.c_int
+        L.svl_retrieve.argtypes = [P, I32, I32, I32, I32, I32, svl_kv, svl_span, P, I32, F, U32,
+                                   P, P, P, SZ, P]
+        L.svl_retrieve_workspace_size.restype = SZ
+        L.svl_retrieve_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, U32]
+        L.svl_sparse_decode_attn.restype = ctypes.c_int
+        L.svl_sparse_decode_attn.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, P,
+                                             I32, U32, F, P, P, P, SZ, P]
+        L.svl_sparse_decode_workspace_size.restype = SZ
+        L.svl_sparse_decode_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, I32, U32]
+        L.svl_prefill_prune.restype = ctypes.c_int
+        L.svl_prefill_prune.argtypes = [P, I32, I32, P, I32, D, P, I32, P, P, SZ, P]
+        L.svl_prune_workspace_size.restype = SZ
+        L.svl_prune_workspace_size.argtypes = [I32, I32, I32]
+        L.svl_salience.restype = ctypes.c_int
+        L.svl_salience.argtypes = [P, P, I32, I32, I32, I32, I32, I32, F, P, P, SZ, P]
+        L.svl_salience_workspace_size.restype = SZ
+        L.svl_salience_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32]
+        L.svl_keep_budget.restype = I64
+        L.svl_keep_budget.argtypes = [I64, D]
+        L.svl_workspace_init.restype = ctypes.c_int
+        L.svl_workspace_init.argtypes = [P, SZ, P]
+        L.svl_status_string.restype = ctypes.c_char_p
+        L.svl_status_string.argtypes = [ctypes.c_int]
+        L.svl_last_error_message.restype = ctypes.c_char_p
+        L.svl_last_error_message.argtypes = []
+        L.svl_read_device_flags.restype = ctypes.c_int
+        L.svl_read_device_flags.argtypes = [P, P, P]
+        L.svl_reset_device_flags.restype = ctypes.c_int
+        L.svl_reset_device_flags.argtypes = [P, P]
+        L.svl_version.restype = ctypes.c_char_p
+        L.svl_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != SVL_OK:
+        raise SvlError(rc, lib().svl_last_error_message().decode())
+
+
+def _cuda(t: torch.Tensor, name: str, dtype=None) -> int:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def kv_view(t: torch.Tensor, name: str = "K") -> svl_kv:
+    """[B][Hkv][cap][d] bf16 CUDA tensor (last dim contiguous) -> svl_kv."""
+    _cuda(t, name, torch.bfloat16)
+    if t.dim() != 4 or t.stride(3) != 1:
+        raise ValueError(f"{name} must be [B][Hkv][cap][d] with a contiguous last dim")
+    return svl_kv(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2), t.shape[2])
+
+
+def span(visual_begin: int, visual_len: int, seq_len: torch.Tensor) -> svl_span:
+    _cuda(seq_len, "seq_len", torch.int32)
+    return svl_span(visual_begin, visual_len, seq_len.data_ptr())
+
+
+class Workspace:
+    """A zero-initialised device workspace (grown on demand)."""
+
+    def __init__(self, device=None):
+        self.buf: Optional[torch.Tensor] = None
+        self.device = device
+
+    def get(self, nbytes: int, stream=None) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device or "cuda")
+        return self.buf
+
+    def flags(self, stream=None) -> int:
+        out = ctypes.c_uint32(0)
+        _check(lib().svl_read_device_flags(ctypes.c_void_p(self.buf.data_ptr()),
+                                           ctypes.c_void_p(_stream(stream)), ctypes.byref(out)))
+        return out.value
+
+    def reset_flags(self, stream=None):
+        _check(lib().svl_reset_device_flags(ctypes.c_void_p(self.buf.data_ptr()),
+                                            ctypes.c_void_p(_stream(stream))))
+
+
+_default_ws = {}
+
+
+def _ws(ws: Optional[Workspace], device) -> Workspace:
+    if ws is not None:
+        return ws
+    key = str(device)
+    if key not in _default_ws:
+        _default_ws[key] = Workspace(device)
+    return _default_ws[key]
+
+
+def keep_budget(n: int, s: float) -> int:
+    return int(lib().svl_keep_budget(n, s))
+
+
+def retrieve_workspace_size(B, n_q, H, Hkv, d, visual_len, flags=0) -> int:
+    return int(lib().svl_retrieve_workspace_size(B, n_q, H, Hkv, d, visual_len, flags))
+
+
+def sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags=0) -> int:
+    return int(lib().svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags))
+
+
+def retrieve(q: torch.Tensor, K: torch.Tensor, seq_len: torch.Tensor, visual_begin: int,
+             visual_len: int, k: int, scale: Optional[float] = None, flags: int = 0,
+             lse_in: Optional[torch.Tensor] = None, idx_out: Optional[torch.Tensor] = None,
+             scores_out: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None,
+             stream=None) -> torch.Tensor:
+    """svl_retrieve.  q bf16 [B][n_q][H][d]; K bf16 [B][Hkv][cap][d]; returns
+    int32 [B][U][k] ascending visual indices (U = Hkv, or 1 with SHARED)."""
+    B, n_q, H, d = q.shape
+    Hkv = K.shape[1]
+    U = 1 if flags & SVL_SELECT_SHARED else Hkv
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous")
+    if idx_out is None:
+        idx_out = torch.empty(B, U, max(k, 0), dtype=torch.int32, device=q.device)
+    wsz = retrieve_workspace_size(B, n_q, H, Hkv, d, visual_len, flags)
+    w = _ws(ws, q.device).get(wsz)
+    _check(lib().svl_retrieve(
+        q.data_ptr(), B, n_q, H, Hkv, d, kv_view(K), span(visual_begin, visual_len, seq_len),
+        _cuda(lse_in, "lse_in", torch.float32) if lse_in is not None else None, k, scale, flags,
+        _cuda(idx_out, "idx_out", torch.int32),
+        _cuda(scores_out, "scores_out", torch.float32) if scores_out is not None else None,
+        w.data_ptr(), w.numel(), _stream(stream)))
+    return idx_out
+
+
+def sparse_decode_attn(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor,
+                       visual_begin: int, visual_len: int, vis_idx: Optional[torch.Tensor],
+                       scale: Optional[float] = None, flags: int = 0,
+                       out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None,
+                       ws: Optional[Workspace] = None, stream=None):
+    """svl_sparse_decode_attn.  q bf16 [B][H][d]; vis_idx int32 [B][U][k].
+    Returns (out fp32 [B][H][d], lse fp32 [B][H] or None)."""
+    B, H, d = q.shape
+    Hkv = K.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous")
+    k = 0 if vis_idx is None else vis_idx.shape[-1]
+    if out is None:
+        out = torch.empty(B, H, d, dtype=torch.float32, device=q.device)
+    wsz = sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, K.shape[2], flags)
+    w = _ws(ws, q.device).get(wsz)
+    _check(lib().svl_sparse_decode_attn(
+        q.data_ptr(), B, H, Hkv, d, kv_view(K, "K"), kv_view(V, "V"),
+        span(visual_begin, visual_len, seq_len),
+        _cuda(vis_idx, "vis_idx", torch.int32) if vis_idx is not None else None, k, flags, scale,
+        _cuda(out, "out", torch.float32),
+        _cuda(lse_out, "lse_out", torch.float32) if lse_out is not None else None,
+        w.data_ptr(), w.numel(), _stream(stream)))
+    return out, lse_out
+
+
+def prefill_prune(saliency: torch.Tensor, prefill_sparsity: float, frame_offsets=None,
+                  kept_idx: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None,
+                  stream=None):
+    """svl_prefill_prune.  saliency fp32 [B][N] (CUDA); frame_offsets: host
+    sequence of n_frames+1 ints or None.  Returns (kept int32 [B][total], total)."""
+    _cuda(saliency, "saliency", torch.float32)
+    B, N = saliency.shape
+    if frame_offsets is not None:
+        fo = (ctypes.c_int32 * len(frame_offsets))(*[int(x) for x in frame_offsets])
+        nf = len(frame_offsets) - 1
+        cap = sum(max(keep_budget(int(frame_offsets[i + 1]) - int(frame_offsets[i]),
+                                  prefill_sparsity), 0) for i in range(nf))
+    else:
+        fo, nf = None, 1
+        cap = keep_budget(N, prefill_sparsity)
+    cap = max(cap, 1)
+    if kept_idx is None:
+        kept_idx = torch.empty(B, cap, dtype=torch.int32, device=saliency.device)
+    total = ctypes.c_int32(0)
+    w = _ws(ws, saliency.device).get(lib().svl_prune_workspace_size(B, N, nf))
+    _check(lib().svl_prefill_prune(
+        saliency.data_ptr(), B, N, ctypes.cast(fo, ctypes.c_void_p) if fo is not None else None,
+        nf, float(prefill_sparsity), _cuda(kept_idx, "kept_idx", torch.int32), kept_idx.shape[1],
+        ctypes.addressof(total), w.data_ptr(), w.numel(), _stream(stream)))
+    return kept_idx[:, :total.value], total.value
+
+
+def salience(Qe: torch.Tensor, Ke: torch.Tensor, S: int, mode: int,
+             scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+             ws: Optional[Workspace] = None, stream=None) -> torch.Tensor:
+    """svl_salience.  Qe, Ke bf16 [F][S+N_f][H_e][d_e] -> fp32 [F][N_f]."""
+    _cuda(Qe, "Qe", torch.bfloat16)
+    _cuda(Ke, "Ke", torch.bfloat16)
+    if not (Qe.is_contiguous() and Ke.is_contiguous()):
+        raise ValueError("Qe, Ke must be contiguous")
+    F, T, He, de = Qe.shape
+    Nf = T - S
+    if scale is None:
+        scale = 1.0 / math.sqrt(de)
+    if out is None:
+        out = torch.empty(F, Nf, dtype=torch.float32, device=Qe.device)
+    w = _ws(ws, Qe.device).get(lib().svl_salience_workspace_size(F, S, Nf, He, de, mode))
+    _check(lib().svl_salience(Qe.data_ptr(), Ke.data_ptr(), F, S, Nf, He, de, mode, scale,
+                              _cuda(out, "out", torch.float32), w.data_ptr(), w.numel(),
+                              _stream(stream)))
+    return out
+
+
+def version() -> str:
+    return lib().svl_version().decode()
