@@ -102,6 +102,7 @@ static int plan_splits(int units, int n_att_max, int sms) {
     const int fill = (sms + units - 1) / units;  // at least one CTA per SM
     S = std::max(S, fill);
     S = std::min(S, std::max(1, n_att_max));
+    S = std::min(S, kMergeMaxSplits);
     return S;
 }
 
@@ -192,7 +193,8 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
                         svl_kv K, svl_span span, const float* lse_in, int32_t k, float scale,
                         uint32_t flags, int32_t* idx_out, float* scores_out, void* ws,
                         size_t ws_bytes, void* stream) {
-    if (!q || !idx_out || !span.seq_len) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (!q || (!idx_out && k > 0) || !span.seq_len)
+        return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
     if (flags & ~(SVL_NORM_VISUAL_ONLY | SVL_SELECT_SHARED | SVL_RETRIEVE_SCORE_ONLY |
                   SVL_RETRIEVE_SELECT_ONLY))
         return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
@@ -308,6 +310,8 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
 
     const int units = B * Hkv;
     const int n_att_max = std::max(1, k + std::max(0, K.capacity - span.visual_len));
+    if (n_att_max > kMergeMaxSplits * kDecodeRowsMax)
+        return fail(SVL_ERR_UNSUPPORTED, "more than 131072 attended rows per (b, KV head)%s");
     const int S = plan_splits(units, n_att_max, device_sm_count());
     const size_t need = round_up(kWsHeader + (size_t)units * S * g * (d + 2) * sizeof(float), 256);
     if (ws_bytes < need) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");

@@ -281,18 +281,32 @@ __global__ void __launch_bounds__(D / 2) merge_kernel(const DecodeParams p) {
     const int dd = threadIdx.x * 2;
     const float* base = p.part + (int64_t)u * p.S * p.g * (D + 2);
     const int stride = p.g * (D + 2);
-    float M = -INFINITY;
-    for (int s = 0; s < p.S; ++s) M = fmaxf(M, base[s * stride + p.g * D + h]);
+    // split weights: all (m_s, l_s) loads issued in parallel, then reduced in
+    // a fixed order (deterministic)
+    __shared__ float sw[kMergeMaxSplits], sl[kMergeMaxSplits];
+    __shared__ float sM;
+    for (int s = threadIdx.x; s < p.S; s += blockDim.x) {
+        sw[s] = base[s * stride + p.g * D + h];
+        sl[s] = base[s * stride + p.g * D + p.g + h];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY;
+        for (int s = 0; s < p.S; ++s) M = fmaxf(M, sw[s]);
+        sM = M;
+    }
+    __syncthreads();
+    const float M = sM;
+    for (int s = threadIdx.x; s < p.S; s += blockDim.x)
+        sw[s] = (M == -INFINITY) ? 0.f : exp2f(sw[s] - M);
+    __syncthreads();
     float o0 = 0.f, o1 = 0.f, l = 0.f;
-    if (M != -INFINITY) {
-        for (int s = 0; s < p.S; ++s) {
-            const float* ps = base + s * stride;
-            const float w = exp2f(ps[p.g * D + h] - M);
-            const float2 ov = *reinterpret_cast<const float2*>(ps + h * D + dd);
-            o0 += w * ov.x;
-            o1 += w * ov.y;
-            l += w * ps[p.g * D + p.g + h];
-        }
+#pragma unroll 8
+    for (int s = 0; s < p.S; ++s) {
+        const float2 ov = *reinterpret_cast<const float2*>(base + s * stride + h * D + dd);
+        o0 += sw[s] * ov.x;
+        o1 += sw[s] * ov.y;
+        l += sw[s] * sl[s];
     }
     const int hh = G * p.g + h;
     const float inv = (l > 0.f) ? 1.f / l : 0.f;
@@ -310,6 +324,8 @@ cudaError_t launch_decode_t(const DecodeParams& p, cudaStream_t s) {
     if (dev < 64 && !attr_done[dev]) {
         cudaError_t e = cudaFuncSetAttribute(decode_kernel<D>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+        if (e == cudaSuccess) e = set_max_carveout(decode_kernel<D>);
+        if (e == cudaSuccess) e = set_max_carveout(merge_kernel<D>);
         if (e != cudaSuccess) return e;
         attr_done[dev] = true;
     }

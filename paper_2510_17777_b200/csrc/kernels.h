@@ -84,6 +84,7 @@ constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA
 constexpr int kDecodeThreads = 128;
 constexpr int kDecodeRowsMax = 128;  // rows staged per decode CTA
+constexpr int kMergeMaxSplits = 1024;  // => <= 131072 attended rows per unit
 
 cudaError_t launch_score(const ScoreParams& p, int d, int NT, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s);
@@ -92,6 +93,13 @@ cudaError_t launch_decode(const DecodeParams& p, int d, cudaStream_t s);
 cudaError_t launch_salience(const SalienceParams& p, cudaStream_t s);
 
 int device_sm_count();
+
+// All kernels request the maximum shared-memory carveout so that consecutive
+// launches in a graph never force an L1/shared reconfiguration of the SMs.
+template <typename K>
+inline cudaError_t set_max_carveout(K kern) {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
 int select_cluster_size(int n);  // CTAs per selection unit for n keys
 
 }  // namespace svl

@@ -229,6 +229,12 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const ScorePara
 
 template <int D, int NT>
 cudaError_t launch_score_t(const ScoreParams& p, cudaStream_t s) {
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev]) {
+        attr_done[dev] = true;  // default carveout: this kernel keeps L1 for its register spills
+    }
     const int n_items = p.B * p.Hkv * p.C;
     const int grid = n_items < device_sm_count() ? n_items : device_sm_count();
     score_kernel<D, NT><<<grid, kScoreThreads, 0, s>>>(p);

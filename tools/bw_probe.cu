@@ -1,0 +1,141 @@
+// bw_probe.cu -- how much HBM bandwidth can N SMs pull?  (design probe for the
+// fused cluster retrieve kernel; not part of the library)
+//   mode 0: cp.async.bulk (TMA 1-D) into a smem ring, STAGES x CHUNK bytes in flight
+//   mode 1: ld.global.nc.v4 with 8 loads in flight per thread, 512 threads
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int STAGES, int CHUNK>
+__global__ void __launch_bounds__(128, 1) bulk_kernel(const uint8_t* src, size_t per_cta, unsigned long long* sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t full[STAGES];
+    const uint8_t* base = src + (size_t)blockIdx.x * per_cta;
+    const int n = (int)(per_cta / CHUNK);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s)
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    unsigned long long acc = 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n + STAGES; ++i) {
+            if (i >= STAGES) {  // wait for chunk i-STAGES
+                const int s = (i - STAGES) % STAGES;
+                const uint32_t ph = ((i - STAGES) / STAGES) & 1;
+                asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n@!p bra W;\n}" ::"r"(smem_u32(&full[s])), "r"(ph));
+                acc += sm[s * CHUNK + (i & 63)];
+            }
+            if (i < n) {
+                const int s = i % STAGES;
+                asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(CHUNK));
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(smem_u32(sm + s * CHUNK)), "l"(base + (size_t)i * CHUNK), "r"(CHUNK), "r"(smem_u32(&full[s])) : "memory");
+            }
+        }
+        if (acc == 0xdeadbeef) *sink = acc;
+    }
+}
+
+__global__ void __launch_bounds__(512, 1) ldg_kernel(const uint4* src, size_t per_cta16, unsigned long long* sink) {
+    const uint4* base = src + (size_t)blockIdx.x * per_cta16;
+    uint32_t acc = 0;
+    for (size_t i = threadIdx.x; i < per_cta16; i += 512 * 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            size_t j = i + u * 512;
+            if (j < per_cta16) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(base + j));
+            else v[u] = make_uint4(0,0,0,0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc ^= v[u].x ^ v[u].w;
+    }
+    if (acc == 0xdeadbeef) *sink = acc;
+}
+
+
+__global__ void empty_kernel() {}
+
+int main() {
+    const size_t total = 2ull << 30;
+    uint8_t* buf; cudaMalloc(&buf, total);
+    cudaMemset(buf, 1, total);
+    unsigned long long* sink; cudaMalloc(&sink, 8);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaFuncSetAttribute(bulk_kernel<6, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768);
+    cudaStream_t st; cudaStreamCreate(&st);
+    // empty kernel latency (events around one launch)
+    {
+        float best = 1e9;
+        for (int r = 0; r < 50; ++r) {
+            cudaEventRecord(a, st); empty_kernel<<<148, 128, 0, st>>>(); cudaEventRecord(b, st);
+            cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); if (r > 5 && ms < best) best = ms;
+        }
+        printf("empty kernel (events): %.2f us\n", best * 1e3);
+    }
+    size_t sizes[] = {8ull << 20, 32ull << 20, 128ull << 20, 512ull << 20};
+    for (size_t bytes : sizes) {
+        for (int mode = 0; mode < 2; ++mode) {
+            const int nsm = 148;
+            const size_t per = (bytes / nsm) / 32768 * 32768;
+            float best = 1e9;
+            for (int rep = 0; rep < 20; ++rep) {
+                const uint8_t* src = buf + ((size_t)rep * bytes) % (total - bytes);
+                cudaEventRecord(a, st);
+                if (mode == 0) bulk_kernel<6, 32768><<<nsm, 128, 6 * 32768, st>>>(src, per, sink);
+                else ldg_kernel<<<nsm, 512, 0, st>>>((const uint4*)src, per / 16, sink);
+                cudaEventRecord(b, st);
+                cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b);
+                if (rep > 2 && ms < best) best = ms;
+            }
+            printf("%s 148 SMs %4zu MiB: %7.1f GB/s (%.2f us)\n", mode == 0 ? "bulk" : "ldg ",
+                   bytes >> 20, per * nsm / (best * 1e-3) / 1e9, best * 1e3);
+        }
+    }
+    // graph of 28 back-to-back 32 MiB launches on distinct regions (like the bench)
+    int nsms[] = {32, 48, 64, 96, 128, 148};
+    for (int mode = 0; mode < 2; ++mode) for (int nsm : nsms) {
+        const size_t bytes = 32ull << 20;
+        const size_t per = (bytes / nsm) / 32768 * 32768;
+        cudaGraph_t g; cudaGraphExec_t ge;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+        for (int l = 0; l < 28; ++l) {
+            const uint8_t* src = buf + (size_t)l * (bytes + (1 << 20));
+            if (mode == 0) bulk_kernel<6, 32768><<<nsm, 128, 6 * 32768, st>>>(src, per, sink);
+            else ldg_kernel<<<nsm, 512, 0, st>>>((const uint4*)src, per / 16, sink);
+        }
+        cudaStreamEndCapture(st, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+        for (int w = 0; w < 3; ++w) cudaGraphLaunch(ge, st);
+        cudaEventRecord(a, st);
+        for (int r = 0; r < 20; ++r) cudaGraphLaunch(ge, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        const double us = ms * 1e3 / (20 * 28);
+        printf("graph 28x32MiB %s SMs %3d: %.2f us per launch, %.1f GB/s\n", mode == 0 ? "bulk" : "ldg ", nsm, us, per * nsm / (us * 1e-6) / 1e9);
+    }
+    // empty kernels in a graph: per-launch floor
+    {
+        cudaGraph_t g; cudaGraphExec_t ge;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+        for (int l = 0; l < 28; ++l) empty_kernel<<<148, 128, 0, st>>>();
+        cudaStreamEndCapture(st, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+        for (int w = 0; w < 3; ++w) cudaGraphLaunch(ge, st);
+        cudaEventRecord(a, st);
+        for (int r = 0; r < 50; ++r) cudaGraphLaunch(ge, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        printf("graph 28 empty kernels: %.2f us per launch\n", ms * 1e3 / (50 * 28));
+    }
+    // one kernel streaming 28 x 32 MiB (persistent), to see the asymptote
+    printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
