@@ -155,6 +155,34 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
 size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                         int32_t visual_len, int32_t capacity, uint32_t flags);
 
+/* ------------------------------------------------ fused fresh decode step */
+/*
+ * svl_fresh_decode_step -- svl_retrieve (n_q = 1) followed by
+ * svl_sparse_decode_attn with the SAME query, fused: the decode step that
+ * re-retrieves its visual tokens.  Because the retrieval
+ * logits s = scale*q.K_j are exactly the decode logits, K is read from HBM
+ * once: one thread-block cluster per (b, KV group) streams K with TMA bulk
+ * copies, keeps the logits on chip, selects the top-k over DSMEM and attends
+ * over [text rows] U [kept visual rows] (see fused.cu).  Results equal
+ * svl_retrieve + svl_sparse_decode_attn up to fp32 rounding of the LSE.
+ *
+ * q        device bf16 [B][H][d] contiguous (the current token, post-RoPE).
+ * flags    SVL_NORM_VISUAL_ONLY or 0 (SVL_SELECT_SHARED -> UNSUPPORTED).
+ * idx_out  device int32 [B][Hkv][k]: the kept visual indices (reusable by
+ *          later svl_sparse_decode_attn steady steps).
+ * out      device fp32 [B][H][d]; lse_out device fp32 [B][H] or NULL.
+ * Shapes outside the fused kernel's on-chip budget (visual_len > 32768 with
+ * g <= 8, > 16384 with 8 < g <= 16, or more than 4096 text rows) run the two
+ * separate calls instead (same kernels as svl_retrieve / svl_sparse_decode_attn).
+ */
+svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                 svl_kv K, svl_kv V, svl_span span, int32_t k, float scale,
+                                 uint32_t flags, int32_t* idx_out, float* out, float* lse_out,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
+                                       int32_t visual_len, int32_t capacity, uint32_t flags);
+
 /* ----------------------------------------------------- prefill companion */
 /*
  * svl_prefill_prune -- query-agnostic per-frame pruning (PAPER.md:113,

@@ -339,6 +339,96 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
     return SVL_OK;
 }
 
+// ----------------------------------------------------- fused fresh step
+// Cluster size and eligibility of the fused kernel for a shape.
+static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice) {
+    if (g > 16) return false;
+    const int smax = kFusedSliceMax / ((g + 7) / 8);
+    int cmin = (nv + smax - 1) / smax;
+    if (cmin > 16) return false;
+    const int units = B * Hkv;
+    int c = 1;
+    while (c < cmin) c <<= 1;
+    // many SMs per unit while the units are few (HBM streaming is per-SM bound)
+    const int want = (units * 16 <= 2 * device_sm_count()) ? 16 : 8;
+    CS = std::max(c, want);
+    slice = (nv + CS - 1) / CS;
+    if (slice > smax) return false;
+    const int tmax = std::max(0, capacity - nv);  // every non-visual row could be text
+    if ((tmax + CS - 1) / CS > kFusedTextMax) return false;
+    return true;
+}
+
+size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
+                                       int32_t visual_len, int32_t capacity, uint32_t flags) {
+    if (B < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
+    int CS, slice;
+    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice)) return kWsHeader;
+    return std::max(svl_retrieve_workspace_size(B, 1, H, Hkv, d, visual_len, flags),
+                    svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags));
+}
+
+svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                 svl_kv K, svl_kv V, svl_span span, int32_t k, float scale,
+                                 uint32_t flags, int32_t* idx_out, float* out, float* lse_out,
+                                 void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !out || !span.seq_len || (k > 0 && !idx_out))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags & ~SVL_NORM_VISUAL_ONLY)
+        return fail((flags & SVL_SELECT_SHARED) ? SVL_ERR_UNSUPPORTED : SVL_ERR_INVALID_ARGUMENT,
+                    "svl_fresh_decode_step accepts only SVL_NORM_VISUAL_ONLY%s");
+    if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
+    if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
+    if (span.visual_len < 1) return fail(SVL_ERR_SHAPE, "no visual rows to retrieve from%s");
+    if (span.visual_begin < 0 || (int64_t)span.visual_begin + span.visual_len + 1 > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span + current token outside the KV capacity%s");
+    if (K.capacity != V.capacity) return fail(SVL_ERR_SHAPE, "K and V capacities differ%s");
+    if (k < 0 || k > span.visual_len) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, visual_len]%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    const int g = H / Hkv;
+    if (g > 16) return fail(SVL_ERR_UNSUPPORTED, "g = H/Hkv must be <= 16 in this version%s");
+    if (!aligned16(q) || !aligned16(out)) return fail(SVL_ERR_ALIGNMENT, "q / out not 16-byte aligned%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st != SVL_OK) return st;
+    st = check_kv(V, B, Hkv, d, "V");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    if (ws_bytes < svl_fresh_decode_workspace_size(B, H, Hkv, d, k, span.visual_len, K.capacity, flags))
+        return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+
+    int CS, slice;
+    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice)) {
+        // outside the on-chip budget: the two separate calls (same q as [B][1][H][d])
+        st = svl_retrieve(q, B, 1, H, Hkv, d, K, span, nullptr, k, scale, flags, idx_out, nullptr,
+                          ws, ws_bytes, stream);
+        if (st != SVL_OK) return st;
+        return svl_sparse_decode_attn(q, B, H, Hkv, d, K, V, span, idx_out, k, 0u, scale, out,
+                                      lse_out, ws, ws_bytes, stream);
+    }
+    FreshParams p;
+    p.q = static_cast<const uint16_t*>(q);
+    p.K = static_cast<const uint16_t*>(K.data);
+    p.ksb = K.stride_b; p.ksh = K.stride_h; p.kst = K.stride_t;
+    p.V = static_cast<const uint16_t*>(V.data);
+    p.vsb = V.stride_b; p.vsh = V.stride_h; p.vst = V.stride_t;
+    p.seq_len = span.seq_len;
+    p.B = B; p.H = H; p.Hkv = Hkv; p.g = g;
+    p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k; p.capacity = K.capacity;
+    p.slice = slice;
+    p.flags_in = flags;
+    p.scale2 = scale * kLog2e;
+    p.idx_out = idx_out;
+    p.out = out;
+    p.lse_out = lse_out;
+    p.flags = static_cast<uint32_t*>(ws);
+    cudaError_t e = launch_fresh(p, d, CS, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_fresh_decode_step");
+    return SVL_OK;
+}
+
 // ---------------------------------------------------------------- prune
 size_t svl_prune_workspace_size(int32_t B, int32_t N, int32_t n_frames) {
     (void)B;

@@ -68,6 +68,27 @@ struct DecodeParams {
     uint32_t* flags;
 };
 
+struct FreshParams {
+    const uint16_t* q;  // [B][H][d] -- retrieval query == decode query
+    const uint16_t* K;
+    int64_t ksb, ksh, kst;
+    const uint16_t* V;
+    int64_t vsb, vsh, vst;
+    const int32_t* seq_len;
+    int B, H, Hkv, g, vb, nv, k, capacity;
+    int slice;          // visual rows per CTA of a unit's cluster
+    uint32_t flags_in;  // SVL_NORM_VISUAL_ONLY
+    float scale2;
+    int32_t* idx_out;  // [B][Hkv][k]
+    float* out;        // [B][H][d]
+    float* lse_out;    // [B][H] or null
+    uint32_t* flags;
+};
+constexpr int kFusedThreads = 288;    // 8 consumer warps + 1 TMA producer warp
+constexpr int kFusedTextMax = 256;    // text rows per CTA
+constexpr int kFusedSliceMax = 2048;  // visual rows per CTA (halved for g > 8)
+cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
+
 struct SalienceParams {
     const uint16_t* Qe;
     const uint16_t* Ke;

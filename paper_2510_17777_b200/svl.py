@@ -29,7 +29,8 @@ STATUS = {0: "SVL_OK", 1: "SVL_ERR_INVALID_ARGUMENT", 2: "SVL_ERR_SHAPE", 3: "SV
           4: "SVL_ERR_WORKSPACE", 5: "SVL_ERR_UNSUPPORTED", 6: "SVL_ERR_CUDA"}
 
 EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_attn",
-           "svl_sparse_decode_workspace_size", "svl_prefill_prune", "svl_prune_workspace_size",
+           "svl_sparse_decode_workspace_size", "svl_fresh_decode_step",
+           "svl_fresh_decode_workspace_size", "svl_prefill_prune", "svl_prune_workspace_size",
            "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
            "svl_reset_device_flags", "svl_version"]
@@ -75,6 +76,11 @@ def lib():
                                              I32, U32, F, P, P, P, SZ, P]
         L.svl_sparse_decode_workspace_size.restype = SZ
         L.svl_sparse_decode_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, I32, U32]
+        L.svl_fresh_decode_step.restype = ctypes.c_int
+        L.svl_fresh_decode_step.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, I32,
+                                            F, U32, P, P, P, P, SZ, P]
+        L.svl_fresh_decode_workspace_size.restype = SZ
+        L.svl_fresh_decode_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, I32, U32]
         L.svl_prefill_prune.restype = ctypes.c_int
         L.svl_prefill_prune.argtypes = [P, I32, I32, P, I32, D, P, I32, P, P, SZ, P]
         L.svl_prune_workspace_size.restype = SZ
@@ -236,6 +242,39 @@ def sparse_decode_attn(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_le
         _cuda(lse_out, "lse_out", torch.float32) if lse_out is not None else None,
         w.data_ptr(), w.numel(), _stream(stream)))
     return out, lse_out
+
+
+def fresh_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags=0) -> int:
+    return int(lib().svl_fresh_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags))
+
+
+def fresh_decode_step(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor,
+                      visual_begin: int, visual_len: int, k: int, scale: Optional[float] = None,
+                      flags: int = 0, idx_out: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None,
+                      ws: Optional[Workspace] = None, stream=None):
+    """svl_fresh_decode_step (fused retrieve + sparse decode, same query).
+    q bf16 [B][H][d].  Returns (out fp32 [B][H][d], idx int32 [B][Hkv][k])."""
+    B, H, d = q.shape
+    Hkv = K.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous")
+    if idx_out is None:
+        idx_out = torch.empty(B, Hkv, max(k, 0), dtype=torch.int32, device=q.device)
+    if out is None:
+        out = torch.empty(B, H, d, dtype=torch.float32, device=q.device)
+    wsz = fresh_decode_workspace_size(B, H, Hkv, d, k, visual_len, K.shape[2], flags)
+    w = _ws(ws, q.device).get(wsz)
+    _check(lib().svl_fresh_decode_step(
+        q.data_ptr(), B, H, Hkv, d, kv_view(K, "K"), kv_view(V, "V"),
+        span(visual_begin, visual_len, seq_len), k, scale, flags,
+        _cuda(idx_out, "idx_out", torch.int32), _cuda(out, "out", torch.float32),
+        _cuda(lse_out, "lse_out", torch.float32) if lse_out is not None else None,
+        w.data_ptr(), w.numel(), _stream(stream)))
+    return out, idx_out
 
 
 def prefill_prune(saliency: torch.Tensor, prefill_sparsity: float, frame_offsets=None,

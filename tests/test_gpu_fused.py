@@ -1,0 +1,116 @@
+"""GPU parity of svl_fresh_decode_step (fused retrieve + sparse decode) vs the
+fp64 oracle: indices by the gap rule, attention output within tolerance
+(SURVEY.md 8(c) c6), at toy size and the BASELINE configs at full size."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2510_17777_b200 import inputs as gen
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+NTH = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def svl():
+    from paper_2510_17777_b200 import build, svl as mod
+    build.build()
+    mod.lib()
+    return mod
+
+
+def _run(svl, orc, wl, seed, flags=0, k=None, big=True):
+    k = wl.k if k is None else k
+    x = gen.make_decode_inputs(wl, seed=seed, device="cuda" if big else "cpu")
+    cpu = {kk: v.cpu() for kk, v in x.items()}
+    dev = {kk: v.cuda() for kk, v in x.items()}
+    lse = torch.empty(wl.B, wl.H, device="cuda")
+    out, idx = svl.fresh_decode_step(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb,
+                                     wl.nv, k, flags=flags, lse_out=lse)
+    torch.cuda.synchronize()
+    idx = idx.cpu().numpy()
+    oi, osc, gap = orc.retrieve(cpu["q"], cpu["K"], cpu["seq_len"], wl.vb, wl.nv, k, flags=flags,
+                                nthreads=NTH)
+    frac = parity.check_indices(idx, osc, gap, k)
+    # decode parity on the GPU's own (validated) selection
+    oo, ol = orc.sparse_decode(cpu["q_dec"], cpu["K"], cpu["V"], cpu["seq_len"], wl.vb, wl.nv,
+                               idx if k else np.zeros((wl.B, wl.Hkv, 0), np.int32), nthreads=NTH)
+    mx, rel = parity.check_attention(out.cpu().numpy(), lse.cpu().numpy(), oo, ol)
+    return frac, mx, rel, idx, oi
+
+
+@pytest.mark.parametrize("name", ["toy", "nvila-4k", "long-video", "multi-turn"])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_fresh_step_configs(svl, orc, name, flags):
+    wl = gen.CONFIGS[name]
+    frac, mx, rel, _, _ = _run(svl, orc, wl, seed=31, flags=flags, big=(name != "toy"))
+    print(f"{name} flags={flags}: strict {frac:.2f} max-abs {mx:.2e} rel {rel:.2e}")
+
+
+def test_fresh_step_gapped_bitexact(svl, orc):
+    base = gen.CONFIGS["long-video"]
+    for gamma in (4.0, 8.0, 16.0):
+        wl = gen.DecodeWorkload(**{**base.__dict__, "gap_gamma": gamma, "sinks": 0, "needles": 0})
+        x = gen.make_decode_inputs(wl, seed=32, device="cuda")
+        oi, osc, gap = orc.retrieve(x["q"].cpu(), x["K"].cpu(), x["seq_len"].cpu(), wl.vb, wl.nv,
+                                    wl.k, nthreads=NTH)
+        if gap.min() > 1e-3:
+            break
+    out, idx = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    assert np.array_equal(idx.cpu().numpy(), oi)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2000])
+def test_fresh_step_k_edges_ragged(svl, orc, k):
+    wl = gen.DecodeWorkload("fe", 3, 28, 4, 128, 19, 2000, 77, k, 1, 256)
+    wl.seq_lens = [wl.seq_len, wl.seq_len - 30, wl.seq_len - 70]
+    _run(svl, orc, wl, seed=33 + k, k=k, big=False)
+
+
+@pytest.mark.parametrize("H,Hkv,d", [(16, 1, 128), (8, 2, 64), (4, 4, 64), (32, 2, 128)])
+def test_fresh_step_shapes(svl, orc, H, Hkv, d):
+    wl = gen.DecodeWorkload("fs", 2, H, Hkv, d, 8, 5000, 40, 500, 1, 256)
+    _run(svl, orc, wl, seed=34, big=False)
+
+
+def test_fresh_step_matches_unfused(svl):
+    """Fused == retrieve + sparse decode (the two-call path) within tolerance,
+    identical kept sets where the selection is not a near-tie."""
+    wl = gen.CONFIGS["long-video"]
+    x = gen.make_decode_inputs(wl, seed=35, device="cuda")
+    out_f, idx_f = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    idx_u = svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    out_u, _ = svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx_u)
+    torch.cuda.synchronize()
+    same = (idx_f == idx_u).all(dim=-1).float().mean().item()
+    assert same >= 0.5
+    if same == 1.0:
+        assert (out_f - out_u).abs().max().item() < 1e-5
+
+
+def test_fresh_step_sweep_fallback_sampled(svl, orc):
+    """64k visual tokens exceed the fused on-chip budget -> the two-call path."""
+    wl = gen.CONFIGS["sweep"]
+    x = gen.make_decode_inputs(wl, seed=36, device="cuda")
+    out, idx = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    torch.cuda.synchronize()
+    for b in (3,):
+        sl = slice(b, b + 1)
+        cpu = {kk: v[sl].cpu() for kk, v in x.items()}
+        oi, osc, gap = orc.retrieve(cpu["q"], cpu["K"], cpu["seq_len"], wl.vb, wl.nv, wl.k, nthreads=NTH)
+        parity.check_indices(idx[sl].cpu().numpy(), osc, gap, wl.k)
+        oo, ol = orc.sparse_decode(cpu["q_dec"], cpu["K"], cpu["V"], cpu["seq_len"], wl.vb, wl.nv,
+                                   idx[sl].cpu().numpy(), nthreads=NTH)
+        parity.check_attention(out[sl].cpu().numpy(), None, oo, ol)
+
+
+def test_fresh_step_deterministic(svl):
+    wl = gen.CONFIGS["long-video"]
+    x = gen.make_decode_inputs(wl, seed=37, device="cuda")
+    a, ia = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    a, ia = a.clone(), ia.clone()
+    b, ib = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    assert torch.equal(a, b) and torch.equal(ia, ib)
