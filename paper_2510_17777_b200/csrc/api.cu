@@ -5,6 +5,7 @@
 // the device's SM count), error strings.  No allocation, no synchronisation.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -363,7 +364,8 @@ size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_
                                        int32_t visual_len, int32_t capacity, uint32_t flags) {
     if (B < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
     int CS, slice;
-    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice)) return kWsHeader;
+    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice))
+        return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
     return std::max(svl_retrieve_workspace_size(B, 1, H, Hkv, d, visual_len, flags),
                     svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags));
 }
@@ -424,6 +426,9 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
     p.out = out;
     p.lse_out = lse_out;
     p.flags = static_cast<uint32_t*>(ws);
+    p.trace = (getenv("SVL_TRACE") && ws_bytes >= kWsHeader + ((size_t)1 << 20))
+                  ? reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader)
+                  : nullptr;
     cudaError_t e = launch_fresh(p, d, CS, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "svl_fresh_decode_step");
     return SVL_OK;

@@ -19,7 +19,7 @@
 //   2. cluster reduction of the (max, sum) partials over DSMEM -> the
 //      full-prefix LSE of every head (same value in every CTA);
 //   3. score_j = sum_h exp2(s2[j,h] - LSE2[h]) -> order-preserving keys;
-//   4. cluster_topk (select_core.cuh) -> threshold; kept indices written to
+//   4. cluster_topk_push (select_push.cuh) -> threshold; kept indices written to
 //      idx_out (ascending, ties to the lower index);
 //   5. decode attention over this CTA's kept rows + text share, reusing the
 //      logits: fixed max M_h, l_h = sum exp2(s2 - M_h), O_h = sum p V with V
@@ -31,7 +31,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
-#include "select_core.cuh"
+#include "select_push.cuh"
 
 namespace svl {
 
@@ -56,9 +56,10 @@ struct FGeom {
     static constexpr int ATT_OFF = LOG_OFF + LOG_BYTES;
     static constexpr int ATT_BYTES = (SMAX + TMAX) * 4;
     static constexpr int MISC_OFF = ATT_OFF + ATT_BYTES;
-    static constexpr int MISC_BYTES = 2 * NST * 8 + FCW * NCP * 8 + NCP * 8 + NCP * 4 + 64 * 4;
+    static constexpr int MISC_BYTES = 2 * NST * 8 + FCW * NCP * 8 + 16 * NCP * 8 + NCP * 4 + 64 * 4;
     static constexpr int BYTES = MISC_OFF + MISC_BYTES;
     static constexpr int KEYS_OFF = 96 * 1024;  // inside the ring once streaming is over
+    static constexpr int STATE_OFF = KEYS_OFF + SMAX * 4;
     static constexpr int VBUF_BYTES = VB_ROWS * ROWB;
     static constexpr int OCTA_OFF = 64 * 1024;  // CTA O [16][D] fp32 inside the ring at the end
 };
@@ -72,8 +73,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     constexpr int NCH = D / 32;  // 16-byte chunks per thread per row (permuted contraction)
     constexpr int CH = D / 8;    // 16-byte chunks per row
     constexpr int NVT = D / 8;   // output n-tiles
-    constexpr int EMAXF = (GM::SMAX + FT - 1) / FT;
-    static_assert(sizeof(TopkSmem) <= GM::KEYS_OFF, "top-k scratch must fit in the ring");
+    static_assert(GM::STATE_OFF + GM::SMAX <= RING, "keys + state must fit in the ring");
+    static_assert(sizeof(PushTopkSmem) <= GM::KEYS_OFF, "top-k scratch must fit in the ring");
     static_assert(GM::BYTES <= 227 * 1024, "shared memory budget");
 
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -91,12 +92,19 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     uint64_t* full = reinterpret_cast<uint64_t*>(misc);
     uint64_t* empty = full + NST;
     float2* wpart = reinterpret_cast<float2*>(empty + NST);  // [FCW][NCP]
-    float2* cta_part = wpart + FCW * NCP;                    // [NCP]
-    float* lse2 = reinterpret_cast<float*>(cta_part + NCP);  // [NCP]
+    float2* allpart = wpart + FCW * NCP;                       // [16][NCP] pushed by the peers
+    float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
     float* Mh = lse2 + NCP;                                  // [16]
     float* lh = Mh + 16;                                     // [16]
     int* cnt = reinterpret_cast<int*>(lh + 16);              // [4]
     const uint32_t ring = smem_u32(smem);
+#define SVL_TRACE(ph)                                                                     \
+    if (p.trace && tid == 0) {                                                            \
+        uint64_t tnow;                                                                    \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                          \
+        p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + (ph)] = tnow;        \
+    }
+    SVL_TRACE(0);
 
     // ------------------------------------------------------------ geometry
     int L = p.seq_len[b];
@@ -136,7 +144,14 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     // ------------------------------------------------ 1. stream K, logits
     if (warp == FCW) {
         if (lane == 0) {
+            // the work list is <= 3 contiguous row segments: visual slice, system
+            // text, after-visual text; each stage is their intersection with it
+            const int nsys = max(0, min(ntext, p.vb - t0));
+            const int seg_w0[3] = {0, nvis, nvis + nsys};
+            const int seg_w1[3] = {nvis, nvis + nsys, nwork};
+            const int seg_row0[3] = {p.vb + v0, t0, t0 + nsys + p.nv};  // cache row of the segment start
             const bool dense = (p.kst == D);
+            const int64_t kst = p.kst;
             for (int i = 0; i < nstages; ++i) {
                 const int slot = i % NST;
                 if (i >= NST) mbar_wait(smem_u32(&empty[slot]), ((i / NST) - 1) & 1);
@@ -144,18 +159,21 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
                 const uint32_t bar = smem_u32(&full[slot]);
                 mbar_arrive_expect_tx(bar, (uint32_t)((w1 - w0) * ROWB));
                 const uint32_t dst0 = ring + slot * GM::STAGE_BYTES;
-                int w = w0;
-                while (w < w1) {  // contiguous runs of cache rows
-                    const int row = work_row(w);
-                    int n = 1;
-                    if (dense)
-                        while (w + n < w1 && work_row(w + n) == row + n) ++n;
-                    bulk_g2s(dst0 + (w - w0) * ROWB, Kb + (int64_t)row * p.kst, (uint32_t)(n * ROWB), bar);
-                    w += n;
+#pragma unroll
+                for (int sg = 0; sg < 3; ++sg) {
+                    const int a = max(w0, seg_w0[sg]), z = min(w1, seg_w1[sg]);
+                    if (a >= z) continue;
+                    const int row = seg_row0[sg] + (a - seg_w0[sg]);
+                    if (dense) {
+                        bulk_g2s(dst0 + (a - w0) * ROWB, Kb + (int64_t)row * kst, (uint32_t)((z - a) * ROWB), bar);
+                    } else {
+                        for (int w = a; w < z; ++w)
+                            bulk_g2s(dst0 + (w - w0) * ROWB, Kb + (int64_t)(row + w - a) * kst, ROWB, bar);
+                    }
                 }
             }
         }
-    } else {
+    } else if (warp < FCW) {
         // query B fragments: column c = head G*g + c (c < g), same chunk layout as K
         uint4 bq[NT][NCH];
 #pragma unroll
@@ -241,6 +259,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     }
     __syncthreads();
 
+    SVL_TRACE(1);
     // ------------------------------------------------ 2. cluster LSE
     if (tid < NCP) {
         float m = -INFINITY, l = 0.f;
@@ -252,14 +271,14 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
                 m = M;
             }
         }
-        cta_part[tid] = make_float2(m, l);
+        // push this CTA's partial into every peer's allpart[rank] (no remote reads)
+        for (int q = 0; q < CS; ++q) cl.map_shared_rank(allpart, q)[rank * NCP + tid] = make_float2(m, l);
     }
     cl.sync();
     if (tid < NCP) {
         float2 x[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-            x[q] = (q < CS) ? cl.map_shared_rank(cta_part, q)[tid] : make_float2(-INFINITY, 0.f);
+        for (int q = 0; q < 16; ++q) x[q] = (q < CS) ? allpart[q * NCP + tid] : make_float2(-INFINITY, 0.f);
         float m = -INFINITY, l = 0.f;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -273,57 +292,59 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     }
     __syncthreads();
 
+    SVL_TRACE(2);
+    if (p.trace && tid == 0) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + 12] = clock64();
     // ------------------------------------------------ 3. keys
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + GM::KEYS_OFF);
-    {
+    for (int rep = 0; rep < (p.trace ? 2 : 1); ++rep) {  // (trace builds: run twice, i-cache probe)
+        if (rep == 1) {
+            __syncthreads();
+            SVL_TRACE(11);
+        }
         bool nan_seen = false;
+        // normalisers in registers; padded columns get +inf so they add exp2(-inf) = 0
+        // (no per-column branch: all NCP exponentials of a row issue back to back)
+        float nl[NCP];
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) nl[c] = (c < g) ? lse2[c] : INFINITY;
+#pragma unroll 2
         for (int i = tid; i < nvis; i += FT) {
-            const float* lr = logits + i * NCP;
+            const float4* lr = reinterpret_cast<const float4*>(logits + i * NCP);
             float sc = 0.f;
-            for (int c = 0; c < g; ++c) sc += exp2f(lr[c] - lse2[c]);
+#pragma unroll
+            for (int c4 = 0; c4 < NCP / 4; ++c4) {
+                const float4 x = lr[c4];
+                sc += fast_exp2(x.x - nl[4 * c4]) + fast_exp2(x.y - nl[4 * c4 + 1]) +
+                      fast_exp2(x.z - nl[4 * c4 + 2]) + fast_exp2(x.w - nl[4 * c4 + 3]);
+            }
             keys_s[i] = float_key(sc, nan_seen);
         }
         if (nan_seen) raise_flag(p.flags, 2u /*NONFINITE*/);
     }
     __syncthreads();
-    const int E = (nvis + FT - 1) / FT;
-    const int nmine = max(0, min(E, nvis - tid * E));
-    uint32_t key[EMAXF];
-#pragma unroll
-    for (int e = 0; e < EMAXF; ++e) key[e] = (e < nmine) ? keys_s[tid * E + e] : 0u;
 
     // ------------------------------------------------ 4. top-k
-    TopkSmem& ts = *reinterpret_cast<TopkSmem*>(smem);
-    const TopkResult r = cluster_topk<FT>(cl, ts, key, nmine, E, v0, slice, p.nv, p.k);
-    int32_t* idx_out = p.idx_out + (int64_t)u * p.k;
-    const int nsel = (int)topk_emit<FT>(ts, r, key, nmine, [&](int e, uint32_t slot) {
-        idx_out[slot] = v0 + tid * E + e;
-        att[slot - r.offset] = tid * E + e;
-    });
+    PushTopkSmem& ts = *reinterpret_cast<PushTopkSmem*>(smem);
+    uint8_t* state_s = smem + GM::STATE_OFF;
+    SVL_TRACE(3);
+    if (p.trace && tid == 0) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + 13] = clock64();
+    uint32_t sel_off;
+    const int nsel = (int)cluster_topk_push<FT>(
+        cl, ts, keys_s, state_s, nvis, v0, slice, p.nv, p.k, /*relevance=*/true, &sel_off,
+        p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + 16 : nullptr);
+    SVL_TRACE(4);
+    {
+        int32_t* idx_out = p.idx_out + (int64_t)u * p.k;
+        push_emit<FT>(ts, state_s, nvis, sel_off, [&](int i, uint32_t slot) {
+            idx_out[slot] = v0 + i;
+            att[slot - sel_off] = i;
+        });
+    }
     for (int i = tid; i < ntext; i += FT) att[nsel + i] = nvis + i;
     __syncthreads();
     const int natt = nsel + ntext;
 
     // ------------------------------------------------ 5. decode over the kept rows
-    // fixed per-head max / sum over this CTA's attended rows (logits are all known)
-    if (warp < FCW) {
-        for (int h = warp; h < 16; h += FCW) {
-            float m = -INFINITY;
-            if (h < g)
-                for (int i = lane; i < natt; i += 32) m = fmaxf(m, logits[att[i] * NCP + h]);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-            float l = 0.f;
-            if (h < g && m != -INFINITY)
-                for (int i = lane; i < natt; i += 32) l += exp2f(logits[att[i] * NCP + h] - m);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-            if (lane == 0) {
-                Mh[h] = m;
-                lh[h] = l;
-            }
-        }
-    }
     auto issue_batch = [&](int bi) {
         const int r0 = bi * VB_ROWS, n = min(VB_ROWS, natt - r0);
         const uint32_t vbuf = ring + (bi & 1) * GM::VBUF_BYTES;
@@ -337,11 +358,33 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         cp_async_commit();
     };
     const int nbatch = (natt + VB_ROWS - 1) / VB_ROWS;
-    __syncthreads();  // Mh/lh visible; ring free (top-k scratch done)
+    // the V gather of the first batch overlaps the max / sum pass below (the
+    // ring is free: the top-k exchange finished with a cluster barrier)
+    if (nbatch > 0) issue_batch(0);
+    // fixed per-head max / sum over this CTA's attended rows (logits are all known)
+    {
+        for (int h = warp; h < 16; h += FT / 32) {
+            float m = -INFINITY;
+            if (h < g)
+                for (int i = lane; i < natt; i += 32) m = fmaxf(m, logits[att[i] * NCP + h]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            float l = 0.f;
+            if (h < g && m != -INFINITY)
+                for (int i = lane; i < natt; i += 32) l += fast_exp2(logits[att[i] * NCP + h] - m);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+            if (lane == 0) {
+                Mh[h] = m;
+                lh[h] = l;
+            }
+        }
+    }
+    __syncthreads();  // Mh/lh visible
+    SVL_TRACE(5);
     float o[NVT][4];
 #pragma unroll
     for (int n = 0; n < NVT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    if (nbatch > 0) issue_batch(0);
     for (int bi = 0; bi < nbatch; ++bi) {
         if (bi + 1 < nbatch) {
             issue_batch(bi + 1);
@@ -364,8 +407,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
                         const int rr = tb + kh * 8 + 2 * t + e;
                         const bool ok = rr < n;
                         const float* lr = logits + (ok ? att[r0 + rr] : 0) * NCP;
-                        pv[kh][e] = (ok && gid < g && Ma != -INFINITY) ? exp2f(lr[gid] - Ma) : 0.f;
-                        pv[kh][2 + e] = (ok && gid + 8 < g && Mb != -INFINITY) ? exp2f(lr[gid + 8] - Mb) : 0.f;
+                        pv[kh][e] = (ok && gid < g && Ma != -INFINITY) ? fast_exp2(lr[gid] - Ma) : 0.f;
+                        pv[kh][2 + e] = (ok && gid + 8 < g && Mb != -INFINITY) ? fast_exp2(lr[gid + 8] - Mb) : 0.f;
                     }
                 uint32_t ph[4], pl[4];
                 {
@@ -393,6 +436,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         }
         __syncthreads();  // batch buffer free for batch bi + 2
     }
+    SVL_TRACE(6);
     // warp partials -> CTA O (fixed warp order); ring [0, 64K) as [FCW][16][D]
     float* wo = reinterpret_cast<float*>(smem);
     if (warp < FCW) {
@@ -413,14 +457,21 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         octa[h * D + dd] = acc;
     }
     // ------------------------------------------------ 6. cluster merge
+    SVL_TRACE(7);
     cl.sync();
+    SVL_TRACE(8);
     const int items = g * D;
     const int per = (items + CS - 1) / CS;
     for (int i = rank * per + tid; i < min(items, (rank + 1) * per); i += FT) {
         const int h = i / D, dd = i % D;
-        float mq[16];
+        // all 3 x CS remote loads issued before any use (one DSMEM round trip)
+        float mq[16], oq[16], lq[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) mq[q] = (q < CS) ? cl.map_shared_rank(Mh, q)[h] : -INFINITY;
+        for (int q = 0; q < 16; ++q) {
+            mq[q] = (q < CS) ? cl.map_shared_rank(Mh, q)[h] : -INFINITY;
+            oq[q] = (q < CS) ? cl.map_shared_rank(octa, q)[h * D + dd] : 0.f;
+            lq[q] = (q < CS) ? cl.map_shared_rank(lh, q)[h] : 0.f;
+        }
         float M = -INFINITY;
 #pragma unroll
         for (int q = 0; q < 16; ++q) M = fmaxf(M, mq[q]);
@@ -428,10 +479,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         if (M != -INFINITY) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                if (q < CS && mq[q] != -INFINITY) {
+                if (mq[q] != -INFINITY) {
                     const float w = exp2f(mq[q] - M);
-                    num += w * cl.map_shared_rank(octa, q)[h * D + dd];
-                    den += w * cl.map_shared_rank(lh, q)[h];
+                    num += w * oq[q];
+                    den += w * lq[q];
                 }
             }
         }
@@ -440,7 +491,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         if (dd == 0 && p.lse_out) p.lse_out[(int64_t)b * p.H + hh] = (den > 0.f) ? (M + log2f(den)) * kLn2 : -INFINITY;
     }
     (void)cnt;
+    SVL_TRACE(9);
     cl.sync();  // peers may still read this CTA's shared memory until here
+    SVL_TRACE(10);
+#undef SVL_TRACE
 }
 
 template <int D, int NT>

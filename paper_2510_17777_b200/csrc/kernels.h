@@ -83,8 +83,9 @@ struct FreshParams {
     float* out;        // [B][H][d]
     float* lse_out;    // [B][H] or null
     uint32_t* flags;
+    uint64_t* trace;   // debug: per-CTA phase timestamps (SVL_TRACE=1), else null
 };
-constexpr int kFusedThreads = 288;    // 8 consumer warps + 1 TMA producer warp
+constexpr int kFusedThreads = 512;    // 8 stream-consumer warps + 1 TMA producer warp + 7 helper warps
 constexpr int kFusedTextMax = 256;    // text rows per CTA
 constexpr int kFusedSliceMax = 2048;  // visual rows per CTA (halved for g > 8)
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
