@@ -209,6 +209,86 @@ def config_dict(wl):
 # ---------------------------------------------------------------- GPU arm
 
 
+def run_heads(args):
+    """the multi-turn batch (B=8, 16k visual) sharded over
+    (batch x KV head), one fused fresh step per layer per rank, then the NCCL
+    all-gather of head outputs (captured in the same CUDA graph).  Strong
+    scaling: the total work is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_17777_b200 import inputs as gen
+    from paper_2510_17777_b200 import sharding, svl
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = gen.CONFIGS["multi-turn"]
+    sp = sharding.plan(wl.B, wl.H, wl.Hkv, world, rank)
+    lwl = gen.DecodeWorkload(**{**wl.__dict__, "B": sp.B_local, "Hkv": sp.kv1 - sp.kv0,
+                                "H": sp.H_local})
+    layers = []
+    for layer in range(LAYERS):
+        x = gen.make_decode_inputs(lwl, seed=7000 + 100 * rank + layer, device=dev)
+        layers.append(x)
+    ws = svl.Workspace(dev)
+    ws.get(svl.fresh_decode_workspace_size(lwl.B, lwl.H, lwl.Hkv, lwl.d, lwl.k, lwl.nv, lwl.capacity))
+    outs = [torch.empty(lwl.B, lwl.H, lwl.d, device=dev) for _ in range(LAYERS)]
+    idxs = [torch.empty(lwl.B, lwl.Hkv, lwl.k, dtype=torch.int32, device=dev) for _ in range(LAYERS)]
+    full = [torch.empty(wl.B, wl.H, wl.d, device=dev) for _ in range(LAYERS)]
+
+    def step():
+        for l, x in enumerate(layers):
+            svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], lwl.vb, lwl.nv, lwl.k,
+                                  idx_out=idxs[l], out=outs[l], ws=ws)
+            if world > 1:
+                full[l].copy_(sharding.all_gather_heads(outs[l], sp, wl.H))
+            else:
+                full[l].copy_(outs[l])
+
+    step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            step()
+    for _ in range(args.warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    total = step_bytes(wl)["total"] * LAYERS
+    if rank == 0:
+        print(json.dumps({
+            "metric": "decode step HBM GB/s (retrieve+sparse attn), multi-turn batch head-sharded",
+            "value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "multi-turn: B=8, 16384 visual, k=1638, 28 layers, (batch x KV-head) "
+                                   "shards + NCCL all-gather of head outputs per layer",
+                       "P_b": sp.P_b, "P_h": sp.P_h},
+            "tokens_per_s": wl.B / (ms * 1e-3), "clocks": clk.summary(),
+            "gpu_launches": LAYERS * args.steps}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -217,9 +297,15 @@ def main():
     ap.add_argument("--impl", default="svl", choices=["svl", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON checks)")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "heads"],
+                    help="replicas: every rank serves its own long-video request (weak); heads: "
+                         "one multi-turn batch sharded over (batch x KV head) with a per-layer "
+                         "NCCL all-gather of the head outputs (strong)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "heads":
+        return run_heads(args)
 
     import torch
     import torch.distributed as dist

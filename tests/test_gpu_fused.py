@@ -107,6 +107,26 @@ def test_fresh_step_sweep_fallback_sampled(svl, orc):
         parity.check_attention(out[sl].cpu().numpy(), None, oo, ol)
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_fresh_step_simulated_shards_bitwise(svl, P):
+    """SURVEY.md 4 'simulated-shard test': each rank's (batch x KV-head) slice
+    run separately on one GPU and assembled == the unsharded run, bitwise."""
+    from paper_2510_17777_b200 import sharding
+    wl = gen.DecodeWorkload("shd", 4, 28, 4, 128, 32, 8192, 300, 819, 1, 256)
+    x = gen.make_decode_inputs(wl, seed=38, device="cuda")
+    ref, _ = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    ref = ref.clone()
+    parts, plans = [], []
+    for r in range(P):
+        sp = sharding.plan(wl.B, wl.H, wl.Hkv, P, r)
+        ql, Kl, Vl, sl = sharding.local_inputs(sp, x["q_dec"], x["K"], x["V"], x["seq_len"])
+        o, _ = svl.fresh_decode_step(ql, Kl, Vl, sl, wl.vb, wl.nv, wl.k)
+        parts.append(o.clone())
+        plans.append(sp)
+    full = sharding.assemble(parts, plans, wl.B, wl.H)
+    assert torch.equal(full, ref)
+
+
 def test_fresh_step_deterministic(svl):
     wl = gen.CONFIGS["long-video"]
     x = gen.make_decode_inputs(wl, seed=37, device="cuda")
