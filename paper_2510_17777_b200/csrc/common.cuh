@@ -66,6 +66,9 @@ SVL_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.clust
 SVL_DEV void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+SVL_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {  // no arrival
+    asm volatile("mbarrier.expect_tx.shared.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 SVL_DEV void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(bar) : "memory");
 }

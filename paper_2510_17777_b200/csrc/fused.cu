@@ -10,71 +10,88 @@
 //
 // One thread-block cluster (CS <= 16 CTAs, distributed shared memory) per
 // unit (b, KV group G); CTA r owns visual rows [r*slice, (r+1)*slice) and a
-// 1/CS share of the text rows.  Per CTA (8 consumer warps + 1 TMA warp):
-//   1. the TMA warp streams the CTA's K rows (visual slice, then text share)
-//      with cp.async.bulk into a 4-stage x 32 KB mbarrier ring; consumer warps
-//      compute the base-2 logits of all g heads per 16-row tile with
-//      mma.sync (swap-AB, permuted contraction, as in score.cu) and keep them
-//      in shared memory (never written to HBM), plus a running (max, sum);
-//   2. cluster reduction of the (max, sum) partials over DSMEM -> the
-//      full-prefix LSE of every head (same value in every CTA);
-//   3. score_j = sum_h exp2(s2[j,h] - LSE2[h]) -> order-preserving keys;
-//   4. cluster_topk_push (select_push.cuh) -> threshold; kept indices written to
-//      idx_out (ascending, ties to the lower index);
-//   5. decode attention over this CTA's kept rows + text share, reusing the
-//      logits: fixed max M_h, l_h = sum exp2(s2 - M_h), O_h = sum p V with V
-//      rows gathered by cp.async (swizzled) and P split bf16 hi+lo for
-//      mma.sync (ldmatrix.trans V fragments);
-//   6. cluster merge of (M, l, O) over DSMEM -> out fp32 [B][H][d], lse.
-// HBM traffic per unit: visual K + text K once + kept V + text V.
+// 1/CS share of the text rows.  Per CTA: 1 TMA producer warp, 8 consumer
+// warps, 7 helper warps (512 threads), 216 KB of shared memory.
+//   1. stream: the TMA warp streams the CTA's K rows (visual slice, then text
+//      share) with cp.async.bulk into a 4 x 32 KB mbarrier ring; the consumer
+//      warps turn every 16-row tile into the base-2 logits of all g heads with
+//      mma.sync (swap-AB, permuted contraction) kept in shared memory, plus a
+//      running (max, sum) per head.  The text rows' V gather starts as soon as
+//      the ring drains.
+//   2. LSE: (max, sum) partials pushed to every peer over DSMEM; one cluster
+//      barrier; every CTA folds the same 16 partials -> identical LSE2[h].
+//   3. top-k (two cluster barriers): relevance keys + a 256-bin value-adaptive
+//      histogram, all-gathered; the threshold bin b*; the V gather of every row
+//      at or above b* is issued right away (a superset of the kept rows); the
+//      keys of b* are all-gathered in index order and resolved locally (one
+//      8-bit radix pass + exact ranking inside the last bin, ties to the lower
+//      index).  A generic exact radix (select_push.cuh) handles massive ties.
+//   4. decode: weights p = exp2(s2 - LSE2[h]) relative to the GLOBAL
+//      normaliser (identical in every CTA, so the merge needs no rescaling),
+//      tabulated once as split bf16 hi + lo; warp w owns output columns
+//      [16w, 16w+16) (ldmatrix.trans P and V fragments, mma.sync) -- no
+//      cross-warp reduction.
+//   5. merge: plain sums of (O, l) over the cluster -> out fp32, lse.
+// HBM traffic per unit: visual K + text K once + kept V + text V (+ the V of
+// the few non-kept keys of the threshold bin).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "kernels.h"
-#include "select_push.cuh"
+#include "select_fast.cuh"
 
 namespace svl {
 
 namespace {
 
-constexpr int FT = kFusedThreads;  // 8 consumer warps + 1 producer warp
-constexpr int FCW = 8;
+constexpr int FT = kFusedThreads;  // 512
+constexpr int FCW = 8;             // stream consumer warps (warp FCW = TMA producer)
 constexpr int STAGE_ROWS = 128;
 constexpr int RING = 128 * 1024;
 constexpr int TMAX = kFusedTextMax;
-constexpr int VB_ROWS = 256;  // V rows per staging batch (two batches in the ring)
 
 template <int D, int NT>
 struct FGeom {
     static constexpr int NCP = 8 * NT;
     static constexpr int SMAX = kFusedSliceMax / NT;
-    static constexpr int NST = 512 / D;  // ring stages
+    static constexpr int NST = 512 / D;  // ring stages of 32 KB
     static constexpr int ROWB = 2 * D;
     static constexpr int STAGE_BYTES = STAGE_ROWS * ROWB;
+    // persistent regions
     static constexpr int LOG_OFF = RING;
     static constexpr int LOG_BYTES = (SMAX + TMAX) * NCP * 4;
-    static constexpr int ATT_OFF = LOG_OFF + LOG_BYTES;
+    static constexpr int ATT_OFF = LOG_OFF + LOG_BYTES;  // V slot -> local row
     static constexpr int ATT_BYTES = (SMAX + TMAX) * 4;
     static constexpr int MISC_OFF = ATT_OFF + ATT_BYTES;
-    static constexpr int MISC_BYTES = 2 * NST * 8 + FCW * NCP * 8 + 16 * NCP * 8 + NCP * 4 + 64 * 4;
+    static constexpr int MISC_BYTES = 2 * NST * 8 + 8 + FCW * NCP * 8 + 16 * NCP * 8 + NCP * 4 + 16 * 4 + 64 * 4 + 32 * 8;
     static constexpr int BYTES = MISC_OFF + MISC_BYTES;
-    static constexpr int KEYS_OFF = 96 * 1024;  // inside the ring once streaming is over
-    static constexpr int STATE_OFF = KEYS_OFF + SMAX * 4;
-    static constexpr int VBUF_BYTES = VB_ROWS * ROWB;
-    static constexpr int OCTA_OFF = 64 * 1024;  // CTA O [16][D] fp32 inside the ring at the end
+    // ring re-use once streaming is over
+    static constexpr int SEL_OFF = 0;                     // FastSelSmem
+    static constexpr int KEYS_OFF = 32 * 1024;            // keys [SMAX]
+    static constexpr int STATE_OFF = KEYS_OFF + SMAX * 4; // per-row state [SMAX]
+    static constexpr int VST_OFF = 44 * 1024;             // V staging [VCAP][D], rows padded by 16 B
+    static constexpr int VROWB = ROWB + 16;               // (conflict-free ldmatrix without a swizzle)
+    static constexpr int VCAP = ((RING - VST_OFF) / VROWB) / 16 * 16 > 320 ? 320 : ((RING - VST_OFF) / VROWB) / 16 * 16;
+    static constexpr int PUSH_OFF = VST_OFF;              // generic top-k scratch (fallback only)
+    static constexpr int WHIST_OFF = RING - 16 * 1024;    // private histograms (before any selected-row V)
+    static_assert(VST_OFF + TMAX * VROWB <= WHIST_OFF, "text-row V below the private histograms");
+    static constexpr int PT_OFF = 0;                      // P table hi + lo [VCAP][16] (after top-k)
+    static constexpr int OCTA_OFF = PT_OFF + 2 * VCAP * 16 * 2;  // CTA O [16][D] fp32
+    static constexpr int LRED_OFF = OCTA_OFF + 16 * D * 4;       // [FT] fp32
+    static_assert(STATE_OFF + SMAX <= VST_OFF, "keys + state below the V staging");
+    static_assert(VST_OFF + VCAP * VROWB <= RING, "V staging inside the ring");
+    static_assert(LRED_OFF + FT * 4 <= VST_OFF, "P table / O / l scratch below the V staging");
 };
 
-SVL_DEV int swz_v(int row, int c) { return c ^ (row & 7); }
 
 template <int D, int NT>
 __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     using GM = FGeom<D, NT>;
-    constexpr int NCP = GM::NCP, NST = GM::NST, ROWB = GM::ROWB;
+    constexpr int NCP = GM::NCP, NST = GM::NST, ROWB = GM::ROWB, VCAP = GM::VCAP;
     constexpr int NCH = D / 32;  // 16-byte chunks per thread per row (permuted contraction)
     constexpr int CH = D / 8;    // 16-byte chunks per row
-    constexpr int NVT = D / 8;   // output n-tiles
-    static_assert(GM::STATE_OFF + GM::SMAX <= RING, "keys + state must fit in the ring");
-    static_assert(sizeof(PushTopkSmem) <= GM::KEYS_OFF, "top-k scratch must fit in the ring");
+    static_assert(sizeof(FastSelSmem) <= GM::KEYS_OFF, "fast top-k scratch");
+    static_assert(GM::PUSH_OFF + sizeof(PushTopkSmem) <= RING, "generic top-k scratch");
     static_assert(GM::BYTES <= 227 * 1024, "shared memory budget");
 
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -91,19 +108,25 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     uint8_t* misc = smem + GM::MISC_OFF;
     uint64_t* full = reinterpret_cast<uint64_t*>(misc);
     uint64_t* empty = full + NST;
-    float2* wpart = reinterpret_cast<float2*>(empty + NST);  // [FCW][NCP]
-    float2* allpart = wpart + FCW * NCP;                       // [16][NCP] pushed by the peers
+    uint64_t* vbar = empty + NST;                                // V gathers (TMA bulk, per row)
+    float2* wpart = reinterpret_cast<float2*>(vbar + 1);         // [FCW][NCP]
+    float2* allpart = wpart + FCW * NCP;                         // [16][NCP] pushed by the peers
     float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
-    float* Mh = lse2 + NCP;                                  // [16]
-    float* lh = Mh + 16;                                     // [16]
-    int* cnt = reinterpret_cast<int*>(lh + 16);              // [4]
+    float* lh = lse2 + NCP;                                      // [16]
+    int* ibc = reinterpret_cast<int*>(lh + 16);                  // broadcasts
+    uint64_t* trs = reinterpret_cast<uint64_t*>(ibc + 64);       // debug stamps (SVL_TRACE), flushed at exit
     const uint32_t ring = smem_u32(smem);
+    const uint32_t vst = ring + GM::VST_OFF;
+    uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + GM::KEYS_OFF);
+    uint8_t* state_s = smem + GM::STATE_OFF;
+    FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(smem + GM::SEL_OFF);
 #define SVL_TRACE(ph)                                                                     \
     if (p.trace && tid == 0) {                                                            \
         uint64_t tnow;                                                                    \
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                          \
-        p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + (ph)] = tnow;        \
+        trs[(ph)] = tnow;                                                                 \
     }
+    if (p.trace && tid < 32) trs[tid] = 0;
     SVL_TRACE(0);
 
     // ------------------------------------------------------------ geometry
@@ -126,17 +149,27 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     const int nstages = (nwork + STAGE_ROWS - 1) / STAGE_ROWS;
     const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
     const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
-    auto text_row = [&](int ti) {  // text share index -> cache row
-        const int tt = t0 + ti;
+    auto work_row = [&](int w) {  // local work row -> cache row
+        if (w < nvis) return p.vb + v0 + w;
+        const int tt = t0 + (w - nvis);
         return tt < p.vb ? tt : tt + p.nv;
     };
-    auto work_row = [&](int w) { return w < nvis ? p.vb + v0 + w : text_row(w - nvis); };
+    // V gather of slots [s0, s1) (slot -> local row in att[]): one TMA bulk copy
+    // per row, issued by many threads, completion counted on vbar (the single
+    // arrival of a phase carries the phase's total byte count; completions may
+    // precede it).  The TMA engine does the gather: the LSUs stay free.
+    const uint32_t vbar_a = smem_u32(vbar);
+    auto gather_rows = [&](int s0, int s1, int base) {
+        for (int sl = s0 + tid; sl < s1; sl += FT)
+            bulk_g2s(vst + (sl - base) * GM::VROWB, Vb + (int64_t)work_row(att[sl]) * p.vst, ROWB, vbar_a);
+    };
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
             mbar_init(smem_u32(&empty[s]), FCW);
         }
+        mbar_init(vbar_a, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -257,206 +290,158 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
                 if (gid == 0) wpart[warp * NCP + nt * 8 + 2 * t + e2] = make_float2(rm[nt][e2], rl[nt][e2]);
             }
     }
-    __syncthreads();
+    __syncthreads();  // ring drained (every stage was consumed)
 
+    // text rows' V: V slots [0, ntext); their gather overlaps everything up to the decode
+    for (int i = tid; i < ntext; i += FT) att[i] = nvis + i;
+    __syncthreads();
+    gather_rows(0, ntext, 0);
     SVL_TRACE(1);
+
     // ------------------------------------------------ 2. cluster LSE
-    if (tid < NCP) {
-        float m = -INFINITY, l = 0.f;
-        for (int w = 0; w < FCW; ++w) {
-            const float2 x = wpart[w * NCP + tid];
-            const float M = fmaxf(m, x.x);
-            if (M != -INFINITY) {
-                l = l * exp2f(m - M) + x.y * exp2f(x.x - M);
-                m = M;
-            }
+    auto lse_merge = [](float& m, float& l, float m2, float l2) {
+        const float M = fmaxf(m, m2);
+        if (M != -INFINITY) {
+            l = l * fast_exp2(m - M) + l2 * fast_exp2(m2 - M);
+            m = M;
         }
-        // push this CTA's partial into every peer's allpart[rank] (no remote reads)
-        for (int q = 0; q < CS; ++q) cl.map_shared_rank(allpart, q)[rank * NCP + tid] = make_float2(m, l);
+    };
+    if (warp < NCP) {  // warp c folds column c (fixed shuffle tree), lanes push to the peers
+        float2 x = (lane < FCW) ? wpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+        for (int off = 1; off < 16; off <<= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, x.x, off);
+            const float l2 = __shfl_xor_sync(0xffffffffu, x.y, off);
+            lse_merge(x.x, x.y, m2, l2);
+        }
+        if (lane < CS) cl.map_shared_rank(allpart, lane)[rank * NCP + warp] = x;
     }
     cl.sync();
-    if (tid < NCP) {
-        float2 x[16];
+    if (warp < NCP) {
+        float2 x = (lane < CS) ? allpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) x[q] = (q < CS) ? allpart[q * NCP + tid] : make_float2(-INFINITY, 0.f);
-        float m = -INFINITY, l = 0.f;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const float M = fmaxf(m, x[q].x);
-            if (M != -INFINITY) {
-                l = l * exp2f(m - M) + x[q].y * exp2f(x[q].x - M);
-                m = M;
-            }
+        for (int off = 1; off < 16; off <<= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, x.x, off);
+            const float l2 = __shfl_xor_sync(0xffffffffu, x.y, off);
+            lse_merge(x.x, x.y, m2, l2);
         }
-        lse2[tid] = m + log2f(l);
+        if (lane == 0) lse2[warp] = x.x + log2f(x.y);
     }
     __syncthreads();
-
     SVL_TRACE(2);
-    if (p.trace && tid == 0) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + 12] = clock64();
-    // ------------------------------------------------ 3. keys
-    uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + GM::KEYS_OFF);
-    for (int rep = 0; rep < (p.trace ? 2 : 1); ++rep) {  // (trace builds: run twice, i-cache probe)
-        if (rep == 1) {
-            __syncthreads();
-            SVL_TRACE(11);
-        }
-        bool nan_seen = false;
-        // normalisers in registers; padded columns get +inf so they add exp2(-inf) = 0
-        // (no per-column branch: all NCP exponentials of a row issue back to back)
-        float nl[NCP];
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) nl[c] = (c < g) ? lse2[c] : INFINITY;
-#pragma unroll 2
-        for (int i = tid; i < nvis; i += FT) {
-            const float4* lr = reinterpret_cast<const float4*>(logits + i * NCP);
-            float sc = 0.f;
-#pragma unroll
-            for (int c4 = 0; c4 < NCP / 4; ++c4) {
-                const float4 x = lr[c4];
-                sc += fast_exp2(x.x - nl[4 * c4]) + fast_exp2(x.y - nl[4 * c4 + 1]) +
-                      fast_exp2(x.z - nl[4 * c4 + 2]) + fast_exp2(x.w - nl[4 * c4 + 3]);
-            }
-            keys_s[i] = float_key(sc, nan_seen);
-        }
-        if (nan_seen) raise_flag(p.flags, 2u /*NONFINITE*/);
-    }
-    __syncthreads();
 
-    // ------------------------------------------------ 4. top-k
-    PushTopkSmem& ts = *reinterpret_cast<PushTopkSmem*>(smem);
-    uint8_t* state_s = smem + GM::STATE_OFF;
+    // ------------------------------------------------ 3. top-k (+ early V gather)
+    int32_t* idx_out = p.idx_out + (int64_t)u * p.k;
+    FastSelect<FT, NCP> sel(cl, fs, logits, lse2, g, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags,
+                            reinterpret_cast<uint32_t*>(smem + GM::WHIST_OFF));
+    if (p.trace) sel.tr = trs + 16;
+    int nslots = ntext;
+    uint32_t vphase = 0;
+    const int stage = sel.histogram_and_threshold();  // 0 = all / none, 1 = fast path, 2 = generic
     SVL_TRACE(3);
-    if (p.trace && tid == 0) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + 13] = clock64();
-    uint32_t sel_off;
-    const int nsel = (int)cluster_topk_push<FT>(
-        cl, ts, keys_s, state_s, nvis, v0, slice, p.nv, p.k, /*relevance=*/true, &sel_off,
-        p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + 16 : nullptr);
+    if (stage == 1) {
+        // every row at or above the threshold bin gets a V slot now (superset of the kept rows)
+        nslots = ntext + sel.assign_slots_and_push_candidates(att + ntext);
+        SVL_TRACE(11);
+        gather_rows(ntext, min(nslots, VCAP), 0);
+        if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(min(nslots, VCAP) * ROWB));
+        SVL_TRACE(12);
+        sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
+    } else {
+        if (stage == 2) {
+            // the generic scratch aliases the V staging: every CTA's text-row gather
+            // must land before any peer pushes into it (text rows are re-gathered)
+            if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(ntext * ROWB));
+            mbar_wait(vbar_a, 0);
+            vphase = 1;
+            cl.sync();
+        }
+        const int nsel = sel.generic_or_trivial(stage, *reinterpret_cast<PushTopkSmem*>(smem + GM::PUSH_OFF),
+                                                idx_out, att + ntext);
+        nslots = ntext + nsel;
+        gather_rows(stage == 2 ? 0 : ntext, min(nslots, VCAP), 0);
+        if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(min(nslots, VCAP) * ROWB));
+    }
     SVL_TRACE(4);
-    {
-        int32_t* idx_out = p.idx_out + (int64_t)u * p.k;
-        push_emit<FT>(ts, state_s, nvis, sel_off, [&](int i, uint32_t slot) {
-            idx_out[slot] = v0 + i;
-            att[slot - sel_off] = i;
-        });
-    }
-    for (int i = tid; i < ntext; i += FT) att[nsel + i] = nvis + i;
-    __syncthreads();
-    const int natt = nsel + ntext;
 
-    // ------------------------------------------------ 5. decode over the kept rows
-    auto issue_batch = [&](int bi) {
-        const int r0 = bi * VB_ROWS, n = min(VB_ROWS, natt - r0);
-        const uint32_t vbuf = ring + (bi & 1) * GM::VBUF_BYTES;
+    // ------------------------------------------------ 4. decode over the kept rows
+    // p = exp2(s2 - LSE2[h]): the same reference in every CTA -> plain-sum merge.
+    const int hmine = tid & 15;  // FT % 16 == 0: thread tid always handles head tid % 16
+    const float lse_mine = (hmine < g) ? lse2[hmine] : 0.f;
+    float lacc = 0.f;
+    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::PT_OFF);
+    uint16_t* ptl = pth + VCAP * 16;
+    __syncthreads();  // top-k scratch (aliased by the P table) is dead
+    for (int s0 = 0; s0 < nslots; s0 += VCAP) {
+        const int n = min(VCAP, nslots - s0);
         const int nr = (n + 15) & ~15;
-        for (int i = tid; i < nr * CH; i += FT) {
+        if (s0 > 0) {  // overflow batches (rare): after the previous PV
+            gather_rows(s0, s0 + n, s0);
+            if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(n * ROWB));
+        }
+        for (int i = tid; i < nr * 16; i += FT) {
+            const int rr = i >> 4;
+            float pv = 0.f;
+            if (rr < n && hmine < g) {
+                const int r = att[s0 + rr];
+                if (r >= nvis || state_s[r] == kKeySel) pv = fast_exp2(logits[r * NCP + hmine] - lse_mine);
+            }
+            lacc += pv;
+            const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+            const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+            pth[i] = *reinterpret_cast<const uint16_t*>(&hi);
+            ptl[i] = *reinterpret_cast<const uint16_t*>(&lo);
+        }
+        // rows [n, nr) of the staging buffer: zero V (the P rows are zero, avoid NaN * 0)
+        for (int i = n * CH + tid; i < nr * CH; i += FT) {
             const int rr = i / CH, c = i % CH;
-            const bool valid = rr < n;
-            const int row = valid ? work_row(att[r0 + rr]) : 0;
-            cp_async16(vbuf + rr * ROWB + swz_v(rr, c) * 16, Vb + (int64_t)row * p.vst + c * 8, valid);
+            *reinterpret_cast<uint4*>(smem + GM::VST_OFF + rr * GM::VROWB + c * 16) = make_uint4(0, 0, 0, 0);
         }
-        cp_async_commit();
-    };
-    const int nbatch = (natt + VB_ROWS - 1) / VB_ROWS;
-    // the V gather of the first batch overlaps the max / sum pass below (the
-    // ring is free: the top-k exchange finished with a cluster barrier)
-    if (nbatch > 0) issue_batch(0);
-    // fixed per-head max / sum over this CTA's attended rows (logits are all known)
-    {
-        for (int h = warp; h < 16; h += FT / 32) {
-            float m = -INFINITY;
-            if (h < g)
-                for (int i = lane; i < natt; i += 32) m = fmaxf(m, logits[att[i] * NCP + h]);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-            float l = 0.f;
-            if (h < g && m != -INFINITY)
-                for (int i = lane; i < natt; i += 32) l += fast_exp2(logits[att[i] * NCP + h] - m);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-            if (lane == 0) {
-                Mh[h] = m;
-                lh[h] = l;
-            }
-        }
-    }
-    __syncthreads();  // Mh/lh visible
-    SVL_TRACE(5);
-    float o[NVT][4];
-#pragma unroll
-    for (int n = 0; n < NVT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    for (int bi = 0; bi < nbatch; ++bi) {
-        if (bi + 1 < nbatch) {
-            issue_batch(bi + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        mbar_wait(vbar_a, vphase);
+        vphase ^= 1u;
         __syncthreads();
-        const int r0 = bi * VB_ROWS, n = min(VB_ROWS, natt - r0);
-        const uint32_t vbuf = ring + (bi & 1) * GM::VBUF_BYTES;
-        if (warp < FCW) {
-            const float Ma = (gid < g) ? Mh[gid] : 0.f, Mb = (gid + 8 < g) ? Mh[gid + 8] : 0.f;
-            for (int tile = warp; tile * 16 < n; tile += FCW) {
-                const int tb = tile * 16;
-                float pv[2][4];  // [k-half][a-rows]: (gid,2t),(gid,2t+1),(gid+8,2t),(gid+8,2t+1)
-#pragma unroll
-                for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int rr = tb + kh * 8 + 2 * t + e;
-                        const bool ok = rr < n;
-                        const float* lr = logits + (ok ? att[r0 + rr] : 0) * NCP;
-                        pv[kh][e] = (ok && gid < g && Ma != -INFINITY) ? fast_exp2(lr[gid] - Ma) : 0.f;
-                        pv[kh][2 + e] = (ok && gid + 8 < g && Mb != -INFINITY) ? fast_exp2(lr[gid + 8] - Mb) : 0.f;
-                    }
+        SVL_TRACE(5);
+        if (warp < D / 16) {
+            const int mi = lane >> 3, rin = lane & 7;
+            const uint32_t aph = smem_u32(pth), apl = smem_u32(ptl);
+            for (int tb = 0; tb < nr; tb += 16) {
+                // P fragment (m = heads, k = rows): matrices (h0-7,k0-7) (h8-15,k0-7) (h0-7,k8-15) (h8-15,k8-15)
+                const int prow = tb + (mi >> 1) * 8 + rin;
                 uint32_t ph[4], pl[4];
-                {
-                    const float v[4][2] = {{pv[0][0], pv[0][1]}, {pv[0][2], pv[0][3]},
-                                           {pv[1][0], pv[1][1]}, {pv[1][2], pv[1][3]}};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        ph[i] = pack_bf16(v[i][0], v[i][1]);
-                        pl[i] = pack_bf16(v[i][0] - bf16lo(ph[i]), v[i][1] - bf16hi(ph[i]));
-                    }
-                }
-                const int mi = lane >> 3, rin = lane & 7;
+                ldsm_x4_trans(aph + prow * 32 + (mi & 1) * 16, ph[0], ph[1], ph[2], ph[3]);
+                ldsm_x4_trans(apl + prow * 32 + (mi & 1) * 16, pl[0], pl[1], pl[2], pl[3]);
                 const int vrow = tb + (mi & 1) * 8 + rin;
-#pragma unroll
-                for (int j = 0; j < NVT / 2; ++j) {
-                    const int c = 2 * j + (mi >> 1);
-                    uint32_t v0r, v1r, v2r, v3r;
-                    ldsm_x4_trans(vbuf + vrow * ROWB + swz_v(vrow, c) * 16, v0r, v1r, v2r, v3r);
-                    mma_bf16_16816(o[2 * j], ph, v0r, v1r);
-                    mma_bf16_16816(o[2 * j], pl, v0r, v1r);
-                    mma_bf16_16816(o[2 * j + 1], ph, v2r, v3r);
-                    mma_bf16_16816(o[2 * j + 1], pl, v2r, v3r);
-                }
+                const int c = 2 * warp + (mi >> 1);
+                uint32_t v0r, v1r, v2r, v3r;
+                ldsm_x4_trans(vst + vrow * GM::VROWB + c * 16, v0r, v1r, v2r, v3r);
+                mma_bf16_16816(o[0], ph, v0r, v1r);
+                mma_bf16_16816(o[0], pl, v0r, v1r);
+                mma_bf16_16816(o[1], ph, v2r, v3r);
+                mma_bf16_16816(o[1], pl, v2r, v3r);
             }
         }
-        __syncthreads();  // batch buffer free for batch bi + 2
+        __syncthreads();  // staging + P table free for the next batch
     }
     SVL_TRACE(6);
-    // warp partials -> CTA O (fixed warp order); ring [0, 64K) as [FCW][16][D]
-    float* wo = reinterpret_cast<float*>(smem);
-    if (warp < FCW) {
+    float* lred = reinterpret_cast<float*>(smem + GM::LRED_OFF);
+    float* octa = reinterpret_cast<float*>(smem + GM::OCTA_OFF);  // [16][D]
+    lred[tid] = lacc;
+    if (warp < D / 16) {
 #pragma unroll
-        for (int n = 0; n < NVT; ++n) {
-            const int col = n * 8 + 2 * t;
-            *reinterpret_cast<float2*>(wo + (warp * 16 + gid) * D + col) = make_float2(o[n][0], o[n][1]);
-            *reinterpret_cast<float2*>(wo + (warp * 16 + gid + 8) * D + col) = make_float2(o[n][2], o[n][3]);
+        for (int nt = 0; nt < 2; ++nt) {
+            const int col = warp * 16 + nt * 8 + 2 * t;
+            if (gid < g) *reinterpret_cast<float2*>(octa + gid * D + col) = make_float2(o[nt][0], o[nt][1]);
+            if (gid + 8 < g) *reinterpret_cast<float2*>(octa + (gid + 8) * D + col) = make_float2(o[nt][2], o[nt][3]);
         }
     }
     __syncthreads();
-    float* octa = reinterpret_cast<float*>(smem + GM::OCTA_OFF);  // [16][D]
-    for (int i = tid; i < g * D; i += FT) {
-        const int h = i / D, dd = i % D;
+    if (tid < 16) {
         float acc = 0.f;
-#pragma unroll
-        for (int w = 0; w < FCW; ++w) acc += wo[(w * 16 + h) * D + dd];
-        octa[h * D + dd] = acc;
+        for (int j = 0; j < FT / 16; ++j) acc += lred[j * 16 + tid];
+        lh[tid] = acc;
     }
-    // ------------------------------------------------ 6. cluster merge
+    // ------------------------------------------------ 5. cluster merge (plain sums)
     SVL_TRACE(7);
     cl.sync();
     SVL_TRACE(8);
@@ -464,36 +449,28 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     const int per = (items + CS - 1) / CS;
     for (int i = rank * per + tid; i < min(items, (rank + 1) * per); i += FT) {
         const int h = i / D, dd = i % D;
-        // all 3 x CS remote loads issued before any use (one DSMEM round trip)
-        float mq[16], oq[16], lq[16];
+        float oq[16], lq[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            mq[q] = (q < CS) ? cl.map_shared_rank(Mh, q)[h] : -INFINITY;
+        for (int q = 0; q < 16; ++q) {  // all remote loads issued before use
             oq[q] = (q < CS) ? cl.map_shared_rank(octa, q)[h * D + dd] : 0.f;
             lq[q] = (q < CS) ? cl.map_shared_rank(lh, q)[h] : 0.f;
         }
-        float M = -INFINITY;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) M = fmaxf(M, mq[q]);
         float num = 0.f, den = 0.f;
-        if (M != -INFINITY) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                if (mq[q] != -INFINITY) {
-                    const float w = exp2f(mq[q] - M);
-                    num += w * oq[q];
-                    den += w * lq[q];
-                }
-            }
+        for (int q = 0; q < 16; ++q) {
+            num += oq[q];
+            den += lq[q];
         }
         const int hh = G * g + h;
         p.out[((int64_t)b * p.H + hh) * D + dd] = (den > 0.f) ? num / den : 0.f;
-        if (dd == 0 && p.lse_out) p.lse_out[(int64_t)b * p.H + hh] = (den > 0.f) ? (M + log2f(den)) * kLn2 : -INFINITY;
+        if (dd == 0 && p.lse_out)
+            p.lse_out[(int64_t)b * p.H + hh] = (den > 0.f) ? (lse2[h] + log2f(den)) * kLn2 : -INFINITY;
     }
-    (void)cnt;
+    (void)ibc;
     SVL_TRACE(9);
     cl.sync();  // peers may still read this CTA's shared memory until here
     SVL_TRACE(10);
+    if (p.trace && tid < 32) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + tid] = trs[tid];
 #undef SVL_TRACE
 }
 

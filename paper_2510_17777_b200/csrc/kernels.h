@@ -86,7 +86,7 @@ struct FreshParams {
     uint64_t* trace;   // debug: per-CTA phase timestamps (SVL_TRACE=1), else null
 };
 constexpr int kFusedThreads = 512;    // 8 stream-consumer warps + 1 TMA producer warp + 7 helper warps
-constexpr int kFusedTextMax = 256;    // text rows per CTA
+constexpr int kFusedTextMax = 128;    // text rows per CTA
 constexpr int kFusedSliceMax = 2048;  // visual rows per CTA (halved for g > 8)
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
 

@@ -1,0 +1,346 @@
+// select_fast.cuh -- the fused kernel's relevance top-k, latency-trimmed.
+//
+// Same result as cluster_topk_push (select_push.cuh): the k largest relevance
+// scores of a unit spread over the cluster, ties to the lower index, the kept
+// indices written ascending.  Two cluster barriers in the common case:
+//   histogram_and_threshold: keys (score -> order-preserving uint32) and a
+//     256-bin value-adaptive histogram (float exponent 101..132 x 3 mantissa
+//     bits; relevance scores are <= n_q*g <= 32) in one pass over the CTA's
+//     logits; histogram pushed to every peer; cluster barrier; every CTA sums
+//     the 16 histograms and finds the bin b* holding the k-th key;
+//   assign_slots_and_push_candidates: rows at or above b* get decode V slots
+//     (the caller starts their gather right away), the keys of b* (they share
+//     key bits 31..20) are pushed to every peer in index order; cluster
+//     barrier;
+//   resolve_and_emit: every CTA resolves the exact cut inside b* with one
+//     local 8-bit radix pass (bits 19..12) and an exact ranking within the
+//     final sub-bin (key desc, index asc), derives every CTA's output offset
+//     from the gathered counts, and writes its kept indices.
+// If b* is the catch-all bin 0 or a CTA holds more than 64 keys of b*, the
+// generic exact radix of select_push.cuh takes over (generic_or_trivial).
+// Per-row state after the selection: 2 (kKeySel) = kept, 0 = not kept.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "select_push.cuh"
+
+namespace svl {
+
+constexpr int kFastCandPerCta = 64;
+constexpr int kFastSub = 256;  // sub-bin members ranked by a short list
+
+struct FastSelSmem {
+    uint32_t allhist[16][256];
+    uint2 cand[16][kFastCandPerCta];
+    uint32_t hist[256];
+    uint32_t tot[256];
+    uint32_t cnt_q[16], above_q[16], sel_q[16];
+    uint32_t sel2[16][kFastCandPerCta / 32];
+    uint2 sub[kFastSub];
+    uint32_t warp_sums[32];
+    uint32_t bcast[16];
+    uint8_t cflag[16][kFastCandPerCta];
+};
+
+SVL_DEV int rel_digit(uint32_t key) {  // == push_digit(key, 0, .)
+    const int e = (int)((key >> 23) & 0xffu);
+    const int b = (e - 101) * 8 + (int)((key >> 20) & 7u);
+    return (key & 0x80000000u) ? min(max(b, 0), 255) : 0;
+}
+
+// one warp: bin of the need-th largest over NB ascending bins
+template <int NB>
+__device__ __noinline__ void warp_find_nb(const uint32_t* bins, uint32_t need, uint32_t* out) {
+    constexpr int PER = NB / 32;
+    const int lane = threadIdx.x & 31;
+    uint32_t c[PER];
+    uint32_t grp = 0u;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        c[i] = bins[lane * PER + i];
+        grp += c[i];
+    }
+    uint32_t suf = grp;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, suf, off);
+        if (lane + off < 32) suf += y;
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, suf >= need);
+    const int lstar = ball ? 31 - __clz(ball) : 0;
+    if (lane == lstar) {
+        uint32_t above = suf - grp;
+        int b = lane * PER;
+#pragma unroll
+        for (int i = PER - 1; i >= 0; --i) {
+            if (above + c[i] >= need) {
+                b = lane * PER + i;
+                break;
+            }
+            above += c[i];
+        }
+        out[0] = (uint32_t)b;
+        out[1] = above;
+    }
+}
+
+template <int NTH, int NCP>
+struct FastSelect {
+    cg::cluster_group& cl;
+    FastSelSmem& s;
+    const float* logits;
+    const float* lse2;
+    int g, nvis, v0, slice, nv, k;
+    uint32_t* keys;
+    uint8_t* state;
+    uint32_t* flags;
+    uint32_t* whist;  // [NTH/32][256] private histograms (scratch, dead after the push)
+    int bstar = 0;
+    uint32_t krem = 0;
+    uint64_t* tr = nullptr;  // debug stamps (SVL_TRACE)
+
+    SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmem& s_, const float* logits_, const float* lse2_,
+                       int g_, int nvis_, int v0_, int slice_, int nv_, int k_, uint32_t* keys_,
+                       uint8_t* state_, uint32_t* flags_, uint32_t* whist_)
+        : cl(cl_), s(s_), logits(logits_), lse2(lse2_), g(g_), nvis(nvis_), v0(v0_), slice(slice_),
+          nv(nv_), k(k_), keys(keys_), state(state_), flags(flags_), whist(whist_) {}
+
+    // contiguous ownership for slots / emit: thread tid handles rows [i0, i1)
+    SVL_DEV void my_rows(int& i0, int& i1) const {
+        const int E = (nvis + NTH - 1) / NTH;
+        i0 = min(nvis, (int)threadIdx.x * E);
+        i1 = min(nvis, i0 + E);
+    }
+
+    // returns 0 (trivial k), 1 (fast path) or 2 (generic path)
+    SVL_DEV int histogram_and_threshold() {
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+        if (k <= 0 || k >= nv) return 0;
+        for (int i = tid; i < (NTH / 32) * 256; i += NTH) whist[i] = 0u;
+        __syncthreads();
+        {
+            float nl[NCP];
+#pragma unroll
+            for (int c = 0; c < NCP; ++c) nl[c] = (c < g) ? lse2[c] : INFINITY;
+            bool nan_seen = false;
+            uint32_t* my = whist + warp * 256;
+#pragma unroll 2
+            for (int i = tid; i < nvis; i += NTH) {
+                const float4* lr = reinterpret_cast<const float4*>(logits + i * NCP);
+                float sc = 0.f;
+#pragma unroll
+                for (int c4 = 0; c4 < NCP / 4; ++c4) {
+                    const float4 x = lr[c4];
+                    sc += fast_exp2(x.x - nl[4 * c4]) + fast_exp2(x.y - nl[4 * c4 + 1]) +
+                          fast_exp2(x.z - nl[4 * c4 + 2]) + fast_exp2(x.w - nl[4 * c4 + 3]);
+                }
+                const uint32_t key = float_key(sc, nan_seen);
+                keys[i] = key;
+                atomicAdd(&my[rel_digit(key)], 1u);
+            }
+            if (nan_seen) raise_flag(flags, 2u /*NONFINITE*/);
+        }
+        stamp(tr, 8);
+        __syncthreads();
+        stamp(tr, 9);
+        // fold the private histograms and push bin b straight to every peer
+        for (int b = tid; b < 256; b += NTH) {
+            uint32_t acc = 0u;
+#pragma unroll
+            for (int w = 0; w < NTH / 32; ++w) acc += whist[w * 256 + b];
+            s.hist[b] = acc;
+        }
+        __syncthreads();
+        for (int i = tid; i < CS * 64; i += NTH) {
+            const int q = i >> 6, c = i & 63;
+            reinterpret_cast<uint4*>(cl.map_shared_rank(&s.allhist[rank][0], q))[c] =
+                reinterpret_cast<const uint4*>(s.hist)[c];
+        }
+        stamp(tr, 10);
+        cl.sync();
+        stamp(tr, 11);
+        for (int b = tid; b < 256; b += NTH) {
+            uint32_t v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = (q < CS) ? s.allhist[q][b] : 0u;
+            uint32_t acc = 0u;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc += v[q];
+            s.tot[b] = acc;
+        }
+        __syncthreads();
+        if (warp == 0) warp_find_nb<256>(s.tot, (uint32_t)k, s.bcast);
+        __syncthreads();
+        stamp(tr, 12);
+        bstar = (int)s.bcast[0];
+        krem = (uint32_t)k - s.bcast[1];
+        for (int q = warp; q < CS; q += NTH / 32) {
+            uint32_t a = 0u;
+            for (int b = bstar + 1 + lane; b < 256; b += 32) a += s.allhist[q][b];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+            if (lane == 0) {
+                s.above_q[q] = a;
+                s.cnt_q[q] = s.allhist[q][bstar];
+                s.sel_q[q] = 0u;
+            }
+        }
+        __syncthreads();
+        uint32_t maxc = 0u;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
+        return (bstar == 0 || maxc > (uint32_t)kFastCandPerCta) ? 2 : 1;
+    }
+
+    // V slots for every row with digit >= b* (att_sel[slot] = local row, in
+    // index order); keys of b* pushed to the peers; returns the slot count.
+    SVL_DEV int assign_slots_and_push_candidates(int* att_sel) {
+        const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+        int i0, i1;
+        my_rows(i0, i1);
+        uint32_t ge = 0u, eq = 0u;
+        for (int i = i0; i < i1; ++i) {
+            const int d = rel_digit(keys[i]);
+            ge += d >= bstar;
+            eq += d == bstar;
+        }
+        uint32_t tot;
+        const uint32_t pre = block_scan_excl<NTH>(ge | (eq << 16), s.warp_sums, &tot);
+        uint32_t pge = pre & 0xffffu, peq = pre >> 16;
+        for (int i = i0; i < i1; ++i) {
+            const uint32_t key = keys[i];
+            const int d = rel_digit(key);
+            uint8_t st = 0;
+            if (d >= bstar) att_sel[pge++] = i;
+            if (d == bstar) {
+                st = (uint8_t)(peq + 1);
+                const uint2 c = make_uint2(key, (uint32_t)(v0 + i));
+                for (int q = 0; q < CS; ++q) cl.map_shared_rank(&s.cand[rank][0], q)[peq] = c;
+                ++peq;
+            }
+            state[i] = st;
+        }
+        cl.sync();
+        return (int)(tot & 0xffffu);
+    }
+
+    SVL_DEV void resolve_and_emit(int32_t* idx_out) {
+        const int tid = threadIdx.x, warp = tid >> 5;
+        const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+        // one radix pass on key bits 19..12 over all candidates
+        for (int i = tid; i < 256; i += NTH) s.hist[i] = 0u;
+        if (tid == 0) s.bcast[6] = 0u;
+        __syncthreads();
+        for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
+            const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
+            if (q < CS && (uint32_t)j < s.cnt_q[q]) atomicAdd(&s.hist[(s.cand[q][j].x >> 12) & 255u], 1u);
+        }
+        __syncthreads();
+        stamp(tr, 0);
+        if (warp == 0) warp_find_nb<256>(s.hist, krem, s.bcast + 4);
+        __syncthreads();
+        stamp(tr, 1);
+        const uint32_t bA = s.bcast[4];
+        const uint32_t need = krem - s.bcast[5];  // keys to keep inside sub-bin bA (>= 1)
+        // (no shared atomics here: fire-and-forget ATOMS on a few hot counters
+        // serialise and stall every later shared access of the CTA by microseconds)
+        static_assert(kFastCandPerCta % 32 == 0 && NTH % kFastCandPerCta == 0, "one q per warp");
+        // the members of sub-bin bA (usually a handful) compacted into sub[]
+        const uint32_t nsub = s.hist[bA];
+        if (nsub <= (uint32_t)kFastSub) {
+            for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
+                const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
+                if (q < CS && (uint32_t)j < s.cnt_q[q]) {
+                    const uint2 c = s.cand[q][j];
+                    if (((c.x >> 12) & 255u) == bA) s.sub[atomicAdd(&s.bcast[6], 1u)] = c;
+                }
+            }
+            __syncthreads();
+        }
+        for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
+            const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
+            bool take = false;
+            if (q < CS && (uint32_t)j < s.cnt_q[q]) {
+                const uint2 c = s.cand[q][j];
+                const uint32_t dA = (c.x >> 12) & 255u;
+                take = dA > bA;
+                if (dA == bA) {  // exact rank inside the sub-bin: (key desc, index asc)
+                    uint32_t r = 0u;
+                    if (nsub <= (uint32_t)kFastSub) {
+                        for (uint32_t i = 0; i < nsub; ++i) {
+                            const uint2 d = s.sub[i];
+                            r += d.x > c.x || (d.x == c.x && d.y < c.y);
+                        }
+                    } else {
+                        for (int q2 = 0; q2 < CS; ++q2)
+                            for (uint32_t j2 = 0; j2 < s.cnt_q[q2]; ++j2) {
+                                const uint2 d = s.cand[q2][j2];
+                                r += (((d.x >> 12) & 255u) == bA) && (d.x > c.x || (d.x == c.x && d.y < c.y));
+                            }
+                    }
+                    take = r < need;
+                }
+                s.cflag[q][j] = take;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, take);
+            if ((tid & 31) == 0) s.sel2[q][j >> 5] = (uint32_t)__popc(bal);
+        }
+        __syncthreads();
+        if (tid < 16) s.sel_q[tid] = s.sel2[tid][0] + s.sel2[tid][1];
+        __syncthreads();
+        stamp(tr, 2);
+        uint32_t off = 0u;
+        for (int q = 0; q < rank; ++q) off += s.above_q[q] + s.sel_q[q];
+        int i0, i1;
+        my_rows(i0, i1);
+        stamp(tr, 5);
+        uint32_t mine = 0u;
+        for (int i = i0; i < i1; ++i) {
+            const int d = rel_digit(keys[i]);
+            mine += (d > bstar) || (d == bstar && s.cflag[rank][state[i] - 1]);
+        }
+        uint32_t tot;
+        stamp(tr, 3);
+        uint32_t pos = off + block_scan_excl<NTH>(mine, s.warp_sums, &tot);
+        stamp(tr, 4);
+        for (int i = i0; i < i1; ++i) {
+            const int d = rel_digit(keys[i]);
+            const bool kept = (d > bstar) || (d == bstar && s.cflag[rank][state[i] - 1]);
+            if (kept) idx_out[pos++] = v0 + i;
+            state[i] = kept ? kKeySel : kKeyOut;
+        }
+    }
+
+    // stage 0: k <= 0 or k >= nv; stage 2: generic exact radix.  Writes
+    // idx_out, att_sel (kept local rows in index order) and state; returns
+    // the CTA's kept count.
+    SVL_DEV int generic_or_trivial(int stage, PushTopkSmem& ps, int32_t* idx_out, int* att_sel) {
+        const int tid = threadIdx.x;
+        if (stage == 0) {
+            const bool all = k >= nv;
+            for (int i = tid; i < nvis; i += NTH) {
+                state[i] = all ? kKeySel : kKeyOut;
+                if (all) {
+                    idx_out[v0 + i] = v0 + i;
+                    att_sel[i] = i;
+                }
+            }
+            __syncthreads();
+            return all ? nvis : 0;
+        }
+        uint32_t off;
+        const int nsel = (int)cluster_topk_push<NTH>(cl, ps, keys, state, nvis, v0, slice, nv, k,
+                                                     /*relevance=*/true, &off);
+        push_emit<NTH>(ps, state, nvis, off, [&](int i, uint32_t slot) {
+            idx_out[slot] = v0 + i;
+            att_sel[slot - off] = i;
+        });
+        __syncthreads();
+        return nsel;
+    }
+};
+
+}  // namespace svl

@@ -1,4 +1,5 @@
-"""Phase timeline of the fused fresh-step kernel (SVL_TRACE=1 debug stamps)."""
+"""Phase timeline of the fused fresh-step kernel (SVL_TRACE=1 debug stamps).
+usage: python tools/trace_fresh.py [config]"""
 import os, sys
 os.environ["SVL_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -18,17 +19,28 @@ for it in range(6):
 tr = ws.buf[256:256 + (1 << 20)].view(torch.int64)[: 2048 * 32].view(-1, 32).cpu()
 tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
-names = ["start", "stream", "lse", "keys", "topk", "emit+M", "V+PV", "Ored", "merge-sync", "merge", "end", "keys#1"]
+names = {0: "start", 1: "stream+textV", 2: "lse", 3: "hist+thr", 4: "select", 5: "Ptab+Vwait", 6: "PV", 7: "O+l",
+         8: "merge-sync", 9: "merge", 10: "end", 11: "assign+push", 12: "gather-issue"}
 print(f"{name}: {tr.shape[0]} CTAs; phase end times (us, min/median/max over CTAs, from first start)")
-for ph in range(12):
-    v = (tr[:, ph] - t0).double() / 1e3
-    print(f"  {ph:2d} {names[ph]:10s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
-cyc = (tr[:, 13] - tr[:, 12]).double()
-ns = (tr[:, 3] - tr[:, 2]).double()
-print("keys phase: cycles median", cyc.median().item(), "ns median", ns.median().item(), "=> GHz", (cyc / ns).median().item())
+for ph, nm in names.items():
+    col = tr[:, ph]
+    if (col == 0).any():
+        continue
+    v = (col - t0).double() / 1e3
+    print(f"  {ph:2d} {nm:10s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
 
-tn = ["push1", "sync1", "find1", "state1", "candpush+sync", "kth", "flags", "end"]
-print("topk internals (us from keys end, median over CTAs):")
-for j, nm in enumerate(tn):
-    v = (tr[:, 16 + j] - tr[:, 3]).double() / 1e3
-    print(f"   {nm:14s} {v.median().item():8.2f}")
+sub = ["cand-hist", "find", "flags", "mine", "scan", "off", "-", "-", "-", "-", "-", "-", "-"]
+print("resolve internals (us from gather-issue, median):")
+for j, nm in enumerate(sub):
+    col = tr[:, 16 + j]
+    if (col == 0).any():
+        continue
+    print(f"   {nm:10s} {((col - tr[:, 12]).double() / 1e3).median().item():8.2f}")
+
+hsub = {8: "keys+hist", 9: "hist-sync", 10: "fold+push", 11: "cl.sync", 12: "sum+find"}
+print("histogram internals (us from lse stamp, median):")
+for j, nm in hsub.items():
+    col = tr[:, 16 + j]
+    if (col == 0).any():
+        continue
+    print(f"   {nm:10s} {((col - tr[:, 2]).double() / 1e3).median().item():8.2f}")
