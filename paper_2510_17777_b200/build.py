@@ -21,11 +21,16 @@ ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libsparsevila.so")
 BUILD = os.path.join(ROOT, "build", "obj")
+# experiment builds: SVL_VARIANT=name SVL_DEFS="-DX=1 ..." -> build/<name>/libsparsevila.so
+VARIANT = os.environ.get("SVL_VARIANT")
+if VARIANT:
+    BUILD = os.path.join(ROOT, "build", VARIANT)
+    LIB = os.path.join(BUILD, "libsparsevila.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I", INCLUDE, "-I", CSRC]
+         "-I", INCLUDE, "-I", CSRC] + os.environ.get("SVL_DEFS", "").split()
 
 
 def _deps():

@@ -111,6 +111,37 @@ static int plan_splits(int units, int n_att_max, int sms) {
 
 using namespace svl;
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static const EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+namespace svl {
+bool encode_kv_tensor_map(CUtensorMap* map, const void* data, int d, int capacity, int Hkv, int B,
+                          int64_t stride_b, int64_t stride_h, int64_t stride_t, int box_rows) {
+    const EncodeTiledFn fn = encode_fn();
+    if (!fn || d % 64 || stride_t <= 0 || stride_h <= 0 || stride_b <= 0) return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)capacity, (cuuint64_t)Hkv, (cuuint64_t)B};
+    const cuuint64_t strides[3] = {(cuuint64_t)stride_t * 2, (cuuint64_t)stride_h * 2, (cuuint64_t)stride_b * 2};
+    const cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(data), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace svl
+
 extern "C" {
 
 const char* svl_version(void) { return "libsparsevila 0.1 sm_100a (tensor-core mma.sync swap-AB, cluster radix select)"; }
@@ -342,6 +373,7 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
 
 // ----------------------------------------------------- fused fresh step
 // Cluster size and eligibility of the fused kernel for a shape.
+
 static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice) {
     if (g > 16) return false;
     const int smax = kFusedSliceMax / ((g + 7) / 8);
@@ -402,7 +434,9 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
     if (st != SVL_OK) return st;
 
     int CS, slice;
-    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice)) {
+    FreshParams p;
+    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice) ||
+        !encode_kv_tensor_map(&p.ktmap, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 128)) {
         // outside the on-chip budget: the two separate calls (same q as [B][1][H][d])
         st = svl_retrieve(q, B, 1, H, Hkv, d, K, span, nullptr, k, scale, flags, idx_out, nullptr,
                           ws, ws_bytes, stream);
@@ -410,7 +444,6 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
         return svl_sparse_decode_attn(q, B, H, Hkv, d, K, V, span, idx_out, k, 0u, scale, out,
                                       lse_out, ws, ws_bytes, stream);
     }
-    FreshParams p;
     p.q = static_cast<const uint16_t*>(q);
     p.K = static_cast<const uint16_t*>(K.data);
     p.ksb = K.stride_b; p.ksh = K.stride_h; p.kst = K.stride_t;

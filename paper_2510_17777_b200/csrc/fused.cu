@@ -45,51 +45,61 @@ namespace svl {
 namespace {
 
 constexpr int FT = kFusedThreads;  // 512
-constexpr int FCW = 8;             // stream consumer warps (warp FCW = TMA producer)
-constexpr int STAGE_ROWS = 128;
-constexpr int RING = 128 * 1024;
+constexpr int STAGE_ROWS = 128;    // = UMMA M: one K stage is one tcgen05.mma row block
+#ifndef SVL_RING_KB
+#define SVL_RING_KB 192
+#endif
+constexpr int RING = SVL_RING_KB * 1024;
 constexpr int TMAX = kFusedTextMax;
+constexpr int UMMA_N = 16;        // q columns per KV group (g <= 16, zero padded)
+constexpr int TMEM_COLS = 256;    // 16 visual stages x UMMA_N fp32 accumulator columns
 
 template <int D, int NT>
 struct FGeom {
     static constexpr int NCP = 8 * NT;
     static constexpr int SMAX = kFusedSliceMax / NT;
-    static constexpr int NST = 512 / D;  // ring stages of 32 KB
     static constexpr int ROWB = 2 * D;
     static constexpr int STAGE_BYTES = STAGE_ROWS * ROWB;
+    static constexpr int NST = RING / STAGE_BYTES;  // ring stages
+    static_assert(SMAX / STAGE_ROWS * UMMA_N <= TMEM_COLS, "visual stages fit the TMEM allocation");
     // persistent regions
-    static constexpr int LOG_OFF = RING;
-    static constexpr int LOG_BYTES = (SMAX + TMAX) * NCP * 4;
-    static constexpr int ATT_OFF = LOG_OFF + LOG_BYTES;  // V slot -> local row
+    static constexpr int QT_OFF = RING;                        // q tile [16][D], K-major SW128 (UMMA B)
+    static constexpr int QT_BYTES = UMMA_N * ROWB;
+    static constexpr int TXL_OFF = QT_OFF + QT_BYTES;          // text-row logits [TMAX][NCP] fp32
+    static constexpr int ATT_OFF = TXL_OFF + TMAX * NCP * 4;   // V slot -> local row
     static constexpr int ATT_BYTES = (SMAX + TMAX) * 4;
     static constexpr int MISC_OFF = ATT_OFF + ATT_BYTES;
-    static constexpr int MISC_BYTES = 2 * NST * 8 + 8 + FCW * NCP * 8 + 16 * NCP * 8 + NCP * 4 + 16 * 4 + 64 * 4 + 32 * 8;
+    static constexpr int NVS_MAX = SMAX / STAGE_ROWS;
+    static constexpr int MISC_BYTES = 2 * NST * 8 + NVS_MAX * 8 + 8 + 8 + 16 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
+                                      16 * 4 + 64 * 4 + 64 * 8;
     static constexpr int BYTES = MISC_OFF + MISC_BYTES;
     // ring re-use once streaming is over
-    static constexpr int SEL_OFF = 0;                     // FastSelSmem
-    static constexpr int KEYS_OFF = 32 * 1024;            // keys [SMAX]
-    static constexpr int STATE_OFF = KEYS_OFF + SMAX * 4; // per-row state [SMAX]
-    static constexpr int VST_OFF = 44 * 1024;             // V staging [VCAP][D], rows padded by 16 B
-    static constexpr int VROWB = ROWB + 16;               // (conflict-free ldmatrix without a swizzle)
-    static constexpr int VCAP = ((RING - VST_OFF) / VROWB) / 16 * 16 > 320 ? 320 : ((RING - VST_OFF) / VROWB) / 16 * 16;
-    static constexpr int PUSH_OFF = VST_OFF;              // generic top-k scratch (fallback only)
-    static constexpr int WHIST_OFF = RING - 16 * 1024;    // private histograms (before any selected-row V)
+    static constexpr int SEL_OFF = 0;                      // FastSelSmem
+    static constexpr int KEYS_OFF = 44 * 1024;             // keys [SMAX]; then slot_of [SMAX] uint16
+    static constexpr int STATE_OFF = KEYS_OFF + SMAX * 4;  // per-row state [SMAX]
+    static constexpr int VST_OFF = 56 * 1024;              // V staging [VCAP][D], rows padded by 16 B
+    static constexpr int VROWB = ROWB + 16;                // (conflict-free ldmatrix without a swizzle)
+    static constexpr int VCAP = ((RING - VST_OFF) / VROWB) / 16 * 16 > 512 ? 512 : ((RING - VST_OFF) / VROWB) / 16 * 16;
+    static constexpr int PUSH_OFF = VST_OFF;               // generic top-k scratch (fallback only)
+    static constexpr int WHIST_OFF = RING - 16 * 1024;     // private histograms (before any selected-row V)
     static_assert(VST_OFF + TMAX * VROWB <= WHIST_OFF, "text-row V below the private histograms");
-    static constexpr int PT_OFF = 0;                      // P table hi + lo [VCAP][16] (after top-k)
+    static constexpr int PT_OFF = 0;                       // P table hi + lo [VCAP][16] (after top-k)
     static constexpr int OCTA_OFF = PT_OFF + 2 * VCAP * 16 * 2;  // CTA O [16][D] fp32
     static constexpr int LRED_OFF = OCTA_OFF + 16 * D * 4;       // [FT] fp32
     static_assert(STATE_OFF + SMAX <= VST_OFF, "keys + state below the V staging");
     static_assert(VST_OFF + VCAP * VROWB <= RING, "V staging inside the ring");
-    static_assert(LRED_OFF + FT * 4 <= VST_OFF, "P table / O / l scratch below the V staging");
+    static_assert(LRED_OFF + FT * 4 <= KEYS_OFF, "P table / O / l scratch below keys, state, slot_of");
+    static_assert(RING % 1024 == 0 && QT_OFF % 1024 == 0, "128-B swizzle atoms are 1024-B aligned");
 };
 
 
 template <int D, int NT>
-__global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
+__global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ FreshParams p) {
     using GM = FGeom<D, NT>;
     constexpr int NCP = GM::NCP, NST = GM::NST, ROWB = GM::ROWB, VCAP = GM::VCAP;
     constexpr int NCH = D / 32;  // 16-byte chunks per thread per row (permuted contraction)
     constexpr int CH = D / 8;    // 16-byte chunks per row
+    constexpr uint32_t IDESC = umma_idesc_bf16(STAGE_ROWS, UMMA_N);
     static_assert(sizeof(FastSelSmem) <= GM::KEYS_OFF, "fast top-k scratch");
     static_assert(GM::PUSH_OFF + sizeof(PushTopkSmem) <= RING, "generic top-k scratch");
     static_assert(GM::BYTES <= 227 * 1024, "shared memory budget");
@@ -99,25 +109,31 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     const int CS = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gid = lane >> 2, t = lane & 3;
+    const int q4 = warp & 3;  // this warp's TMEM lane quarter (rows 32*q4 .. 32*q4+31 of a stage)
     const int u = blockIdx.y;
     const int b = u / p.Hkv, G = u % p.Hkv;
     const int g = p.g;
 
-    float* logits = reinterpret_cast<float*>(smem + GM::LOG_OFF);
+    float* txl = reinterpret_cast<float*>(smem + GM::TXL_OFF);
     int* att = reinterpret_cast<int*>(smem + GM::ATT_OFF);
     uint8_t* misc = smem + GM::MISC_OFF;
-    uint64_t* full = reinterpret_cast<uint64_t*>(misc);
-    uint64_t* empty = full + NST;
-    uint64_t* vbar = empty + NST;                                // V gathers (TMA bulk, per row)
-    float2* wpart = reinterpret_cast<float2*>(vbar + 1);         // [FCW][NCP]
-    float2* allpart = wpart + FCW * NCP;                         // [16][NCP] pushed by the peers
+    uint64_t* full = reinterpret_cast<uint64_t*>(misc);  // K stage landed
+    uint64_t* empty = full + NST;                         // K stage consumed by the tensor core
+    uint64_t* accf = empty + NST;                         // [NVS_MAX] stage i's accumulator in TMEM (single use)
+    uint64_t* tbar = accf + GM::NVS_MAX;                  // text stage landed (single use)
+    uint64_t* vbar = tbar + 1;                            // V gathers (TMA variant)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
+    float2* wpart = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(vbar + 1) + 16);  // [16][NCP]
+    float2* allpart = wpart + (FT / 32) * NCP;                   // [16][NCP] pushed by the peers
     float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
     float* lh = lse2 + NCP;                                      // [16]
     int* ibc = reinterpret_cast<int*>(lh + 16);                  // broadcasts
     uint64_t* trs = reinterpret_cast<uint64_t*>(ibc + 64);       // debug stamps (SVL_TRACE), flushed at exit
     const uint32_t ring = smem_u32(smem);
     const uint32_t vst = ring + GM::VST_OFF;
+    const uint32_t qt = ring + GM::QT_OFF;
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(smem + GM::KEYS_OFF);
+    uint16_t* slot_of = reinterpret_cast<uint16_t*>(smem + GM::KEYS_OFF);  // after the top-k
     uint8_t* state_s = smem + GM::STATE_OFF;
     FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(smem + GM::SEL_OFF);
 #define SVL_TRACE(ph)                                                                     \
@@ -126,8 +142,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                          \
         trs[(ph)] = tnow;                                                                 \
     }
-    if (p.trace && tid < 32) trs[tid] = 0;
+    if (p.trace && tid < 64) trs[tid] = 0;
     SVL_TRACE(0);
+    if (p.trace && tid == 0) trs[30] = clock64();
 
     // ------------------------------------------------------------ geometry
     int L = p.seq_len[b];
@@ -145,8 +162,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         if (tid == 0) raise_flag(p.flags, 4u /*SPAN*/);
         ntext = TMAX;
     }
-    const int nwork = nvis + ntext;
-    const int nstages = (nwork + STAGE_ROWS - 1) / STAGE_ROWS;
+    // visual stages (tiled TMA, 128-B swizzle, tcgen05), then <= 1 text stage (plain rows, mma.sync)
+    static_assert(TMAX <= STAGE_ROWS, "text rows fit one stage");
+    const int nvs = (nvis + STAGE_ROWS - 1) / STAGE_ROWS;
+    const int nstages = nvs + (ntext > 0 ? 1 : 0);
     const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
     const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
     auto work_row = [&](int w) {  // local work row -> cache row
@@ -154,125 +173,240 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         const int tt = t0 + (w - nvis);
         return tt < p.vb ? tt : tt + p.nv;
     };
-    // V gather of slots [s0, s1) (slot -> local row in att[]): one TMA bulk copy
-    // per row, issued by many threads, completion counted on vbar (the single
-    // arrival of a phase carries the phase's total byte count; completions may
-    // precede it).  The TMA engine does the gather: the LSUs stay free.
     const uint32_t vbar_a = smem_u32(vbar);
+#ifndef SVL_VGATHER_CPASYNC
+#define SVL_VGATHER_CPASYNC 1  // measured: 30.9 vs 32.3 us/layer for TMA row copies (long-video)
+#endif
+#if SVL_VGATHER_CPASYNC
+    // V gather of slots [s0, s1) (slot -> local row in att[]): cp.async 16-B chunks
+    // over all 512 threads (LSU path); completion per thread (wait_group) + a CTA barrier
     auto gather_rows = [&](int s0, int s1, int base) {
-        for (int sl = s0 + tid; sl < s1; sl += FT)
-            bulk_g2s(vst + (sl - base) * GM::VROWB, Vb + (int64_t)work_row(att[sl]) * p.vst, ROWB, vbar_a);
+        for (int e = tid; e < (s1 - s0) * CH; e += FT) {
+            const int sl = s0 + e / CH, c = e % CH;
+            cp_async16(vst + (sl - base) * GM::VROWB + c * 16, Vb + (int64_t)work_row(att[sl]) * p.vst + c * 8, true);
+        }
+        cp_async_commit();
     };
+    auto v_expect = [&](uint32_t) {};
+    auto v_wait = [&](uint32_t) {
+        cp_async_wait<0>();
+        __syncthreads();
+    };
+#else
+    // one TMA bulk copy per row, one issuing lane per warp (a bulk copy is a
+    // uniform-datapath instruction: 32 active lanes would issue serially)
+    auto gather_rows = [&](int s0, int s1, int base) {
+        if (lane == 0)
+            for (int sl = s0 + warp; sl < s1; sl += FT / 32)
+                bulk_g2s(vst + (sl - base) * GM::VROWB, Vb + (int64_t)work_row(att[sl]) * p.vst, ROWB, vbar_a);
+    };
+    auto v_expect = [&](uint32_t bytes) {
+        if (tid == 0) mbar_arrive_expect_tx(vbar_a, bytes);
+    };
+    auto v_wait = [&](uint32_t ph) { mbar_wait(vbar_a, ph); };
+#endif
 
+    // ------------------------------------------------ 1. stream K, logits -> TMEM
+    // Visual stage i = cache rows vb + v0 + [128 i, 128 i + 128), loaded by the
+    // tiled TMA (tensor map, 128-B swizzle) into ring slot i % NST; one
+    // tcgen05.mma chain (M = 128 rows, N = 16 q columns, K = d) writes its dot
+    // products to TMEM columns [16 i, 16 i + 16) -- the logits stay there for
+    // the whole kernel (no shared-memory copy, so the ring can be deep).
+    // Warp roles: w0 lane 0 = TMA producer, w1 lane 0 = MMA issuer, w2 = TMEM
+    // owner, w4-7 = running LSE of the visual stages (one TMEM lane quarter
+    // each), w8-15 = the text stage (plain rows, mma.sync; logits to smem).
+    const int nsys = max(0, min(ntext, p.vb - t0));
+    auto issue = [&](int i) {
+        const int slot = i % NST;
+        const uint32_t dst0 = ring + slot * GM::STAGE_BYTES;
+        if (i < nvs) {
+            const uint32_t bar = smem_u32(&full[slot]);
+            // 128 visual rows x D: D/64 boxes of 128 rows x 128 B (rows past the slice
+            // are loaded and ignored; past the capacity the TMA zero-fills)
+            mbar_arrive_expect_tx(bar, (uint32_t)GM::STAGE_BYTES);
+#pragma unroll
+            for (int hf = 0; hf < D / 64; ++hf)
+                tma_load_4d(dst0 + hf * (STAGE_ROWS * 128), &p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b, bar);
+            return;
+        }
+        // text rows [t0, t0 + ntext): system rows, then after-visual rows; completion
+        // on the single-use tbar (a far-future phase of full[slot] would be ambiguous)
+        const uint32_t bar = smem_u32(tbar);
+        mbar_arrive_expect_tx(bar, (uint32_t)(ntext * ROWB));
+        const int seg_n[2] = {nsys, ntext - nsys};
+        const int seg_row0[2] = {t0, t0 + nsys + p.nv};
+        int w = 0;
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+            if (seg_n[sg] <= 0) continue;
+            if (p.kst == D) {
+                bulk_g2s(dst0 + w * ROWB, Kb + (int64_t)seg_row0[sg] * p.kst, (uint32_t)(seg_n[sg] * ROWB), bar);
+            } else {
+                for (int r = 0; r < seg_n[sg]; ++r)
+                    bulk_g2s(dst0 + (w + r) * ROWB, Kb + (int64_t)(seg_row0[sg] + r) * p.kst, ROWB, bar);
+            }
+            w += seg_n[sg];
+        }
+    };
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), FCW);
+            mbar_init(smem_u32(&empty[s]), 1);
         }
+        for (int s = 0; s < GM::NVS_MAX; ++s) mbar_init(smem_u32(&accf[s]), 1);
+        mbar_init(smem_u32(tbar), 1);
         mbar_init(vbar_a, 1);
         fence_mbar_init();
+        for (int i = 0; i < min(NST, nstages); ++i) issue(i);
     }
+    if (warp == 2) tmem_alloc(smem_u32(tslot), TMEM_COLS);
+    // q tile (UMMA B operand): row c = head G*g + c (zero for c >= g), K-major,
+    // 128-B swizzle: chunk j of row r in half h at h*16*128 + r*128 + ((j ^ (r & 7)) << 4)
+    for (int e = tid; e < UMMA_N * CH; e += FT) {
+        const int r = e / CH, cf = e % CH, hf = cf >> 3, c = cf & 7;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < g) v = reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.H + G * g + r) * D)[cf];
+        *reinterpret_cast<uint4*>(smem + GM::QT_OFF + hf * (UMMA_N * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+    const bool text_in_lse = !(p.flags_in & 1u /*VISUAL_ONLY*/);
 
-    // ------------------------------------------------ 1. stream K, logits
-    if (warp == FCW) {
+    if (warp == 0) {
+        if (lane == 0)  // producer: refill a slot once the tensor core has consumed it
+            for (int i = NST; i < nstages; ++i) {
+                mbar_wait(smem_u32(&empty[i % NST]), ((i / NST) - 1) & 1);
+                issue(i);
+            }
+        __syncwarp();
+    } else if (warp == 1) {
         if (lane == 0) {
-            // the work list is <= 3 contiguous row segments: visual slice, system
-            // text, after-visual text; each stage is their intersection with it
-            const int nsys = max(0, min(ntext, p.vb - t0));
-            const int seg_w0[3] = {0, nvis, nvis + nsys};
-            const int seg_w1[3] = {nvis, nvis + nsys, nwork};
-            const int seg_row0[3] = {p.vb + v0, t0, t0 + nsys + p.nv};  // cache row of the segment start
-            const bool dense = (p.kst == D);
-            const int64_t kst = p.kst;
-            for (int i = 0; i < nstages; ++i) {
+            for (int i = 0; i < nvs; ++i) {
                 const int slot = i % NST;
-                if (i >= NST) mbar_wait(smem_u32(&empty[slot]), ((i / NST) - 1) & 1);
-                const int w0 = i * STAGE_ROWS, w1 = min(nwork, w0 + STAGE_ROWS);
-                const uint32_t bar = smem_u32(&full[slot]);
-                mbar_arrive_expect_tx(bar, (uint32_t)((w1 - w0) * ROWB));
-                const uint32_t dst0 = ring + slot * GM::STAGE_BYTES;
+                mbar_wait(smem_u32(&full[slot]), (i / NST) & 1);
+                tc_fence_after();
+                if (p.trace && i < 32) {
+                    uint64_t tnow;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                    trs[32 + i] = tnow;
+                }
+                const uint32_t sb = ring + slot * GM::STAGE_BYTES;
+#if !SVL_EXP_NOMATH  // timing experiment: stream only
 #pragma unroll
-                for (int sg = 0; sg < 3; ++sg) {
-                    const int a = max(w0, seg_w0[sg]), z = min(w1, seg_w1[sg]);
-                    if (a >= z) continue;
-                    const int row = seg_row0[sg] + (a - seg_w0[sg]);
-                    if (dense) {
-                        bulk_g2s(dst0 + (a - w0) * ROWB, Kb + (int64_t)row * kst, (uint32_t)((z - a) * ROWB), bar);
-                    } else {
-                        for (int w = a; w < z; ++w)
-                            bulk_g2s(dst0 + (w - w0) * ROWB, Kb + (int64_t)(row + w - a) * kst, ROWB, bar);
-                    }
+#ifndef SVL_EXP_MMA_STEPS
+#define SVL_EXP_MMA_STEPS (D / 16)
+#endif
+                for (int j = 0; j < SVL_EXP_MMA_STEPS; ++j) {  // K = 16 per instruction
+                    const int hf = j >> 2, kk = j & 3;
+                    umma_bf16(tbase + i * UMMA_N, sw128_desc(sb + hf * (STAGE_ROWS * 128) + kk * 32),
+                              sw128_desc(qt + hf * (UMMA_N * 128) + kk * 32), IDESC, j > 0 ? 1u : 0u);
+                }
+#endif
+                umma_commit(smem_u32(&empty[slot]));
+                umma_commit(smem_u32(&accf[i]));
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4 && warp < 8) {
+        // running (max, sum) of the visual logits, one TMEM lane (= stage row) per thread
+        float rm[NCP], rl[NCP];
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) rm[c] = -INFINITY, rl[c] = 0.f;
+        for (int i = 0; i < nvs; ++i) {
+            mbar_wait(smem_u32(&accf[i]), 0);
+            tc_fence_after();
+            uint32_t v[16];
+            tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, v);
+            if (i * STAGE_ROWS + q4 * 32 + lane < nvis) {
+#pragma unroll
+                for (int c = 0; c < NCP; ++c) {
+                    const float x = __uint_as_float(v[c]) * p.scale2;
+                    const float M = fmaxf(rm[c], x);
+                    rl[c] = rl[c] * fast_exp2(rm[c] - M) + fast_exp2(x - M);
+                    rm[c] = M;
                 }
             }
         }
-    } else if (warp < FCW) {
-        // query B fragments: column c = head G*g + c (c < g), same chunk layout as K
-        uint4 bq[NT][NCH];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const int col = nt * 8 + gid;
+        for (int c = 0; c < NCP; ++c) {
 #pragma unroll
-            for (int i = 0; i < NCH; ++i) bq[nt][i] = make_uint4(0, 0, 0, 0);
-            if (col < g) {
-                const uint4* qr = reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.H + G * g + col) * D);
-#pragma unroll
-                for (int i = 0; i < NCH; ++i) bq[nt][i] = qr[t + 4 * i];
+            for (int off = 1; off < 32; off <<= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, rm[c], off);
+                const float l2 = __shfl_xor_sync(0xffffffffu, rl[c], off);
+                const float M = fmaxf(rm[c], m2);
+                if (M != -INFINITY) {
+                    rl[c] = rl[c] * fast_exp2(rm[c] - M) + l2 * fast_exp2(m2 - M);
+                    rm[c] = M;
+                }
             }
+            if (lane == 0) wpart[warp * NCP + c] = make_float2(rm[c], rl[c]);
         }
+    } else if (warp >= 8) {
+        // text stage: 8 warps x 16 rows, mma.sync (swap-AB, permuted contraction)
+        const int wig = warp - 8, r16 = wig * 16;
         float rm[NT][2], rl[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) rm[nt][0] = rm[nt][1] = -INFINITY, rl[nt][0] = rl[nt][1] = 0.f;
-        const bool text_in_lse = !(p.flags_in & 1u /*VISUAL_ONLY*/);
-        for (int i = 0; i < nstages; ++i) {
-            const int slot = i % NST;
-            mbar_wait(smem_u32(&full[slot]), (i / NST) & 1);
-            const int tb = i * STAGE_ROWS + warp * 16;
-            if (tb < nwork) {
-                const uint32_t base = ring + slot * GM::STAGE_BYTES + (warp * 16 + gid) * ROWB;
-                float acc[NT][4];
+        if (ntext > 0 && r16 < ntext) {
+            uint4 bq[NT][NCH];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+            for (int nt = 0; nt < NT; ++nt) {
+                const int col = nt * 8 + gid;
 #pragma unroll
-                for (int c4 = 0; c4 < NCH; ++c4) {
-                    const uint4 ra = lds128(base + (t + 4 * c4) * 16);
-                    const uint4 rb = lds128(base + 8 * ROWB + (t + 4 * c4) * 16);
-                    const uint32_t a0[4] = {ra.x, rb.x, ra.y, rb.y};
-                    const uint32_t a1[4] = {ra.z, rb.z, ra.w, rb.w};
+                for (int i = 0; i < NCH; ++i) bq[nt][i] = make_uint4(0, 0, 0, 0);
+                if (col < g) {
+                    const uint4* qr = reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.H + G * g + col) * D);
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        mma_bf16_16816(acc[nt], a0, bq[nt][c4].x, bq[nt][c4].y);
-                        mma_bf16_16816(acc[nt], a1, bq[nt][c4].z, bq[nt][c4].w);
-                    }
+                    for (int i = 0; i < NCH; ++i) bq[nt][i] = qr[t + 4 * i];
                 }
-                const int wa = tb + gid, wb = wa + 8;
-                const bool va = wa < nwork, vbv = wb < nwork;
-                const bool la = va && (wa < nvis || text_in_lse);
-                const bool lb = vbv && (wb < nvis || text_in_lse);
+            }
+            const int slot = nvs % NST;
+            mbar_wait(smem_u32(tbar), 0);
+            const uint32_t base = ring + slot * GM::STAGE_BYTES + (r16 + gid) * ROWB;
+            float acc[NT][2][4];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) acc[nt][h][0] = acc[nt][h][1] = acc[nt][h][2] = acc[nt][h][3] = 0.f;
+#pragma unroll
+            for (int c4 = 0; c4 < NCH; ++c4) {
+                const uint4 ra = lds128(base + (t + 4 * c4) * 16);
+                const uint4 rb = lds128(base + 8 * ROWB + (t + 4 * c4) * 16);
+                const uint32_t a0[4] = {ra.x, rb.x, ra.y, rb.y};
+                const uint32_t a1[4] = {ra.z, rb.z, ra.w, rb.w};
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
-                    const float x0 = acc[nt][0] * p.scale2, x1 = acc[nt][1] * p.scale2;
-                    const float x2 = acc[nt][2] * p.scale2, x3 = acc[nt][3] * p.scale2;
-                    if (va) *reinterpret_cast<float2*>(logits + wa * NCP + nt * 8 + 2 * t) = make_float2(x0, x1);
-                    if (vbv) *reinterpret_cast<float2*>(logits + wb * NCP + nt * 8 + 2 * t) = make_float2(x2, x3);
+                    mma_bf16_16816(acc[nt][c4 & 1], a0, bq[nt][c4].x, bq[nt][c4].y);
+                    mma_bf16_16816(acc[nt][c4 & 1], a1, bq[nt][c4].z, bq[nt][c4].w);
+                }
+            }
+            const int ra_ = r16 + gid, rb_ = ra_ + 8;
+            const bool va = ra_ < ntext, vbv = rb_ < ntext;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const float x0 = (acc[nt][0][0] + acc[nt][1][0]) * p.scale2;
+                const float x1 = (acc[nt][0][1] + acc[nt][1][1]) * p.scale2;
+                const float x2 = (acc[nt][0][2] + acc[nt][1][2]) * p.scale2;
+                const float x3 = (acc[nt][0][3] + acc[nt][1][3]) * p.scale2;
+                if (va) *reinterpret_cast<float2*>(txl + ra_ * NCP + nt * 8 + 2 * t) = make_float2(x0, x1);
+                if (vbv) *reinterpret_cast<float2*>(txl + rb_ * NCP + nt * 8 + 2 * t) = make_float2(x2, x3);
+                if (text_in_lse) {
 #pragma unroll
                     for (int e2 = 0; e2 < 2; ++e2) {
-                        const float ya = la ? (e2 ? x1 : x0) : -INFINITY;
-                        const float yb = lb ? (e2 ? x3 : x2) : -INFINITY;
+                        const float ya = va ? (e2 ? x1 : x0) : -INFINITY;
+                        const float yb = vbv ? (e2 ? x3 : x2) : -INFINITY;
                         const float mx = fmaxf(ya, yb);
                         if (mx != -INFINITY) {
-                            const float M = fmaxf(rm[nt][e2], mx);
-                            rl[nt][e2] = rl[nt][e2] * fast_exp2(rm[nt][e2] - M) + fast_exp2(ya - M) +
-                                         fast_exp2(yb - M);
-                            rm[nt][e2] = M;
+                            rm[nt][e2] = mx;
+                            rl[nt][e2] = fast_exp2(ya - mx) + fast_exp2(yb - mx);
                         }
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
         }
-        // (max, sum) of each column over this warp
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -290,7 +424,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
                 if (gid == 0) wpart[warp * NCP + nt * 8 + 2 * t + e2] = make_float2(rm[nt][e2], rl[nt][e2]);
             }
     }
-    __syncthreads();  // ring drained (every stage was consumed)
+    if (warp < 4)
+        for (int c = lane; c < NCP; c += 32) wpart[warp * NCP + c] = make_float2(-INFINITY, 0.f);
+    __syncthreads();  // ring drained: every MMA completed (accf waited), text stage consumed
 
     // text rows' V: V slots [0, ntext); their gather overlaps everything up to the decode
     for (int i = tid; i < ntext; i += FT) att[i] = nvis + i;
@@ -307,7 +443,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
         }
     };
     if (warp < NCP) {  // warp c folds column c (fixed shuffle tree), lanes push to the peers
-        float2 x = (lane < FCW) ? wpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
+        float2 x = (lane < FT / 32) ? wpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
 #pragma unroll
         for (int off = 1; off < 16; off <<= 1) {
             const float m2 = __shfl_xor_sync(0xffffffffu, x.x, off);
@@ -329,30 +465,51 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     }
     __syncthreads();
     SVL_TRACE(2);
+    // per-thread copies of the normalisers (+inf pads: exp2(x - inf) = 0)
+    float nl[NCP];
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) nl[c] = (c < g) ? lse2[c] : INFINITY;
 
     // ------------------------------------------------ 3. top-k (+ early V gather)
     int32_t* idx_out = p.idx_out + (int64_t)u * p.k;
-    FastSelect<FT, NCP> sel(cl, fs, logits, lse2, g, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags,
-                            reinterpret_cast<uint32_t*>(smem + GM::WHIST_OFF));
+    FastSelect<FT> sel(cl, fs, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags,
+                       reinterpret_cast<uint32_t*>(smem + GM::WHIST_OFF));
     if (p.trace) sel.tr = trs + 16;
     int nslots = ntext;
     uint32_t vphase = 0;
-    const int stage = sel.histogram_and_threshold();  // 0 = all / none, 1 = fast path, 2 = generic
+    int stage = 0;  // 0 = all / none, 1 = fast path, 2 = generic
+    if (!sel.trivial()) {
+        sel.zero_hist();
+        __syncthreads();
+        // relevance of each visual row = its share of the softmax mass, summed over the g heads
+        for (int i = warp >> 2; i < nvs; i += FT / 128) {
+            uint32_t v[16];
+            tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, v);
+            const int row = i * STAGE_ROWS + q4 * 32 + lane;
+            if (row < nvis) {
+                float sc = 0.f;
+#pragma unroll
+                for (int c = 0; c < NCP; ++c) sc += fast_exp2(__uint_as_float(v[c]) * p.scale2 - nl[c]);
+                sel.add_key(row, sc);
+            }
+        }
+        stage = sel.threshold();
+    }
     SVL_TRACE(3);
     if (stage == 1) {
         // every row at or above the threshold bin gets a V slot now (superset of the kept rows)
         nslots = ntext + sel.assign_slots_and_push_candidates(att + ntext);
         SVL_TRACE(11);
         gather_rows(ntext, min(nslots, VCAP), 0);
-        if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(min(nslots, VCAP) * ROWB));
+        v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
         SVL_TRACE(12);
         sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
     } else {
         if (stage == 2) {
             // the generic scratch aliases the V staging: every CTA's text-row gather
             // must land before any peer pushes into it (text rows are re-gathered)
-            if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(ntext * ROWB));
-            mbar_wait(vbar_a, 0);
+            v_expect((uint32_t)(ntext * ROWB));
+            v_wait(0);
             vphase = 1;
             cl.sync();
         }
@@ -360,47 +517,82 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
                                                 idx_out, att + ntext);
         nslots = ntext + nsel;
         gather_rows(stage == 2 ? 0 : ntext, min(nslots, VCAP), 0);
-        if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(min(nslots, VCAP) * ROWB));
+        v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
     }
     SVL_TRACE(4);
 
     // ------------------------------------------------ 4. decode over the kept rows
     // p = exp2(s2 - LSE2[h]): the same reference in every CTA -> plain-sum merge.
-    const int hmine = tid & 15;  // FT % 16 == 0: thread tid always handles head tid % 16
-    const float lse_mine = (hmine < g) ? lse2[hmine] : 0.f;
-    float lacc = 0.f;
+    float lacc = 0.f;  // thread tid sums head tid % 16 (FT % 16 == 0)
     float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::PT_OFF);
     uint16_t* ptl = pth + VCAP * 16;
-    __syncthreads();  // top-k scratch (aliased by the P table) is dead
+    __syncthreads();  // top-k scratch (aliased by the P table and slot_of) is dead
+    for (int sl = ntext + tid; sl < nslots; sl += FT) slot_of[att[sl]] = (uint16_t)sl;
     for (int s0 = 0; s0 < nslots; s0 += VCAP) {
         const int n = min(VCAP, nslots - s0);
         const int nr = (n + 15) & ~15;
         if (s0 > 0) {  // overflow batches (rare): after the previous PV
             gather_rows(s0, s0 + n, s0);
-            if (tid == 0) mbar_arrive_expect_tx(vbar_a, (uint32_t)(n * ROWB));
+            v_expect((uint32_t)(n * ROWB));
         }
-        for (int i = tid; i < nr * 16; i += FT) {
-            const int rr = i >> 4;
-            float pv = 0.f;
-            if (rr < n && hmine < g) {
-                const int r = att[s0 + rr];
-                if (r >= nvis || state_s[r] == kKeySel) pv = fast_exp2(logits[r * NCP + hmine] - lse_mine);
+        // P table rows [0, nr): zero, then the text rows and the kept visual rows
+        for (int i = tid; i < nr * 2; i += FT) {  // 16 heads x 2 B = 32 B = 2 uint4 per row and table
+            reinterpret_cast<uint4*>(pth)[i] = make_uint4(0, 0, 0, 0);
+            reinterpret_cast<uint4*>(ptl)[i] = make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+        for (int i = tid; i < (min(ntext, s0 + n) - s0) * 16; i += FT) {
+            const int rr = i >> 4, h = i & 15;
+            if (h < g) {
+                const float pv = fast_exp2(txl[(att[s0 + rr] - nvis) * NCP + h] - lse2[h]);
+                const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+                const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+                pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
+                ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
             }
-            lacc += pv;
-            const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
-            const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
-            pth[i] = *reinterpret_cast<const uint16_t*>(&hi);
-            ptl[i] = *reinterpret_cast<const uint16_t*>(&lo);
+        }
+        for (int i = warp >> 2; i < nvs; i += FT / 128) {
+            const int row = i * STAGE_ROWS + q4 * 32 + lane;
+            const bool kept = row < nvis && state_s[row] == kKeySel;
+            if (!__any_sync(0xffffffffu, kept)) continue;
+            uint32_t v[16];
+            tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, v);
+            const int rr = kept ? (int)slot_of[row] - s0 : -1;
+            if (rr >= 0 && rr < n) {
+                uint32_t hw[8], lw[8];
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    float pv2[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int c = 2 * c2 + e;
+                        pv2[e] = (c < NCP) ? fast_exp2(__uint_as_float(v[c]) * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
+                    }
+                    hw[c2] = pack_bf16(pv2[0], pv2[1]);
+                    lw[c2] = pack_bf16(pv2[0] - bf16lo(hw[c2]), pv2[1] - bf16hi(hw[c2]));
+                }
+                uint4* dh = reinterpret_cast<uint4*>(pth + rr * 16);
+                uint4* dl = reinterpret_cast<uint4*>(ptl + rr * 16);
+                dh[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                dh[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+                dl[0] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                dl[1] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+            }
         }
         // rows [n, nr) of the staging buffer: zero V (the P rows are zero, avoid NaN * 0)
         for (int i = n * CH + tid; i < nr * CH; i += FT) {
             const int rr = i / CH, c = i % CH;
             *reinterpret_cast<uint4*>(smem + GM::VST_OFF + rr * GM::VROWB + c * 16) = make_uint4(0, 0, 0, 0);
         }
-        mbar_wait(vbar_a, vphase);
+        v_wait(vphase);
         vphase ^= 1u;
         __syncthreads();
+        // denominators from the table itself (hi + lo: the weights the PV uses)
+        for (int i = tid; i < nr * 16; i += FT) {
+            const uint32_t hv = pth[i], lv = ptl[i];
+            lacc += __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
+        }
         SVL_TRACE(5);
         if (warp < D / 16) {
             const int mi = lane >> 3, rin = lane & 7;
@@ -468,9 +660,15 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const FreshParams p) {
     }
     (void)ibc;
     SVL_TRACE(9);
+    tc_fence_before();
     cl.sync();  // peers may still read this CTA's shared memory until here
     SVL_TRACE(10);
-    if (p.trace && tid < 32) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 + tid] = trs[tid];
+    if (p.trace && tid == 0) trs[31] = clock64();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tbase, TMEM_COLS);
+    }
+    if (p.trace && tid < 64) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + tid] = trs[tid];
 #undef SVL_TRACE
 }
 

@@ -2,6 +2,7 @@
 // (api.cu) and the kernels.  Not part of the public ABI.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -69,6 +70,7 @@ struct DecodeParams {
 };
 
 struct FreshParams {
+    CUtensorMap ktmap;  // K as 4-D {d, capacity, Hkv, B}, box {64, 128, 1, 1}, 128-B swizzle
     const uint16_t* q;  // [B][H][d] -- retrieval query == decode query
     const uint16_t* K;
     int64_t ksb, ksh, kst;
@@ -87,7 +89,10 @@ struct FreshParams {
 };
 constexpr int kFusedThreads = 512;    // 8 stream-consumer warps + 1 TMA producer warp + 7 helper warps
 constexpr int kFusedTextMax = 128;    // text rows per CTA
-constexpr int kFusedSliceMax = 2048;  // visual rows per CTA (halved for g > 8)
+#ifndef SVL_SLICE_MAX
+#define SVL_SLICE_MAX 2048
+#endif
+constexpr int kFusedSliceMax = SVL_SLICE_MAX;  // visual rows per CTA (halved for g > 8)
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
 
 struct SalienceParams {
@@ -123,5 +128,11 @@ inline cudaError_t set_max_carveout(K kern) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 int select_cluster_size(int n);  // CTAs per selection unit for n keys
+
+// K (or V) cache view as a 4-D TMA tensor map {d, capacity, Hkv, B} (strides in
+// elements), box {64, box_rows, 1, 1}, 128-byte swizzle.  False if the driver
+// entry point is missing or the view is not encodable (the caller falls back).
+bool encode_kv_tensor_map(CUtensorMap* map, const void* data, int d, int capacity, int Hkv, int B,
+                          int64_t stride_b, int64_t stride_h, int64_t stride_t, int box_rows);
 
 }  // namespace svl

@@ -86,26 +86,24 @@ __device__ __noinline__ void warp_find_nb(const uint32_t* bins, uint32_t need, u
     }
 }
 
-template <int NTH, int NCP>
+template <int NTH>
 struct FastSelect {
     cg::cluster_group& cl;
     FastSelSmem& s;
-    const float* logits;
-    const float* lse2;
-    int g, nvis, v0, slice, nv, k;
+    int nvis, v0, slice, nv, k;
     uint32_t* keys;
     uint8_t* state;
     uint32_t* flags;
     uint32_t* whist;  // [NTH/32][256] private histograms (scratch, dead after the push)
     int bstar = 0;
     uint32_t krem = 0;
+    bool nan_seen = false;
     uint64_t* tr = nullptr;  // debug stamps (SVL_TRACE)
 
-    SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmem& s_, const float* logits_, const float* lse2_,
-                       int g_, int nvis_, int v0_, int slice_, int nv_, int k_, uint32_t* keys_,
-                       uint8_t* state_, uint32_t* flags_, uint32_t* whist_)
-        : cl(cl_), s(s_), logits(logits_), lse2(lse2_), g(g_), nvis(nvis_), v0(v0_), slice(slice_),
-          nv(nv_), k(k_), keys(keys_), state(state_), flags(flags_), whist(whist_) {}
+    SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmem& s_, int nvis_, int v0_, int slice_, int nv_, int k_,
+                       uint32_t* keys_, uint8_t* state_, uint32_t* flags_, uint32_t* whist_)
+        : cl(cl_), s(s_), nvis(nvis_), v0(v0_), slice(slice_), nv(nv_), k(k_), keys(keys_), state(state_),
+          flags(flags_), whist(whist_) {}
 
     // contiguous ownership for slots / emit: thread tid handles rows [i0, i1)
     SVL_DEV void my_rows(int& i0, int& i1) const {
@@ -114,35 +112,23 @@ struct FastSelect {
         i1 = min(nvis, i0 + E);
     }
 
-    // returns 0 (trivial k), 1 (fast path) or 2 (generic path)
-    SVL_DEV int histogram_and_threshold() {
+    SVL_DEV bool trivial() const { return k <= 0 || k >= nv; }
+
+    // 1. (caller) zero_hist(); barrier; add_key(i, score) for every local row; then threshold()
+    SVL_DEV void zero_hist() {
+        for (int i = threadIdx.x; i < (NTH / 32) * 256; i += NTH) whist[i] = 0u;
+    }
+    SVL_DEV void add_key(int i, float score) {
+        const uint32_t key = float_key(score, nan_seen);
+        keys[i] = key;
+        atomicAdd(&whist[(threadIdx.x >> 5) * 256 + rel_digit(key)], 1u);
+    }
+
+    // returns 1 (fast path) or 2 (generic path); all threads, after the add_key pass
+    SVL_DEV int threshold() {
         const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
         const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-        if (k <= 0 || k >= nv) return 0;
-        for (int i = tid; i < (NTH / 32) * 256; i += NTH) whist[i] = 0u;
-        __syncthreads();
-        {
-            float nl[NCP];
-#pragma unroll
-            for (int c = 0; c < NCP; ++c) nl[c] = (c < g) ? lse2[c] : INFINITY;
-            bool nan_seen = false;
-            uint32_t* my = whist + warp * 256;
-#pragma unroll 2
-            for (int i = tid; i < nvis; i += NTH) {
-                const float4* lr = reinterpret_cast<const float4*>(logits + i * NCP);
-                float sc = 0.f;
-#pragma unroll
-                for (int c4 = 0; c4 < NCP / 4; ++c4) {
-                    const float4 x = lr[c4];
-                    sc += fast_exp2(x.x - nl[4 * c4]) + fast_exp2(x.y - nl[4 * c4 + 1]) +
-                          fast_exp2(x.z - nl[4 * c4 + 2]) + fast_exp2(x.w - nl[4 * c4 + 3]);
-                }
-                const uint32_t key = float_key(sc, nan_seen);
-                keys[i] = key;
-                atomicAdd(&my[rel_digit(key)], 1u);
-            }
-            if (nan_seen) raise_flag(flags, 2u /*NONFINITE*/);
-        }
+        if (nan_seen) raise_flag(flags, 2u /*NONFINITE*/);
         stamp(tr, 8);
         __syncthreads();
         stamp(tr, 9);

@@ -15,7 +15,7 @@ from typing import Optional
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsparsevila.so")
+LIB_PATH = os.environ.get("SVL_LIB") or os.path.join(HERE, "libsparsevila.so")  # SVL_LIB: experiment builds
 
 SVL_OK = 0
 SVL_NORM_VISUAL_ONLY = 1

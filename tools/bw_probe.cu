@@ -120,6 +120,43 @@ int main() {
         const double us = ms * 1e3 / (20 * 28);
         printf("graph 28x32MiB %s SMs %3d: %.2f us per launch, %.1f GB/s\n", mode == 0 ? "bulk" : "ldg ", nsm, us, per * nsm / (us * 1e-6) / 1e9);
     }
+    // cluster placement: 64 / 128 CTAs launched as clusters of CS (bulk, 6 x 32 KB)
+    cudaFuncSetAttribute(bulk_kernel<6, 32768>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int nsm : {64, 128}) for (int cs : {1, 2, 4, 8, 16}) {
+        const size_t bytes = 32ull << 20;
+        const size_t per = (bytes / nsm) / 32768 * 32768;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nsm);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = 6 * 32768;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int maxc = -1;
+        cudaOccupancyMaxActiveClusters(&maxc, bulk_kernel<6, 32768>, &cfg);
+        cudaGraph_t g; cudaGraphExec_t ge;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+        for (int l = 0; l < 28; ++l) {
+            const uint8_t* src = buf + (size_t)l * (bytes + (1 << 20));
+            cudaLaunchKernelEx(&cfg, bulk_kernel<6, 32768>, src, per, sink);
+        }
+        cudaStreamEndCapture(st, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+        for (int w = 0; w < 3; ++w) cudaGraphLaunch(ge, st);
+        cudaEventRecord(a, st);
+        for (int r = 0; r < 20; ++r) cudaGraphLaunch(ge, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        const double us = ms * 1e3 / (20 * 28);
+        printf("graph 28x32MiB bulk CTAs %3d cluster %2d (max active clusters %d): %.2f us per launch, %.1f GB/s  err=%s\n", nsm, cs, maxc, us,
+               per * nsm / (us * 1e-6) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
     // empty kernels in a graph: per-launch floor
     {
         cudaGraph_t g; cudaGraphExec_t ge;
