@@ -99,11 +99,10 @@ static RetrieveLayout retrieve_layout(int B, int Hkv, int nv, const ScorePlan& p
 
 // --------------------------------------------------------------- decode plan
 static int plan_splits(int units, int n_att_max, int sms) {
-    int S = std::max(1, (n_att_max + kDecodeRowsMax - 1) / kDecodeRowsMax);
-    const int fill = (sms + units - 1) / units;  // at least one CTA per SM
-    S = std::max(S, fill);
-    S = std::min(S, std::max(1, n_att_max));
-    S = std::min(S, kMergeMaxSplits);
+    // CTAs per unit = cluster size: the largest power of two <= 16 that keeps the
+    // grid within ~2 waves, and at least one 16-row tile per CTA
+    int S = 16;
+    while (S > 1 && (units * S > 2 * sms || S * 16 > n_att_max)) S >>= 1;
     return S;
 }
 
@@ -305,11 +304,9 @@ size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32
                                         int32_t visual_len, int32_t capacity, uint32_t flags) {
     (void)flags;
     if (B < 1 || Hkv < 1 || H % Hkv || capacity < 1) return 0;
-    const int units = B * Hkv, g = H / Hkv;
-    const int vb_max = capacity - visual_len;  // conservative: rows outside the visual span
-    const int n_att_max = std::max(1, k + std::max(0, vb_max));
-    const int S = plan_splits(units, n_att_max, device_sm_count());
-    return round_up(kWsHeader + (size_t)units * S * g * (d + 2) * sizeof(float), 256);
+    (void)d; (void)k; (void)visual_len;
+    // flag word only: the split merge is on chip (cluster DSMEM); + debug trace
+    return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
 }
 
 svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
@@ -342,11 +339,8 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
 
     const int units = B * Hkv;
     const int n_att_max = std::max(1, k + std::max(0, K.capacity - span.visual_len));
-    if (n_att_max > kMergeMaxSplits * kDecodeRowsMax)
-        return fail(SVL_ERR_UNSUPPORTED, "more than 131072 attended rows per (b, KV head)%s");
     const int S = plan_splits(units, n_att_max, device_sm_count());
-    const size_t need = round_up(kWsHeader + (size_t)units * S * g * (d + 2) * sizeof(float), 256);
-    if (ws_bytes < need) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    if (ws_bytes < kWsHeader) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
 
     DecodeParams p;
     p.q = static_cast<const uint16_t*>(q);
@@ -362,10 +356,12 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
     p.capacity = K.capacity;
     p.S = S;
     p.scale2 = scale * kLog2e;
-    p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kWsHeader);
     p.out = out;
     p.lse_out = lse_out;
     p.flags = static_cast<uint32_t*>(ws);
+    p.trace = (getenv("SVL_TRACE") && ws_bytes >= kWsHeader + ((size_t)1 << 20))
+                  ? reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader)
+                  : nullptr;
     cudaError_t e = launch_decode(p, d, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "svl_sparse_decode_attn");
     return SVL_OK;

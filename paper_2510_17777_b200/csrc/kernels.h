@@ -61,12 +61,12 @@ struct DecodeParams {
     const int32_t* seq_len;
     const int32_t* idx;  // [B][U][k]
     int B, H, Hkv, g, vb, nv, k, shared, capacity;
-    int S;         // splits per unit
+    int S;         // splits per unit = CTAs of the unit's cluster (<= 16)
     float scale2;  // scale * log2(e)
-    float* part;   // [units][S][g][d+2] : o (unnormalised), m (base 2), l
     float* out;    // [B][H][d]
     float* lse_out;
     uint32_t* flags;
+    uint64_t* trace;  // debug: per-CTA phase timestamps (SVL_TRACE=1), else null
 };
 
 struct FreshParams {
@@ -109,9 +109,8 @@ struct SalienceParams {
 constexpr int kScoreThreads = 512;
 constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA
-constexpr int kDecodeThreads = 128;
-constexpr int kDecodeRowsMax = 128;  // rows staged per decode CTA
-constexpr int kMergeMaxSplits = 1024;  // => <= 131072 attended rows per unit
+constexpr int kDecodeThreads = 256;  // 8 warps x one 16-row tile per batch
+constexpr int kDecodeRowsMax = 128;  // rows per double-buffered gather batch
 
 cudaError_t launch_score(const ScoreParams& p, int d, int NT, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s);

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t ph) {
@@ -24,8 +25,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t ph) {
 constexpr int ROWB = 256;
 constexpr int NT = 512;
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 template <int M>
-__global__ void __launch_bounds__(NT, 1) gather_kernel(const uint8_t* V, const int* idx, int R, const __grid_constant__ CUtensorMap tmap, unsigned* sink) {
+__global__ void __launch_bounds__(NT, 1) gather_kernel(const uint8_t* V, const int* idx, int R, const __grid_constant__ CUtensorMap tmap, unsigned* sink, uint64_t* tdur) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
@@ -36,7 +42,8 @@ __global__ void __launch_bounds__(NT, 1) gather_kernel(const uint8_t* V, const i
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     __syncthreads();
-    if (M == 0 || M == 1 || M == 4) {
+    const uint64_t tstart = gtimer();
+    if (M == 0 || M == 1 || M == 4 || M == 5 || M == 6) {
         if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(b), "r"(R * ROWB) : "memory");
         if (M == 0) {
             for (int r = tid; r < R; r += NT)
@@ -47,10 +54,18 @@ __global__ void __launch_bounds__(NT, 1) gather_kernel(const uint8_t* V, const i
                 for (int r = tid; r < R; r += 32)
                     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sm + r * ROWB)),
                                  "l"(V + (size_t)my[r] * ROWB), "r"(ROWB), "r"(b) : "memory");
+        } else if (M == 5) {  // bulk per row, lane 0 of every warp
+            if ((tid & 31) == 0)
+                for (int r = tid >> 5; r < R; r += NT / 32)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(sm + r * ROWB)),
+                                 "l"(V + (size_t)my[r] * ROWB), "r"(ROWB), "r"(b) : "memory");
         } else {
             // 4 rows x 64 cols (128 B) per request; two requests per 4-row group (cols 0, 64)
-            if (tid < 32)
-                for (int q = tid; q < 2 * (R / 4); q += 32) {
+            // M == 4: lanes of warp 0; M == 6: lane 0 of every warp
+            const bool issuer = (M == 4) ? (tid < 32) : ((tid & 31) == 0);
+            const int q0 = (M == 4) ? tid : (tid >> 5), qs = (M == 4) ? 32 : NT / 32;
+            if (issuer)
+                for (int q = q0; q < 2 * (R / 4); q += qs) {
                     const int grp = q >> 1, half = q & 1;
                     const uint32_t dst = smem_u32(sm + grp * 4 * ROWB + half * 512);
                     asm volatile(
@@ -86,6 +101,7 @@ __global__ void __launch_bounds__(NT, 1) gather_kernel(const uint8_t* V, const i
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    if (tid == 0) tdur[blockIdx.x] = gtimer() - tstart;
     if (sm[(tid * 97) % (R * ROWB)] == 0x5a && tid == 7) atomicAdd(sink, 1u);
 }
 
@@ -124,6 +140,10 @@ int main() {
     cudaFuncSetAttribute(gather_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(gather_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(gather_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gather_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gather_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    uint64_t* tdur;
+    cudaMalloc(&tdur, 148 * 8);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -137,18 +157,20 @@ int main() {
             cudaMalloc(&idx, h.size() * 4);
             cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
             float tnull = 0;
-            for (int m = -1; m < 5; ++m) {
+            for (int m = -1; m < 7; ++m) {
                 for (int pass = 0; pass < 2; ++pass) {
                     cudaEventRecord(e0);
                     for (int rep = 0; rep < NREP; ++rep) {
                         const int* ix = idx + (size_t)rep * G * R;
                         switch (m) {
                             case -1: null_kernel<<<G, NT>>>(sink); break;
-                            case 0: gather_kernel<0><<<G, NT, smem>>>(V, ix, R, tmap, sink); break;
-                            case 1: gather_kernel<1><<<G, NT, smem>>>(V, ix, R, tmap, sink); break;
-                            case 2: gather_kernel<2><<<G, NT, smem>>>(V, ix, R, tmap, sink); break;
-                            case 3: gather_kernel<3><<<G, NT, smem>>>(V, ix, R, tmap, sink); break;
-                            case 4: gather_kernel<4><<<G, NT, smem>>>(V, ix, R, tmap, sink); break;
+                            case 0: gather_kernel<0><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
+                            case 1: gather_kernel<1><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
+                            case 2: gather_kernel<2><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
+                            case 3: gather_kernel<3><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
+                            case 4: gather_kernel<4><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
+                            case 5: gather_kernel<5><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
+                            case 6: gather_kernel<6><<<G, NT, smem>>>(V, ix, R, tmap, sink, tdur); break;
                         }
                     }
                     cudaEventRecord(e1);
@@ -158,9 +180,15 @@ int main() {
                 cudaEventElapsedTime(&ms, e0, e1);
                 const float us = ms * 1000.f / NREP;
                 if (m == -1) tnull = us;
-                const char* names[] = {"null", "bulk/row all-thr", "bulk/row 1 warp", "ldg->sts", "cp.async16", "gather4 1 warp"};
-                printf("G=%3d R=%3d %-18s %7.2f us  (minus null %6.2f us, %6.1f GB/s)\n", G, R, names[m + 1], us, us - tnull,
-                       m < 0 ? 0.0 : (double)G * R * ROWB / ((us - tnull) * 1e3));
+                const char* names[] = {"null", "bulk/row all-thr", "bulk/row 1 warp", "ldg->sts", "cp.async16", "gather4 1 warp", "bulk/row lane0/warp", "gather4 lane0/warp"};
+                double med = 0, mx = 0;
+                if (m >= 0) {
+                    std::vector<uint64_t> hd(G);
+                    cudaMemcpy(hd.data(), tdur, G * 8, cudaMemcpyDeviceToHost);
+                    std::sort(hd.begin(), hd.end());
+                    med = hd[G / 2] / 1e3; mx = hd[G - 1] / 1e3;
+                }
+                printf("G=%3d R=%3d %-20s %7.2f us/launch; in-kernel gather median %6.2f max %6.2f us\n", G, R, names[m + 1], us, med, mx);
             }
             cudaError_t err = cudaGetLastError();
             if (err != cudaSuccess) printf("error: %s\n", cudaGetErrorString(err));
