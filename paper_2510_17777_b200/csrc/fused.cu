@@ -52,7 +52,8 @@ constexpr int STAGE_ROWS = 128;    // = UMMA M: one K stage is one tcgen05.mma r
 constexpr int RING = SVL_RING_KB * 1024;
 constexpr int TMAX = kFusedTextMax;
 constexpr int UMMA_N = 16;        // q columns per KV group (g <= 16, zero padded)
-constexpr int TMEM_COLS = 256;    // 16 visual stages x UMMA_N fp32 accumulator columns
+constexpr int TMEM_COLS = 512;    // [0, 256): tcgen05 half of d, [256, 512): mma.sync half; 16 cols per stage
+constexpr int LDS_COL = 256;
 
 template <int D, int NT>
 struct FGeom {
@@ -61,7 +62,7 @@ struct FGeom {
     static constexpr int ROWB = 2 * D;
     static constexpr int STAGE_BYTES = STAGE_ROWS * ROWB;
     static constexpr int NST = RING / STAGE_BYTES;  // ring stages
-    static_assert(SMAX / STAGE_ROWS * UMMA_N <= TMEM_COLS, "visual stages fit the TMEM allocation");
+    static_assert(SMAX / STAGE_ROWS * UMMA_N <= LDS_COL, "visual stages fit the TMEM allocation");
     // persistent regions
     static constexpr int QT_OFF = RING;                        // q tile [16][D], K-major SW128 (UMMA B)
     static constexpr int QT_BYTES = UMMA_N * ROWB;
@@ -70,7 +71,7 @@ struct FGeom {
     static constexpr int ATT_BYTES = (SMAX + TMAX) * 4;
     static constexpr int MISC_OFF = ATT_OFF + ATT_BYTES;
     static constexpr int NVS_MAX = SMAX / STAGE_ROWS;
-    static constexpr int MISC_BYTES = 2 * NST * 8 + NVS_MAX * 8 + 8 + 8 + 16 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
+    static constexpr int MISC_BYTES = 2 * NST * 8 + 2 * NVS_MAX * 8 + 8 + 8 + 16 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
                                       16 * 4 + 64 * 4 + 64 * 8;
     static constexpr int BYTES = MISC_OFF + MISC_BYTES;
     // ring re-use once streaming is over
@@ -119,9 +120,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint8_t* misc = smem + GM::MISC_OFF;
     uint64_t* full = reinterpret_cast<uint64_t*>(misc);  // K stage landed
     uint64_t* empty = full + NST;                         // K stage consumed by the tensor core
-    uint64_t* accf = empty + NST;                         // [NVS_MAX] stage i's accumulator in TMEM (single use)
-    uint64_t* tbar = accf + GM::NVS_MAX;                  // text stage landed (single use)
-    uint64_t* vbar = tbar + 1;                            // V gathers (TMA variant)
+    uint64_t* accf = empty + NST;                         // [NVS_MAX] stage i's tcgen05 half in TMEM (single use)
+    uint64_t* ldsf = accf + GM::NVS_MAX;                  // [NVS_MAX] stage i's mma.sync half in TMEM (8 warps)
+    uint64_t* vbar = ldsf + GM::NVS_MAX + 1;              // V gathers (TMA variant)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
     float2* wpart = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(vbar + 1) + 16);  // [16][NCP]
     float2* allpart = wpart + (FT / 32) * NCP;                   // [16][NCP] pushed by the peers
@@ -165,7 +166,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // visual stages (tiled TMA, 128-B swizzle, tcgen05), then <= 1 text stage (plain rows, mma.sync)
     static_assert(TMAX <= STAGE_ROWS, "text rows fit one stage");
     const int nvs = (nvis + STAGE_ROWS - 1) / STAGE_ROWS;
-    const int nstages = nvs + (ntext > 0 ? 1 : 0);
+    const int toff = ntext > 0 ? 1 : 0;  // stage 0 = the text rows (their latency hides under the stream)
+    const int nstages = nvs + toff;
     const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
     const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
     auto work_row = [&](int w) {  // local work row -> cache row
@@ -212,15 +214,20 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // tcgen05.mma chain (M = 128 rows, N = 16 q columns, K = d) writes its dot
     // products to TMEM columns [16 i, 16 i + 16) -- the logits stay there for
     // the whole kernel (no shared-memory copy, so the ring can be deep).
-    // Warp roles: w0 lane 0 = TMA producer, w1 lane 0 = MMA issuer, w2 = TMEM
-    // owner, w4-7 = running LSE of the visual stages (one TMEM lane quarter
-    // each), w8-15 = the text stage (plain rows, mma.sync; logits to smem).
+    // Warp roles: w0 lane 0 = TMA producer, w1 lane 0 = MMA issuer (first half of
+    // d -> TMEM columns [16 i, 16 i + 16)), w2 = TMEM owner, w8-15 = the text stage
+    // (plain rows, mma.sync, logits to smem) and then the second half of d of every
+    // visual stage by mma.sync from the swizzled stage -> TMEM columns LDS_COL + 16 i
+    // (splitting d between the two datapaths: the tensor core's smem read of A is
+    // the stream's bottleneck), w4-7 = running LSE of the visual rows from TMEM.
+    // Stage s: s = 0 is the text stage when ntext > 0, then visual stage v = s - toff.
     const int nsys = max(0, min(ntext, p.vb - t0));
-    auto issue = [&](int i) {
-        const int slot = i % NST;
+    auto issue = [&](int s) {
+        const int slot = s % NST;
         const uint32_t dst0 = ring + slot * GM::STAGE_BYTES;
-        if (i < nvs) {
-            const uint32_t bar = smem_u32(&full[slot]);
+        const uint32_t bar = smem_u32(&full[slot]);
+        if (s >= toff) {
+            const int i = s - toff;
             // 128 visual rows x D: D/64 boxes of 128 rows x 128 B (rows past the slice
             // are loaded and ignored; past the capacity the TMA zero-fills)
             mbar_arrive_expect_tx(bar, (uint32_t)GM::STAGE_BYTES);
@@ -229,9 +236,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 tma_load_4d(dst0 + hf * (STAGE_ROWS * 128), &p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b, bar);
             return;
         }
-        // text rows [t0, t0 + ntext): system rows, then after-visual rows; completion
-        // on the single-use tbar (a far-future phase of full[slot] would be ambiguous)
-        const uint32_t bar = smem_u32(tbar);
+        // text rows [t0, t0 + ntext): system rows, then after-visual rows
         mbar_arrive_expect_tx(bar, (uint32_t)(ntext * ROWB));
         const int seg_n[2] = {nsys, ntext - nsys};
         const int seg_row0[2] = {t0, t0 + nsys + p.nv};
@@ -251,10 +256,12 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1 + 8);  // tcgen05 commit + the 8 LDS warps
         }
-        for (int s = 0; s < GM::NVS_MAX; ++s) mbar_init(smem_u32(&accf[s]), 1);
-        mbar_init(smem_u32(tbar), 1);
+        for (int s = 0; s < GM::NVS_MAX; ++s) {
+            mbar_init(smem_u32(&accf[s]), 1);
+            mbar_init(smem_u32(&ldsf[s]), 8);
+        }
         mbar_init(vbar_a, 1);
         fence_mbar_init();
         for (int i = 0; i < min(NST, nstages); ++i) issue(i);
@@ -274,6 +281,25 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     tc_fence_after();
     const uint32_t tbase = *tslot;
     const bool text_in_lse = !(p.flags_in & 1u /*VISUAL_ONLY*/);
+    // Full raw q.K of visual row i*128 + 32*q4 + lane (warp-collective): the tcgen05
+    // half (lane = row) plus the mma.sync half, which the LDS warps stored in their
+    // fragment order -- row q of a 16-row tile sits at lane perm^-1(q & 7) + (q & 8).
+    const int lsrc = (lane & 16) | (lane & 8) | (((lane & 3) << 1) | ((lane >> 2) & 1));
+    auto load_logits = [&](int i, float (&x)[16]) {
+        uint32_t a[16], c[16];
+        tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, a);
+        tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + LDS_COL + i * UMMA_N, c);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            x[k] = __uint_as_float(a[k]) + __uint_as_float(__shfl_sync(0xffffffffu, c[k], lsrc));
+    };
+    // after the stream the LSE warps have written the sums back to columns [16 i, 16 i + 16)
+    auto load_full = [&](int i, float (&x)[16]) {
+        uint32_t a[16];
+        tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, a);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = __uint_as_float(a[k]);
+    };
 
     if (warp == 0) {
         if (lane == 0)  // producer: refill a slot once the tensor core has consumed it
@@ -284,9 +310,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {
+            if (toff) mbar_arrive(smem_u32(&empty[0]));  // text stage: no tensor-core read
             for (int i = 0; i < nvs; ++i) {
-                const int slot = i % NST;
-                mbar_wait(smem_u32(&full[slot]), (i / NST) & 1);
+                const int slot = (i + toff) % NST;
+                mbar_wait(smem_u32(&full[slot]), ((i + toff) / NST) & 1);
                 tc_fence_after();
                 if (p.trace && i < 32) {
                     uint64_t tnow;
@@ -296,10 +323,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 const uint32_t sb = ring + slot * GM::STAGE_BYTES;
 #if !SVL_EXP_NOMATH  // timing experiment: stream only
 #pragma unroll
-#ifndef SVL_EXP_MMA_STEPS
-#define SVL_EXP_MMA_STEPS (D / 16)
-#endif
-                for (int j = 0; j < SVL_EXP_MMA_STEPS; ++j) {  // K = 16 per instruction
+                for (int j = 0; j < D / 32; ++j) {  // K = 16 per instruction, d in [0, D/2)
                     const int hf = j >> 2, kk = j & 3;
                     umma_bf16(tbase + i * UMMA_N, sw128_desc(sb + hf * (STAGE_ROWS * 128) + kk * 32),
                               sw128_desc(qt + hf * (UMMA_N * 128) + kk * 32), IDESC, j > 0 ? 1u : 0u);
@@ -317,15 +341,17 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         for (int c = 0; c < NCP; ++c) rm[c] = -INFINITY, rl[c] = 0.f;
         for (int i = 0; i < nvs; ++i) {
             mbar_wait(smem_u32(&accf[i]), 0);
+            mbar_wait(smem_u32(&ldsf[i]), 0);
             tc_fence_after();
-            uint32_t v[16];
-            tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, v);
+            float x[16];
+            load_logits(i, x);
+            tmem_st16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, x);  // full q.K for the later passes
             if (i * STAGE_ROWS + q4 * 32 + lane < nvis) {
 #pragma unroll
                 for (int c = 0; c < NCP; ++c) {
-                    const float x = __uint_as_float(v[c]) * p.scale2;
-                    const float M = fmaxf(rm[c], x);
-                    rl[c] = rl[c] * fast_exp2(rm[c] - M) + fast_exp2(x - M);
+                    const float y = x[c] * p.scale2;
+                    const float M = fmaxf(rm[c], y);
+                    rl[c] = rl[c] * fast_exp2(rm[c] - M) + fast_exp2(y - M);
                     rm[c] = M;
                 }
             }
@@ -345,27 +371,47 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             if (lane == 0) wpart[warp * NCP + c] = make_float2(rm[c], rl[c]);
         }
     } else if (warp >= 8) {
-        // text stage: 8 warps x 16 rows, mma.sync (swap-AB, permuted contraction)
-        const int wig = warp - 8, r16 = wig * 16;
+        // visual stages, second half of d: warp w takes tile j = 2 (w % 4) + (w - 8) / 4
+        // (rows 16 j .. 16 j + 15 lie in its TMEM lane quarter w % 4), mma.sync from the
+        // swizzled stage, then adds the tcgen05 half from TMEM and writes the sum back;
+        // the tensor core's shared-memory read of A is the stream's bottleneck, so
+        // splitting d between the two datapaths shortens every stage.  Then the text
+        // stage (plain rows, all of d) on the same warps.
+        const int wig = warp - 8, r16v = 16 * (2 * (warp & 3) + (wig >> 2)), r16 = wig * 16;
         float rm[NT][2], rl[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) rm[nt][0] = rm[nt][1] = -INFINITY, rl[nt][0] = rl[nt][1] = 0.f;
-        if (ntext > 0 && r16 < ntext) {
-            uint4 bq[NT][NCH];
+        uint4 bq[NT][NCH];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int col = nt * 8 + gid;
+        for (int nt = 0; nt < NT; ++nt) {
+            const int col = nt * 8 + gid;
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) bq[nt][i] = make_uint4(0, 0, 0, 0);
-                if (col < g) {
-                    const uint4* qr = reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.H + G * g + col) * D);
+            for (int i = 0; i < NCH; ++i) bq[nt][i] = make_uint4(0, 0, 0, 0);
+            if (col < g) {
+                const uint4* qr = reinterpret_cast<const uint4*>(p.q + ((int64_t)b * p.H + G * g + col) * D);
 #pragma unroll
-                    for (int i = 0; i < NCH; ++i) bq[nt][i] = qr[t + 4 * i];
-                }
+                for (int i = 0; i < NCH; ++i) bq[nt][i] = qr[t + 4 * i];
             }
-            const int slot = nvs % NST;
-            mbar_wait(smem_u32(tbar), 0);
-            const uint32_t base = ring + slot * GM::STAGE_BYTES + (r16 + gid) * ROWB;
+        }
+        auto lse_fold = [&](int nt, float ya, float yb, int e2) {
+            const float mx = fmaxf(ya, yb);
+            if (mx != -INFINITY) {
+                const float M = fmaxf(rm[nt][e2], mx);
+                rl[nt][e2] = rl[nt][e2] * fast_exp2(rm[nt][e2] - M) + fast_exp2(ya - M) + fast_exp2(yb - M);
+                rm[nt][e2] = M;
+            }
+        };
+        // A rows ra = tile row pa, rb = pa + 8, pa = perm(gid): the two rows of a
+        // quarter-warp are 4 apart, so their XOR-swizzled chunks fall in disjoint bank
+        // halves.  TMEM (16x256b) holds rows gid / gid + 8 per thread: exchange by shuffle.
+        const int pa = ((gid & 1) << 2) | (gid >> 1);
+        const int src_ld = ((pa << 2) | t);                                   // holder of TMEM row pa
+        const int src_st = (((((gid & 3) << 1) | (gid >> 2))) << 2) | t;      // holder of row gid (perm^-1)
+        // text stage (stage 0, slot 0): 8 warps x 16 rows, mma.sync over all of d (swap-AB,
+        // permuted contraction); every warp releases the slot, rows or not
+        if (toff && r16 < ntext) {
+            mbar_wait(smem_u32(&full[0]), 0);
+            const uint32_t base = ring + (r16 + gid) * ROWB;
             float acc[NT][2][4];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
@@ -394,17 +440,63 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 if (va) *reinterpret_cast<float2*>(txl + ra_ * NCP + nt * 8 + 2 * t) = make_float2(x0, x1);
                 if (vbv) *reinterpret_cast<float2*>(txl + rb_ * NCP + nt * 8 + 2 * t) = make_float2(x2, x3);
                 if (text_in_lse) {
+                    lse_fold(nt, va ? x0 : -INFINITY, vbv ? x2 : -INFINITY, 0);
+                    lse_fold(nt, va ? x1 : -INFINITY, vbv ? x3 : -INFINITY, 1);
+                }
+            }
+        }
+        if (toff) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&empty[0]));
+        }
+        for (int i = 0; i < nvs; ++i) {
+            const int slot = (i + toff) % NST;
+            mbar_wait(smem_u32(&full[slot]), ((i + toff) / NST) & 1);
+            const uint32_t sbase = ring + slot * GM::STAGE_BYTES;
+            float acc[NT][4];
 #pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) {
-                        const float ya = va ? (e2 ? x1 : x0) : -INFINITY;
-                        const float yb = vbv ? (e2 ? x3 : x2) : -INFINITY;
-                        const float mx = fmaxf(ya, yb);
-                        if (mx != -INFINITY) {
-                            rm[nt][e2] = mx;
-                            rl[nt][e2] = fast_exp2(ya - mx) + fast_exp2(yb - mx);
-                        }
+            for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+            {
+                const int rA = r16v + pa;  // rA & 7 == pa
+                uint4 ra[NCH / 2], rb[NCH / 2];
+#pragma unroll
+                for (int c4 = NCH / 2; c4 < NCH; ++c4) {
+                    const int hf = c4 >> 1, cc = t + 4 * (c4 & 1);
+                    const uint32_t hb = sbase + hf * (STAGE_ROWS * 128) + ((cc ^ pa) << 4);
+                    ra[c4 - NCH / 2] = lds128(hb + rA * 128);
+                    rb[c4 - NCH / 2] = lds128(hb + (rA + 8) * 128);
+                }
+#pragma unroll
+                for (int c4 = NCH / 2; c4 < NCH; ++c4) {
+                    const uint4 x = ra[c4 - NCH / 2], y = rb[c4 - NCH / 2];
+                    const uint32_t a0[4] = {x.x, y.x, x.y, y.y};
+                    const uint32_t a1[4] = {x.z, y.z, x.w, y.w};
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        mma_bf16_16816(acc[nt], a0, bq[nt][c4].x, bq[nt][c4].y);
+                        mma_bf16_16816(acc[nt], a1, bq[nt][c4].z, bq[nt][c4].w);
                     }
                 }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));  // this warp's reads of the slot are done
+            // raw partial to TMEM in fragment order (rows gid / gid + 8 hold tile rows pa / pa + 8)
+            {
+                float fr[8];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    fr[e] = acc[0][e];
+                    fr[4 + e] = (NT > 1) ? acc[NT - 1][e] : 0.f;
+                }
+                tmem_st16x256_x2(tbase + ((uint32_t)r16v << 16) + LDS_COL + i * UMMA_N, fr);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&ldsf[i]));
+            if (p.trace && tid == 256 && i < 16) {
+                uint64_t tnow;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                trs[48 + i] = tnow;
             }
         }
 #pragma unroll
@@ -426,12 +518,11 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     }
     if (warp < 4)
         for (int c = lane; c < NCP; c += 32) wpart[warp * NCP + c] = make_float2(-INFINITY, 0.f);
+    tc_fence_before();
     __syncthreads();  // ring drained: every MMA completed (accf waited), text stage consumed
+    tc_fence_after();
 
-    // text rows' V: V slots [0, ntext); their gather overlaps everything up to the decode
     for (int i = tid; i < ntext; i += FT) att[i] = nvis + i;
-    __syncthreads();
-    gather_rows(0, ntext, 0);
     SVL_TRACE(1);
 
     // ------------------------------------------------ 2. cluster LSE
@@ -463,6 +554,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         }
         if (lane == 0) lse2[warp] = x.x + log2f(x.y);
     }
+    // text rows' V: V slots [0, ntext); the gather overlaps everything up to the decode
+    // (issued after the LSE barrier: a cluster arrive.release waits for in-flight copies)
+    gather_rows(0, ntext, 0);
     __syncthreads();
     SVL_TRACE(2);
     // per-thread copies of the normalisers (+inf pads: exp2(x - inf) = 0)
@@ -483,13 +577,13 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         __syncthreads();
         // relevance of each visual row = its share of the softmax mass, summed over the g heads
         for (int i = warp >> 2; i < nvs; i += FT / 128) {
-            uint32_t v[16];
-            tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, v);
+            float v[16];
+            load_full(i, v);
             const int row = i * STAGE_ROWS + q4 * 32 + lane;
             if (row < nvis) {
                 float sc = 0.f;
 #pragma unroll
-                for (int c = 0; c < NCP; ++c) sc += fast_exp2(__uint_as_float(v[c]) * p.scale2 - nl[c]);
+                for (int c = 0; c < NCP; ++c) sc += fast_exp2(v[c] * p.scale2 - nl[c]);
                 sel.add_key(row, sc);
             }
         }
@@ -556,8 +650,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             const int row = i * STAGE_ROWS + q4 * 32 + lane;
             const bool kept = row < nvis && state_s[row] == kKeySel;
             if (!__any_sync(0xffffffffu, kept)) continue;
-            uint32_t v[16];
-            tmem_ld16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, v);
+            float v[16];
+            load_full(i, v);
             const int rr = kept ? (int)slot_of[row] - s0 : -1;
             if (rr >= 0 && rr < n) {
                 uint32_t hw[8], lw[8];
@@ -567,7 +661,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int c = 2 * c2 + e;
-                        pv2[e] = (c < NCP) ? fast_exp2(__uint_as_float(v[c]) * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
+                        pv2[e] = (c < NCP) ? fast_exp2(v[c] * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
                     }
                     hw[c2] = pack_bf16(pv2[0], pv2[1]);
                     lw[c2] = pack_bf16(pv2[0] - bf16lo(hw[c2]), pv2[1] - bf16hi(hw[c2]));

@@ -53,3 +53,6 @@ print("stage arrivals (us from start, median):", " ".join(
 cyc = (tr[:, 31] - tr[:, 30]).double()
 ns = (tr[:, 10] - tr[:, 0]).double()
 print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {(cyc / ns).median().item() * 1e3:.0f} MHz")
+
+print("LDS-warp stage done (us from start, median):", " ".join(
+    f"{((tr[:, 48 + i] - tr[:, 0]).double() / 1e3).median().item():.2f}" for i in range(16) if not (tr[:, 48 + i] == 0).any()))
