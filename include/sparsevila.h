@@ -52,6 +52,7 @@ typedef enum {
 #define SVL_DEVFLAG_INDEX 1u      /* vis_idx out of [0,N_v) or not strictly ascending */
 #define SVL_DEVFLAG_NONFINITE 2u  /* NaN relevance / saliency; NaN ranks lowest          */
 #define SVL_DEVFLAG_SPAN 4u       /* seq_len[b] < visual_begin + visual_len + n_q, or > capacity       */
+#define SVL_DEVFLAG_WAIT_TIMEOUT 8u /* svl_wait_flags gave up (~2 s) before every producer flag arrived  */
 
 /* ------------------------------------------------------------------ flags */
 #define SVL_NORM_VISUAL_ONLY 1u /* softmax over visual rows only (default: full causal prefix, reading A2) */
@@ -154,6 +155,46 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
 
 size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                         int32_t visual_len, int32_t capacity, uint32_t flags);
+
+/*
+ * svl_sparse_decode_attn_push -- svl_sparse_decode_attn for one rank's shard of a
+ * head-sharded multi-GPU decode (SURVEY.md 8(b) b7, 8(e) e3 "fused variant"),
+ * with the all-gather of the head outputs folded into the kernel: the merged
+ * output of every (b, h) of the shard is stored straight into EVERY rank's
+ * gathered output buffer (NVLink peer stores through the unified address
+ * space), and once all of this call's stores are visible system-wide the last
+ * CTA sets peer_flags[r][rank] = epoch on every rank r (st.release.sys).  The
+ * consumer side is svl_wait_flags.  Replaces the NCCL all-gather of the fp32
+ * head outputs per layer (north star: "NCCL all-gather of head outputs").
+ *
+ * q, K, V, span, vis_idx, k, flags, scale, lse_out: the shard, exactly as for
+ *   svl_sparse_decode_attn (B = this rank's batch rows, H / Hkv its heads).
+ * out        device fp32 [B][H][d] local copy, or NULL.
+ * peer_out   HOST array [P] of device pointers: rank r's gathered output fp32
+ *            [B_total][H_total][d] (symmetric; peer access enabled, or all on
+ *            one device); the shard lands at rows b0.., heads h0..
+ * peer_flags HOST array [P] of device pointers: rank r's flag row uint32 [P].
+ * rank, P    this rank, 1 <= P <= 8 (one NVLink/NVSwitch node).
+ * epoch      > 0, increasing per call (flags compare modulo 2^32).
+ * The workspace header's word 1 is a CTA counter (zero between calls).
+ */
+svl_status svl_sparse_decode_attn_push(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                       svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
+                                       int32_t k, uint32_t flags, float scale, float* out,
+                                       float* lse_out, float* const* peer_out,
+                                       uint32_t* const* peer_flags, int32_t rank, int32_t P,
+                                       uint32_t epoch, int32_t b0, int32_t h0, int32_t B_total,
+                                       int32_t H_total, void* workspace, size_t workspace_bytes,
+                                       void* stream);
+
+/*
+ * svl_wait_flags -- stream-ordered consumer of svl_sparse_decode_attn_push:
+ * work enqueued on `stream` after this call starts once flags[s] >= epoch
+ * (mod 2^32) for every producer s < P (acquire loads, system scope).  flags
+ * is this rank's device flag row uint32 [P].  Bounded: after ~2 s it gives up
+ * and sets SVL_DEVFLAG_WAIT_TIMEOUT in the workspace flag word.
+ */
+svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void* workspace, void* stream);
 
 /* ------------------------------------------------ fused fresh decode step */
 /*

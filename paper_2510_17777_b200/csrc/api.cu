@@ -309,11 +309,19 @@ size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32
     return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
 }
 
-svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
-                                  svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
-                                  int32_t k, uint32_t flags, float scale, float* out,
-                                  float* lse_out, void* ws, size_t ws_bytes, void* stream) {
-    if (!q || !out || !span.seq_len || (k > 0 && !vis_idx))
+struct PushArgs {
+    int P = 0, rank = 0, b0 = 0, h0 = 0, B_total = 0, H_total = 0;
+    uint32_t epoch = 0;
+    float* const* peer_out = nullptr;
+    uint32_t* const* peer_flags = nullptr;
+};
+
+static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                     svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
+                                     int32_t k, uint32_t flags, float scale, float* out,
+                                     float* lse_out, void* ws, size_t ws_bytes, void* stream,
+                                     const PushArgs& push, const char* name) {
+    if (!q || (!out && push.P == 0) || !span.seq_len || (k > 0 && !vis_idx))
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
     if (flags & ~(SVL_SELECT_SHARED)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
     if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
@@ -328,7 +336,7 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
     const int g = H / Hkv;
     if (g > 16) return fail(SVL_ERR_UNSUPPORTED, "g = H/Hkv must be <= 16 in this version%s");
     if (!aligned16(q)) return fail(SVL_ERR_ALIGNMENT, "q not 16-byte aligned%s");
-    if (!aligned16(out)) return fail(SVL_ERR_ALIGNMENT, "out not 16-byte aligned%s");
+    if (out && !aligned16(out)) return fail(SVL_ERR_ALIGNMENT, "out not 16-byte aligned%s");
     svl_status st = check_kv(K, B, Hkv, d, "K");
     if (st != SVL_OK) return st;
     st = check_kv(V, B, Hkv, d, "V");
@@ -362,8 +370,69 @@ svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t H
     p.trace = (getenv("SVL_TRACE") && ws_bytes >= kWsHeader + ((size_t)1 << 20))
                   ? reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader)
                   : nullptr;
+    p.P = push.P;
+    p.rank = push.rank;
+    p.b0 = push.b0;
+    p.h0 = push.h0;
+    p.B_total = push.B_total;
+    p.H_total = push.H_total;
+    p.epoch = push.epoch;
+    for (int r = 0; r < kMaxPeers; ++r) {
+        p.peer_out[r] = (r < push.P) ? push.peer_out[r] : nullptr;
+        p.peer_flags[r] = (r < push.P) ? push.peer_flags[r] : nullptr;
+    }
+    p.done = static_cast<uint32_t*>(ws) + 1;  // header word 1
     cudaError_t e = launch_decode(p, d, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(e, "svl_sparse_decode_attn");
+    if (e != cudaSuccess) return cuda_fail(e, name);
+    return SVL_OK;
+}
+
+svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                  svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
+                                  int32_t k, uint32_t flags, float scale, float* out,
+                                  float* lse_out, void* ws, size_t ws_bytes, void* stream) {
+    return sparse_decode_impl(q, B, H, Hkv, d, K, V, span, vis_idx, k, flags, scale, out, lse_out, ws,
+                              ws_bytes, stream, PushArgs(), "svl_sparse_decode_attn");
+}
+
+svl_status svl_sparse_decode_attn_push(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
+                                       svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
+                                       int32_t k, uint32_t flags, float scale, float* out,
+                                       float* lse_out, float* const* peer_out,
+                                       uint32_t* const* peer_flags, int32_t rank, int32_t P,
+                                       uint32_t epoch, int32_t b0, int32_t h0, int32_t B_total,
+                                       int32_t H_total, void* ws, size_t ws_bytes, void* stream) {
+    if (P < 1 || P > kMaxPeers) return fail(SVL_ERR_INVALID_ARGUMENT, "P outside [1, 8]%s");
+    if (rank < 0 || rank >= P) return fail(SVL_ERR_INVALID_ARGUMENT, "rank outside [0, P)%s");
+    if (epoch == 0) return fail(SVL_ERR_INVALID_ARGUMENT, "epoch must be > 0%s");
+    if (!peer_out || !peer_flags) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL peer arrays%s");
+    for (int r = 0; r < P; ++r)
+        if (!peer_out[r] || !peer_flags[r] || !aligned16(peer_out[r]))
+            return fail(SVL_ERR_INVALID_ARGUMENT, "NULL or misaligned peer buffer%s");
+    if (b0 < 0 || h0 < 0 || b0 + B > B_total || h0 + H > H_total || H_total % (H / std::max(Hkv, 1)))
+        return fail(SVL_ERR_SHAPE, "shard (b0, h0, B, H) outside (B_total, H_total)%s");
+    PushArgs push;
+    push.P = P;
+    push.rank = rank;
+    push.b0 = b0;
+    push.h0 = h0;
+    push.B_total = B_total;
+    push.H_total = H_total;
+    push.epoch = epoch;
+    push.peer_out = peer_out;
+    push.peer_flags = peer_flags;
+    return sparse_decode_impl(q, B, H, Hkv, d, K, V, span, vis_idx, k, flags, scale, out, lse_out, ws,
+                              ws_bytes, stream, push, "svl_sparse_decode_attn_push");
+}
+
+svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void* ws, void* stream) {
+    if (!flags || !ws) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (P < 1 || P > kMaxPeers) return fail(SVL_ERR_INVALID_ARGUMENT, "P outside [1, 8]%s");
+    if (epoch == 0) return fail(SVL_ERR_INVALID_ARGUMENT, "epoch must be > 0%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    cudaError_t e = launch_wait_flags(flags, P, epoch, static_cast<uint32_t*>(ws), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_wait_flags");
     return SVL_OK;
 }
 

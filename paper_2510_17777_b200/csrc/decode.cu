@@ -345,13 +345,52 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
             }
         }
         const int hh = G * p.g + h;
-        p.out[((int64_t)b * p.H + hh) * D + dd] = (den > 0.f) ? num / den : 0.f;
+        const float ov = (den > 0.f) ? num / den : 0.f;
+        if (p.out) p.out[((int64_t)b * p.H + hh) * D + dd] = ov;
         if (dd == 0 && p.lse_out)
             p.lse_out[(int64_t)b * p.H + hh] = (den > 0.f) ? (M + log2f(den)) * kLn2 : -INFINITY;
+        // push variant: the same value into every peer's gathered output (NVLink stores)
+        const int64_t go = ((int64_t)(p.b0 + b) * p.H_total + p.h0 + hh) * D + dd;
+        for (int r = 0; r < p.P; ++r) p.peer_out[r][go] = ov;
     }
     stamp(13);
+    if (p.P > 0) {
+        // the last CTA of the grid publishes: every CTA's stores are fenced at system
+        // scope before its arrival, so the last arrival sees them all
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            const uint32_t total = gridDim.x * gridDim.y;
+            if (atomicAdd(p.done, 1u) == total - 1u) {
+                atomicExch(p.done, 0u);  // the workspace counter is zero again for the next call
+                __threadfence_system();
+                for (int r = 0; r < p.P; ++r)
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.peer_flags[r] + p.rank), "r"(p.epoch)
+                                 : "memory");
+            }
+        }
+    }
     cl.sync();  // no CTA exits while a peer may still push into it (pushes precede the first barrier)
     stamp(14);
+}
+
+// consumer side of the push variant: one thread spins (acquire, system scope)
+// until flags[s] has reached epoch for every producer s; bounded (~2 s), a
+// timeout sets SVL_DEVFLAG_WAIT_TIMEOUT instead of hanging the stream.
+__global__ void wait_flags_kernel(const uint32_t* flags, int P, uint32_t epoch, uint32_t* ws_flags) {
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < P; ++s) {
+        for (uint32_t it = 0;; ++it) {
+            uint32_t v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + s) : "memory");
+            if ((int32_t)(v - epoch) >= 0) break;
+            if (it > (1u << 21)) {
+                atomicOr(ws_flags, 8u /*SVL_DEVFLAG_WAIT_TIMEOUT*/);
+                return;
+            }
+            __nanosleep(1000);
+        }
+    }
 }
 
 template <int D>
@@ -384,6 +423,11 @@ cudaError_t launch_decode_t(const DecodeParams& p, cudaStream_t s) {
 }
 
 }  // namespace
+
+cudaError_t launch_wait_flags(const uint32_t* flags, int P, uint32_t epoch, uint32_t* ws_flags, cudaStream_t s) {
+    wait_flags_kernel<<<1, 32, 0, s>>>(flags, P, epoch, ws_flags);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_decode(const DecodeParams& p, int d, cudaStream_t s) {
     if (d == 128) return launch_decode_t<128>(p, s);

@@ -52,6 +52,8 @@ struct PruneTable {
     int2 fr[kMaxFrames + 1];
 };
 
+constexpr int kMaxPeers = 8;  // GPUs of one NVLink/NVSwitch node
+
 struct DecodeParams {
     const uint16_t* q;  // [B][H][d]
     const uint16_t* K;
@@ -67,7 +69,16 @@ struct DecodeParams {
     float* lse_out;
     uint32_t* flags;
     uint64_t* trace;  // debug: per-CTA phase timestamps (SVL_TRACE=1), else null
+    // push variant (svl_sparse_decode_attn_push): P > 0 => the merged out tile is also
+    // stored into every peer's gathered [B_total][H_total][d] buffer at (b0, h0), and
+    // the last CTA raises peer_flags[r][rank] = epoch (release, system scope)
+    int P, rank, b0, h0, B_total, H_total;
+    uint32_t epoch;
+    float* peer_out[kMaxPeers];
+    uint32_t* peer_flags[kMaxPeers];
+    uint32_t* done;  // workspace counter (header word 1): CTAs finished this call
 };
+cudaError_t launch_wait_flags(const uint32_t* flags, int P, uint32_t epoch, uint32_t* ws_flags, cudaStream_t s);
 
 struct FreshParams {
     CUtensorMap ktmap;  // K as 4-D {d, capacity, Hkv, B}, box {64, 128, 1, 1}, 128-B swizzle

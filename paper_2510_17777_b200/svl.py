@@ -23,7 +23,7 @@ SVL_SELECT_SHARED = 2
 SVL_RETRIEVE_SCORE_ONLY = 0x100
 SVL_RETRIEVE_SELECT_ONLY = 0x200
 SVL_SAL_SUMMARY, SVL_SAL_MULTI_SUMMARY, SVL_SAL_INTRA_VISUAL = 0, 1, 2
-SVL_DEVFLAG_INDEX, SVL_DEVFLAG_NONFINITE, SVL_DEVFLAG_SPAN = 1, 2, 4
+SVL_DEVFLAG_INDEX, SVL_DEVFLAG_NONFINITE, SVL_DEVFLAG_SPAN, SVL_DEVFLAG_WAIT_TIMEOUT = 1, 2, 4, 8
 
 STATUS = {0: "SVL_OK", 1: "SVL_ERR_INVALID_ARGUMENT", 2: "SVL_ERR_SHAPE", 3: "SVL_ERR_ALIGNMENT",
           4: "SVL_ERR_WORKSPACE", 5: "SVL_ERR_UNSUPPORTED", 6: "SVL_ERR_CUDA"}
@@ -33,7 +33,8 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_fresh_decode_workspace_size", "svl_prefill_prune", "svl_prune_workspace_size",
            "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
-           "svl_reset_device_flags", "svl_version"]
+           "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
+           "svl_wait_flags"]
 
 
 class SvlError(RuntimeError):
@@ -103,6 +104,12 @@ def lib():
         L.svl_reset_device_flags.argtypes = [P, P]
         L.svl_version.restype = ctypes.c_char_p
         L.svl_version.argtypes = []
+        L.svl_sparse_decode_attn_push.restype = ctypes.c_int
+        L.svl_sparse_decode_attn_push.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, P,
+                                                  I32, U32, F, P, P, P, P, I32, I32, U32, I32, I32,
+                                                  I32, I32, P, SZ, P]
+        L.svl_wait_flags.restype = ctypes.c_int
+        L.svl_wait_flags.argtypes = [P, I32, U32, P, P]
         _lib = L
     return _lib
 
@@ -242,6 +249,49 @@ def sparse_decode_attn(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_le
         _cuda(lse_out, "lse_out", torch.float32) if lse_out is not None else None,
         w.data_ptr(), w.numel(), _stream(stream)))
     return out, lse_out
+
+
+def sparse_decode_attn_push(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor,
+                            visual_begin: int, visual_len: int, vis_idx: Optional[torch.Tensor],
+                            peer_out, peer_flags, rank: int, epoch: int, b0: int, h0: int,
+                            scale: Optional[float] = None, flags: int = 0,
+                            out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None,
+                            ws: Optional[Workspace] = None, stream=None):
+    """svl_sparse_decode_attn_push: this rank's shard of the decode, stored into every
+    rank's gathered output peer_out[r] (fp32 [B_total][H_total][d]) and flagged in
+    peer_flags[r] (uint32 [P]) with `epoch`.  Returns out (local copy or None)."""
+    B, H, d = q.shape
+    Hkv = K.shape[1]
+    P = len(peer_out)
+    if len(peer_flags) != P:
+        raise ValueError("peer_out and peer_flags must have one entry per rank")
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous")
+    k = 0 if vis_idx is None else vis_idx.shape[-1]
+    B_total, H_total = peer_out[0].shape[0], peer_out[0].shape[1]
+    po = (ctypes.c_void_p * P)(*[_cuda(t, "peer_out", torch.float32) for t in peer_out])
+    pf = (ctypes.c_void_p * P)(*[_cuda(t, "peer_flags", torch.int32) for t in peer_flags])
+    wsz = sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, K.shape[2], flags)
+    w = _ws(ws, q.device).get(wsz)
+    _check(lib().svl_sparse_decode_attn_push(
+        q.data_ptr(), B, H, Hkv, d, kv_view(K, "K"), kv_view(V, "V"),
+        span(visual_begin, visual_len, seq_len),
+        _cuda(vis_idx, "vis_idx", torch.int32) if vis_idx is not None else None, k, flags, scale,
+        _cuda(out, "out", torch.float32) if out is not None else None,
+        _cuda(lse_out, "lse_out", torch.float32) if lse_out is not None else None,
+        ctypes.cast(po, ctypes.c_void_p), ctypes.cast(pf, ctypes.c_void_p), rank, P, epoch, b0, h0,
+        B_total, H_total, w.data_ptr(), w.numel(), _stream(stream)))
+    return out
+
+
+def wait_flags(flags: torch.Tensor, epoch: int, ws: Optional[Workspace] = None, stream=None):
+    """svl_wait_flags: stream-ordered wait until flags[s] >= epoch for all s (int32 [P] tensor)."""
+    w = _ws(ws, flags.device).get(256)
+    _check(lib().svl_wait_flags(_cuda(flags, "flags", torch.int32), flags.numel(), epoch,
+                                w.data_ptr(), _stream(stream)))
 
 
 def fresh_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags=0) -> int:

@@ -185,3 +185,33 @@ def test_checker_rejects_prune_change():
     bad[0, 4] = 11
     with pytest.raises(parity.ParityError):
         parity.check_prune(bad, ref)
+
+
+@pytest.mark.parametrize("case,status", [("P0", 1), ("P9", 1), ("rank", 1), ("epoch0", 1),
+                                         ("null_peers", 1), ("shard", 2)])
+def test_push_host_validation(svl, case, status):
+    """svl_sparse_decode_attn_push rejects bad multi-GPU arguments on the host
+    (SURVEY.md 8(b) b6/b7), before any launch."""
+    L = svl.lib()
+    P_ = 0x10000
+    peers = (ctypes.c_void_p * 2)(P_, P_)
+    args = dict(q=P_, B=1, H=28, Hkv=4, d=128, K=_kv(), V=_kv(), sp=svl.svl_span(10, 60, P_),
+                idx=P_, k=10, flags=0, scale=0.088, out=P_, lse=None,
+                po=ctypes.cast(peers, ctypes.c_void_p), pf=ctypes.cast(peers, ctypes.c_void_p),
+                rank=0, P=2, epoch=1, b0=0, h0=0, Bt=1, Ht=56, ws=P_, wsb=1 << 20, st=None)
+    if case == "P0":
+        args["P"] = 0
+    elif case == "P9":
+        args["P"] = 9
+    elif case == "rank":
+        args["rank"] = 2
+    elif case == "epoch0":
+        args["epoch"] = 0
+    elif case == "null_peers":
+        args["po"] = None
+    elif case == "shard":
+        args["h0"] = 40          # 40 + 28 > 56
+    rc = L.svl_sparse_decode_attn_push(*args.values())
+    assert rc == status, (rc, L.svl_last_error_message())
+    rc = L.svl_wait_flags(P_, 0 if case == "P0" else 2, 0 if case == "epoch0" else 1, None, None)
+    assert rc == 1
