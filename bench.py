@@ -475,6 +475,36 @@ def main():
         e2e_ms = t.item()
     _ = out_stack
 
+    # ---- prefill companion (a6 salience, a7 per-frame prune) on the SURVEY.md 8(d) d2
+    # "prune" config: 256 frames x 512 tokens, 16 encoder heads, d_e 72, s_p = 0.75
+    prefill = None
+    if rank == 0 and world == 1:
+        pw = gen.PrefillWorkload()
+        px = gen.make_prefill_inputs(pw, seed=7, device=dev)
+        sal = torch.empty(pw.F, pw.Nf, dtype=torch.float32, device=dev)
+        ws_p = svl.Workspace(dev)
+        offs = [f * pw.Nf for f in range(pw.F + 1)]
+        kept = torch.empty(1, svl.keep_budget(pw.Nf, pw.sparsity) * pw.F, dtype=torch.int32, device=dev)
+
+        def sal_step():
+            svl.salience(px["Qe"], px["Ke"], pw.S, svl.SVL_SAL_INTRA_VISUAL, out=sal, ws=ws_p)
+
+        def prune_step():
+            svl.prefill_prune(sal.view(1, -1), pw.sparsity, offs, kept_idx=kept, ws=ws_p)
+
+        g_sal, g_prune = graph_of(sal_step), graph_of(prune_step)
+        ms_sal = timed(g_sal, 20, 3)
+        ms_prune = timed(g_prune, 200, 10)
+        flops = 2 * 2 * pw.Nf * pw.Nf * pw.de * pw.He * pw.F  # 2 passes x 2 N_f^2 d_e per head and frame
+        bf16_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops") \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+        prefill = {"config": f"prune: {pw.F} frames x {pw.Nf} tokens, H_e {pw.He}, d_e {pw.de}, "
+                             f"INTRA_VISUAL, s_p {pw.sparsity}",
+                   "salience_ms": ms_sal, "salience_tflops": flops / (ms_sal * 1e-3) / 1e12,
+                   "salience_bound": "tensor", "bf16_peak_tflops": bf16_peak,
+                   "salience_frac": (flops / (ms_sal * 1e-3) / 1e12 / bf16_peak) if bf16_peak else None,
+                   "prune_us": ms_prune * 1e3, "kept": int(kept.numel())}
+
     # ---- steady step (decode only, indices reused) and the per-round amortised step
     steady_us = ms_decode * 1e3 / LAYERS
     steady_bytes = nbytes["decode"]
@@ -526,6 +556,7 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": nbytes["fused"]},
+            "prefill": prefill,
             "cpu_baseline": cpu,
             "e2e": {"value": nbytes["total"] * LAYERS * world / (e2e_ms * 1e-3) / 1e9,
                     "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,

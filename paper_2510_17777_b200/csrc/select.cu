@@ -12,6 +12,8 @@
 // index, ascending output, bitwise reproducible.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "select_core.cuh"
@@ -152,6 +154,71 @@ __global__ void __launch_bounds__(NTH, 1)
     select_body<1, 1>(p, &tab);
 }
 
+// Per-frame prune for frames of <= 512 tokens (the encoder's frames): one CTA
+// per (b, frame), one key per thread, a bitonic sort of the 64-bit composite
+// (order-preserving key << 32 | ~index) descending -- i.e. saliency desc, index
+// asc, exactly the oracle's stable order -- then the top k_f indices are
+// re-emitted in ascending index order through a block prefix sum.  Stages with
+// partner distance < 32 run inside a warp (shuffles, no barrier).
+constexpr int kSmallFrame = 512;
+
+__global__ void __launch_bounds__(kSmallFrame) prune_small_kernel(const SelectParams p,
+                                                                 const __grid_constant__ PruneTable tab) {
+    __shared__ uint64_t sv[kSmallFrame];
+    __shared__ uint32_t wsum[kSmallFrame / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int u = blockIdx.x;
+    const int bb = u / p.nf, f = u % p.nf;
+    const int2 a = tab.fr[f], z = tab.fr[f + 1];
+    const int n = z.x - a.x, k = z.y - a.y;
+    const float* src = p.scores_in + (int64_t)bb * p.N + a.x;
+    bool nan_seen = false;
+    uint64_t v = 0ull;  // padding sorts last
+    if (tid < n) v = ((uint64_t)float_key(src[tid], nan_seen) << 32) | (uint32_t)(~tid);
+    if (nan_seen) raise_flag(p.flags, 2u /*SVL_DEVFLAG_NONFINITE*/);
+    // bitonic sort, descending
+    for (int size = 2; size <= kSmallFrame; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            uint64_t o;
+            if (stride >= 32) {
+                sv[tid] = v;
+                __syncthreads();
+                o = sv[tid ^ stride];
+                __syncthreads();
+            } else {
+                o = __shfl_xor_sync(0xffffffffu, v, stride);
+            }
+            const bool desc = ((tid & size) == 0);      // direction of this bitonic block
+            const bool lower = ((tid & stride) == 0);   // this thread holds the lower position
+            const uint64_t hi = v > o ? v : o, lo = v > o ? o : v;
+            v = (lower == desc) ? hi : lo;
+        }
+    }
+    // position tid now holds the tid-th largest; the first k are kept
+    sv[tid] = v;
+    __syncthreads();
+    // kept flag per ORIGINAL index, then ascending emission by prefix sum
+    const int idx_of_rank = (int)(~(uint32_t)(sv[tid] & 0xffffffffu));
+    __syncthreads();
+    uint32_t* kept = reinterpret_cast<uint32_t*>(sv);  // reuse: kept[original index]
+    kept[tid] = 0u;
+    __syncthreads();
+    if (tid < k) kept[idx_of_rank] = 1u;
+    __syncthreads();
+    const uint32_t mine = (tid < n) ? kept[tid] : 0u;
+    uint32_t x = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t before = 0u;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (mine) p.idx_out[(int64_t)bb * p.kept_cap + a.y + before + x - 1u] = a.x + tid;
+}
+
 }  // namespace
 
 int select_cluster_size(int n) {
@@ -208,6 +275,12 @@ cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
 
 cudaError_t launch_prune_select(const SelectParams& p, const PruneTable& tab, int n_units,
                                 cudaStream_t s) {
+    int max_n = 0;
+    for (int f = 0; f < p.nf; ++f) max_n = std::max(max_n, tab.fr[f + 1].x - tab.fr[f].x);
+    if (max_n <= kSmallFrame) {
+        prune_small_kernel<<<n_units, kSmallFrame, 0, s>>>(p, tab);
+        return cudaGetLastError();
+    }
     return launch_cluster(select_prune_kernel, p.CS, n_units, s, *attr_flag(0), p, tab);
 }
 
