@@ -498,10 +498,15 @@ def main():
         flops = 2 * 2 * pw.Nf * pw.Nf * pw.de * pw.He * pw.F  # 2 passes x 2 N_f^2 d_e per head and frame
         bf16_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops") \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+        n_exp = pw.Nf * pw.Nf * pw.He * pw.F
         prefill = {"config": f"prune: {pw.F} frames x {pw.Nf} tokens, H_e {pw.He}, d_e {pw.de}, "
                              f"INTRA_VISUAL, s_p {pw.sparsity}",
                    "salience_ms": ms_sal, "salience_tflops": flops / (ms_sal * 1e-3) / 1e12,
-                   "salience_bound": "tensor", "bf16_peak_tflops": bf16_peak,
+                   "salience_flops_accounting": "SURVEY.md 8(d) d5: 2 passes x 2 N_f^2 d_e per head and "
+                                                "frame; the tcgen05 kernel computes S once (half of it)",
+                   "salience_exp2_per_s": n_exp / (ms_sal * 1e-3),
+                   "salience_bound": "tensor (per SURVEY); measured: exp2 + issue bound at d_e = 72",
+                   "bf16_peak_tflops": bf16_peak,
                    "salience_frac": (flops / (ms_sal * 1e-3) / 1e12 / bf16_peak) if bf16_peak else None,
                    "prune_us": ms_prune * 1e3, "kept": int(kept.numel())}
 

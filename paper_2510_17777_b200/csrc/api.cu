@@ -130,7 +130,7 @@ namespace svl {
 bool encode_kv_tensor_map(CUtensorMap* map, const void* data, int d, int capacity, int Hkv, int B,
                           int64_t stride_b, int64_t stride_h, int64_t stride_t, int box_rows) {
     const EncodeTiledFn fn = encode_fn();
-    if (!fn || d % 64 || stride_t <= 0 || stride_h <= 0 || stride_b <= 0) return false;
+    if (!fn || d % 8 || stride_t <= 0 || stride_h <= 0 || stride_b <= 0) return false;  // box cols past d zero-fill
     const cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)capacity, (cuuint64_t)Hkv, (cuuint64_t)B};
     const cuuint64_t strides[3] = {(cuuint64_t)stride_t * 2, (cuuint64_t)stride_h * 2, (cuuint64_t)stride_b * 2};
     const cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
@@ -626,6 +626,13 @@ svl_status svl_salience(const void* Qe, const void* Ke, int32_t F, int32_t S, in
     p.acc = reinterpret_cast<float*>(w + round_up(kWsHeader + (size_t)F * H_e * std::max(rows, 1) * sizeof(float), 256));
     p.sal = saliency;
     p.flags = reinterpret_cast<uint32_t*>(w);
+    // INTRA_VISUAL with no summary rows and frames of <= 512 tokens: the tcgen05 kernel
+    // ([F][T][H_e][d_e] as 4-D {d_e, T, H_e, F} tensor maps); otherwise the mma.sync passes
+    const int64_t T = (int64_t)S + N_f;
+    p.use_tc = (mode == SVL_SAL_INTRA_VISUAL && S == 0 && N_f <= 512 && d_e % 8 == 0 && !getenv("SVL_SALIENCE_NO_TC") &&
+                encode_kv_tensor_map(&p.qmap, Qe, d_e, (int)T, H_e, F, T * H_e * d_e, d_e, (int64_t)H_e * d_e, 128) &&
+                encode_kv_tensor_map(&p.kmap, Ke, d_e, (int)T, H_e, F, T * H_e * d_e, d_e, (int64_t)H_e * d_e, 128))
+                   ? 1 : 0;
     cudaError_t e = launch_salience(p, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "svl_salience");
     return SVL_OK;

@@ -107,6 +107,8 @@ constexpr int kFusedSliceMax = SVL_SLICE_MAX;  // visual rows per CTA (halved fo
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
 
 struct SalienceParams {
+    CUtensorMap qmap, kmap;  // tcgen05 path: Qe / Ke as 4-D {d_e, S+N_f, H_e, F}, box {64, 128}
+    int use_tc;              // maps encoded (INTRA_VISUAL, S = 0, N_f <= 512)
     const uint16_t* Qe;
     const uint16_t* Ke;
     int F, S, Nf, He, de, mode;
@@ -128,6 +130,8 @@ cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s);
 cudaError_t launch_prune_select(const SelectParams& p, const PruneTable& tab, int n_units, cudaStream_t s);
 cudaError_t launch_decode(const DecodeParams& p, int d, cudaStream_t s);
 cudaError_t launch_salience(const SalienceParams& p, cudaStream_t s);
+bool salience_tc_eligible(const SalienceParams& p);
+cudaError_t launch_salience_tc(const SalienceParams& p, cudaStream_t s);
 
 int device_sm_count();
 

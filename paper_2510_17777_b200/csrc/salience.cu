@@ -220,6 +220,12 @@ __global__ void finalize_kernel(const SalienceParams p) {
 }  // namespace
 
 cudaError_t launch_salience(const SalienceParams& p, cudaStream_t s) {
+    if (salience_tc_eligible(p)) {  // INTRA_VISUAL on tcgen05 (salience_tc.cu)
+        cudaError_t e = launch_salience_tc(p, s);
+        if (e != cudaSuccess) return e;
+        finalize_kernel<<<dim3((p.Nf + 127) / 128, p.F), 128, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     const int dep = (p.de + 31) / 32 * 32;
     int rb = dep * 2;
     if (rb % 128 != 64) rb += 64;
