@@ -35,6 +35,7 @@
 // HBM traffic per unit: visual K + text K once + kept V + text V (+ the V of
 // the few non-kept keys of the threshold bin).
 #include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -148,26 +149,20 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     if (p.trace && tid == 0) trs[30] = clock64();
 
     // ------------------------------------------------------------ geometry
-    int L = p.seq_len[b];
-    if (L < p.vb + p.nv + 1 || L > p.capacity) {
-        if (tid == 0 && rank == 0) raise_flag(p.flags, 4u /*SPAN*/);
-        L = min(max(L, p.vb + p.nv + 1), p.capacity);
-    }
+    // The visual slice does not depend on anything an upstream kernel writes, so its
+    // first stages are requested before griddepcontrol.wait (programmatic dependent
+    // launch: this prologue overlaps the previous kernel's tail); seq_len, q and the
+    // text rows (the current token's K) are read only after the wait.
     const int slice = p.slice;
     const int v0 = min(p.nv, rank * slice);
     const int nvis = min(p.nv, v0 + slice) - v0;
-    const int T = p.vb + (L - p.vb - p.nv);
-    const int t0 = (int)((int64_t)rank * T / CS);
-    int ntext = (int)((int64_t)(rank + 1) * T / CS) - t0;
-    if (ntext > TMAX) {
-        if (tid == 0) raise_flag(p.flags, 4u /*SPAN*/);
-        ntext = TMAX;
-    }
-    // visual stages (tiled TMA, 128-B swizzle, tcgen05), then <= 1 text stage (plain rows, mma.sync)
+    // stage 0 = the text rows (possibly none), then the visual stages (tiled TMA,
+    // 128-B swizzle, tcgen05); the text stage's latency hides under the stream
     static_assert(TMAX <= STAGE_ROWS, "text rows fit one stage");
     const int nvs = (nvis + STAGE_ROWS - 1) / STAGE_ROWS;
-    const int toff = ntext > 0 ? 1 : 0;  // stage 0 = the text rows (their latency hides under the stream)
+    constexpr int toff = 1;
     const int nstages = nvs + toff;
+    int L = 0, T = 0, t0 = 0, ntext = 0;  // set after griddepcontrol.wait
     const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
     const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
     auto work_row = [&](int w) {  // local work row -> cache row
@@ -221,7 +216,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // (splitting d between the two datapaths: the tensor core's smem read of A is
     // the stream's bottleneck), w4-7 = running LSE of the visual rows from TMEM.
     // Stage s: s = 0 is the text stage when ntext > 0, then visual stage v = s - toff.
-    const int nsys = max(0, min(ntext, p.vb - t0));
+    int nsys = 0;
     auto issue = [&](int s) {
         const int slot = s % NST;
         const uint32_t dst0 = ring + slot * GM::STAGE_BYTES;
@@ -264,9 +259,25 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         }
         mbar_init(vbar_a, 1);
         fence_mbar_init();
-        for (int i = 0; i < min(NST, nstages); ++i) issue(i);
+        for (int i = 1; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
     }
     if (warp == 2) tmem_alloc(smem_u32(tslot), TMEM_COLS);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the upstream grid has completed
+    L = p.seq_len[b];
+    if (L < p.vb + p.nv + 1 || L > p.capacity) {
+        if (tid == 0 && rank == 0) raise_flag(p.flags, 4u /*SPAN*/);
+        L = min(max(L, p.vb + p.nv + 1), p.capacity);
+    }
+    T = p.vb + (L - p.vb - p.nv);
+    t0 = (int)((int64_t)rank * T / CS);
+    ntext = (int)((int64_t)(rank + 1) * T / CS) - t0;
+    if (ntext > TMAX) {
+        if (tid == 0) raise_flag(p.flags, 4u /*SPAN*/);
+        ntext = TMAX;
+    }
+    nsys = max(0, min(ntext, p.vb - t0));
+    if (tid == 0) issue(0);  // the text stage (an empty one completes at once)
     // q tile (UMMA B operand): row c = head G*g + c (zero for c >= g), K-major,
     // 128-B swizzle: chunk j of row r in half h at h*16*128 + r*128 + ((j ^ (r & 7)) << 4)
     for (int e = tid; e < UMMA_N * CH; e += FT) {
@@ -784,13 +795,18 @@ cudaError_t launch_fresh_t(const FreshParams& p, int CS, cudaStream_t s) {
     cfg.blockDim = dim3(FT, 1, 1);
     cfg.dynamicSmemBytes = GM::BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: the prologue (barriers, TMEM, the first visual
+    // K stages) may start while the previous kernel on the stream drains; the kernel
+    // executes griddepcontrol.wait before reading anything that kernel may write
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = getenv("SVL_NO_PDL") ? 0 : 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fresh_kernel<D, NT>, p);
 }
 
