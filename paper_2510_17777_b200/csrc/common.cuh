@@ -80,6 +80,23 @@ SVL_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// arrive on the mbarrier at the same offset in cluster CTA `rank` (release, cluster scope)
+SVL_DEV void mbar_arrive_remote_cluster(uint32_t bar, uint32_t rank) {
+    asm volatile(
+        "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(bar),
+        "r"(rank)
+        : "memory");
+}
+// wait with acquire at cluster scope (the arrivals came from peer CTAs)
+SVL_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
 // 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
 SVL_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile(

@@ -74,7 +74,9 @@ struct FGeom {
     static constexpr int NVS_MAX = SMAX / STAGE_ROWS;
     static constexpr int MISC_BYTES = 2 * NST * 8 + 2 * NVS_MAX * 8 + 8 + 8 + 16 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
                                       16 * 4 + 64 * 4 + 64 * 8;
-    static constexpr int BYTES = MISC_OFF + MISC_BYTES;
+    static constexpr int RCV_OFF = MISC_OFF + MISC_BYTES;       // merge receive [CS][per] + l [16][16] fp32
+    static constexpr int RCV_FLOATS = 16 * D + 16;              // CS * ceil(g D / CS) <= g D + CS
+    static constexpr int BYTES = RCV_OFF + (RCV_FLOATS + 256) * 4;
     // ring re-use once streaming is over
     static constexpr int SEL_OFF = 0;                      // FastSelSmem
     static constexpr int KEYS_OFF = 44 * 1024;             // keys [SMAX]; then slot_of [SMAX] uint16
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint64_t* empty = full + NST;                         // K stage consumed by the tensor core
     uint64_t* accf = empty + NST;                         // [NVS_MAX] stage i's tcgen05 half in TMEM (single use)
     uint64_t* ldsf = accf + GM::NVS_MAX;                  // [NVS_MAX] stage i's mma.sync half in TMEM (8 warps)
+    uint64_t* mrg = ldsf + GM::NVS_MAX;                    // merge: CS remote arrivals
     uint64_t* vbar = ldsf + GM::NVS_MAX + 1;              // V gathers (TMA variant)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
     float2* wpart = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(vbar + 1) + 16);  // [16][NCP]
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             mbar_init(smem_u32(&ldsf[s]), 8);
         }
         mbar_init(vbar_a, 1);
+        mbar_init(smem_u32(mrg), (uint32_t)CS);
         fence_mbar_init();
         for (int i = 1; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
     }
@@ -605,10 +609,17 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         // every row at or above the threshold bin gets a V slot now (superset of the kept rows)
         nslots = ntext + sel.assign_slots_and_push_candidates(att + ntext);
         SVL_TRACE(11);
+#if SVL_EXP_RESOLVE_FIRST
+        SVL_TRACE(12);
+        sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
+        gather_rows(ntext, min(nslots, VCAP), 0);
+        v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
+#else
         gather_rows(ntext, min(nslots, VCAP), 0);
         v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
         SVL_TRACE(12);
         sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
+#endif
     } else {
         if (stage == 2) {
             // the generic scratch aliases the V staging: every CTA's text-row gather
@@ -738,25 +749,38 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         for (int j = 0; j < FT / 16; ++j) acc += lred[j * 16 + tid];
         lh[tid] = acc;
     }
+    __syncthreads();  // lh complete before it is pushed
     // ------------------------------------------------ 5. cluster merge (plain sums)
-    SVL_TRACE(7);
-    cl.sync();
-    SVL_TRACE(8);
+    // Push style: CTA q owns output items [q*per, (q+1)*per) of the unit's g x D
+    // block; every CTA stores its partial of those items (and its 16 l sums)
+    // straight into the owner's receive buffer, then one remote mbarrier arrival
+    // per owner (release, cluster scope).  The owner waits for CS arrivals and
+    // sums in sender order; no CTA reads a peer's shared memory, so a CTA whose
+    // inbound pushes have landed may exit at once (no closing cluster barrier).
     const int items = g * D;
     const int per = (items + CS - 1) / CS;
-    for (int i = rank * per + tid; i < min(items, (rank + 1) * per); i += FT) {
+    float* rcv = reinterpret_cast<float*>(smem + GM::RCV_OFF);   // [CS][per]
+    float* lrcv = rcv + GM::RCV_FLOATS;                           // [16][16]
+    SVL_TRACE(7);
+    for (int i = tid; i < items; i += FT) {
+        const int q = i / per, j = i - q * per;
+        cl.map_shared_rank(rcv, q)[rank * per + j] = octa[(i / D) * D + (i % D)];
+    }
+    if (tid < 16 * CS) cl.map_shared_rank(lrcv, tid >> 4)[rank * 16 + (tid & 15)] = lh[tid & 15];
+    tc_fence_before();  // every TMEM read of this CTA precedes the barrier (warp 2 deallocates after it)
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    __syncthreads();
+    if (tid < CS) mbar_arrive_remote_cluster(smem_u32(mrg), (uint32_t)tid);
+    SVL_TRACE(8);
+    mbar_wait_cluster(smem_u32(mrg), 0);
+    for (int j = tid; j < per; j += FT) {
+        const int i = rank * per + j;
+        if (i >= items) break;
         const int h = i / D, dd = i % D;
-        float oq[16], lq[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {  // all remote loads issued before use
-            oq[q] = (q < CS) ? cl.map_shared_rank(octa, q)[h * D + dd] : 0.f;
-            lq[q] = (q < CS) ? cl.map_shared_rank(lh, q)[h] : 0.f;
-        }
         float num = 0.f, den = 0.f;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            num += oq[q];
-            den += lq[q];
+        for (int q = 0; q < CS; ++q) {
+            num += rcv[q * per + j];
+            den += lrcv[q * 16 + h];
         }
         const int hh = G * g + h;
         p.out[((int64_t)b * p.H + hh) * D + dd] = (den > 0.f) ? num / den : 0.f;
@@ -766,7 +790,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     (void)ibc;
     SVL_TRACE(9);
     tc_fence_before();
-    cl.sync();  // peers may still read this CTA's shared memory until here
     SVL_TRACE(10);
     if (p.trace && tid == 0) trs[31] = clock64();
     if (warp == 2) {
