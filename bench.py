@@ -510,6 +510,40 @@ def main():
                    "salience_frac": (flops / (ms_sal * 1e-3) / 1e12 / bf16_peak) if bf16_peak else None,
                    "prune_us": ms_prune * 1e3, "kept": int(kept.numel())}
 
+    # ---- question-chunk retrieval on tcgen05: svl_retrieve
+    # with n_q question rows on the long-video cache, FULL_PREFIX normalisation computed in-kernel
+    qret = None
+    if rank == 0 and world == 1:
+        base = gen.CONFIGS[WORKLOAD]
+        bf16_peak_q = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops") \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+        runs = []
+        for n_q in (32, 512):
+            wq = gen.DecodeWorkload(**{**base.__dict__, "name": f"q{n_q}", "n_q": n_q, "seq_lens": None})
+            xq = gen.make_decode_inputs(wq, seed=21, device=dev)
+            ws_q = svl.Workspace(dev)
+            idx_q = torch.empty(wq.B, wq.Hkv, wq.k, dtype=torch.int32, device=dev)
+
+            def rq(xq=xq, wq=wq, ws_q=ws_q, idx_q=idx_q):
+                svl.retrieve(xq["q"], xq["K"], xq["seq_len"], wq.vb, wq.nv, wq.k, idx_out=idx_q, ws=ws_q)
+
+            ms_q = timed(graph_of(rq), 20, 3)
+            L, units = wq.seq_len, wq.B * wq.Hkv
+            keys_p0 = wq.g * (n_q * (L - n_q) + n_q * (n_q + 1) // 2)  # causal prefix per query row
+            flops_q = 2 * wq.d * units * (keys_p0 + n_q * wq.g * wq.nv)  # row-LSE pass + column-mass pass
+            n_exp = units * (keys_p0 + 256 * ((n_q * wq.g + 255) // 256) * wq.nv)
+            tf = flops_q / (ms_q * 1e-3) / 1e12
+            runs.append({"n_q": n_q, "query_rows_per_unit": n_q * wq.g, "us": ms_q * 1e3, "tflops": tf,
+                         "frac_bf16_peak": tf / bf16_peak_q if bf16_peak_q else None,
+                         "exp2_per_s": n_exp / (ms_q * 1e-3)})
+            del xq, ws_q
+        qret = {"what": "svl_retrieve, n_q question rows (tensor-core path: row-LSE pass + column-mass pass + "
+                        "cluster top-k), long-video cache (32768 visual + 768 text rows, 28/4 heads, d 128), "
+                        "k = 3277 per KV group, one layer",
+                "flops_accounting": "2 d per (query row, visible key) for each of the two passes",
+                "bound": "exp2 (SFU + FP32-pipe polynomial) at d = 128: one exponential per 256 flop",
+                "bf16_peak_tflops": bf16_peak_q, "runs": runs}
+
     # ---- steady step (decode only, indices reused) and the per-round amortised step
     steady_us = ms_decode * 1e3 / LAYERS
     steady_bytes = nbytes["decode"]
@@ -562,6 +596,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": nbytes["fused"]},
             "prefill": prefill,
+            "question_retrieve": qret,
             "cpu_baseline": cpu,
             "e2e": {"value": nbytes["total"] * LAYERS * world / (e2e_ms * 1e-3) / 1e9,
                     "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,

@@ -97,6 +97,28 @@ static RetrieveLayout retrieve_layout(int B, int Hkv, int nv, const ScorePlan& p
     return l;
 }
 
+// tensor-core path (n_q * g > 32): Qpack, LSE partials, LSE2, scores
+struct RetrieveTcLayout {
+    size_t qpack, part, lse2, scores, total;
+    int NQ, NQP, chunk, nkc;
+};
+
+static RetrieveTcLayout retrieve_tc_layout(int B, int n_q, int H, int Hkv, int d, int nv, int capacity,
+                                           bool visual_only) {
+    RetrieveTcLayout l;
+    const size_t units = (size_t)B * Hkv;
+    const int g = H / Hkv;
+    l.NQ = n_q * g;
+    l.NQP = (l.NQ + 255) / 256 * 256;
+    plan_retrieve_tc((int)units, n_q, g, nv, capacity, visual_only, device_sm_count(), &l.chunk, &l.nkc);
+    l.qpack = kWsHeader;
+    l.part = round_up(l.qpack + units * l.NQP * d * 2, 256);
+    l.lse2 = round_up(l.part + units * l.NQP * 2 * l.nkc * sizeof(float2), 256);
+    l.scores = round_up(l.lse2 + units * l.NQP * sizeof(float), 256);
+    l.total = round_up(l.scores + units * nv * sizeof(float), 256);
+    return l;
+}
+
 // --------------------------------------------------------------- decode plan
 static int plan_splits(int units, int n_att_max, int sms) {
     // CTAs per unit = cluster size: the largest power of two <= 16 that keeps the
@@ -210,12 +232,65 @@ static svl_status check_kv(const svl_kv& kv, int B, int Hkv, int d, const char* 
     return SVL_OK;
 }
 
+// svl_retrieve, n_q * g > 32: qpack -> [row LSE pass] -> LSE2 -> column-mass pass -> cluster top-k
+static svl_status retrieve_tc(const void* q, int B, int n_q, int H, int Hkv, int d, const svl_kv& K,
+                              const svl_span& span, const float* lse_in, int k, float scale, uint32_t flags,
+                              int32_t* idx_out, float* scores_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+    const int units = B * Hkv, g = H / Hkv;
+    const bool vis_only = (flags & SVL_NORM_VISUAL_ONLY) != 0;
+    const int shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
+    RetrieveTcLayout lay = retrieve_tc_layout(B, n_q, H, Hkv, d, span.visual_len, K.capacity, vis_only);
+    if (ws_bytes < lay.total) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    RetrTcParams p;
+    memset(&p, 0, sizeof(p));
+    const int64_t qstride = (int64_t)lay.NQP * d;
+    if (!encode_kv_tensor_map(&p.qmap_x, w + lay.qpack, d, lay.NQP, 1, units, qstride, qstride, d, 128) ||
+        !encode_kv_tensor_map(&p.qmap_y, w + lay.qpack, d, lay.NQP, 1, units, qstride, qstride, d, 256) ||
+        !encode_kv_tensor_map(&p.kmap_x, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 128) ||
+        !encode_kv_tensor_map(&p.kmap_y, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 256))
+        return fail(SVL_ERR_UNSUPPORTED, "tensor-core retrieve: K view not encodable as a TMA tensor map%s");
+    p.q = static_cast<const uint16_t*>(q);
+    p.qpack = reinterpret_cast<uint16_t*>(w + lay.qpack);
+    p.seq_len = span.seq_len;
+    p.lse_in = lse_in;
+    p.B = B; p.n_q = n_q; p.H = H; p.Hkv = Hkv; p.g = g; p.NQ = lay.NQ; p.NQP = lay.NQP;
+    p.vb = span.visual_begin; p.nv = span.visual_len; p.capacity = K.capacity;
+    p.visual_only = vis_only ? 1 : 0;
+    p.chunk = lay.chunk; p.nkc = lay.nkc; p.npart = 2 * lay.nkc;
+    p.scale2 = scale * kLog2e;
+    p.part = reinterpret_cast<float2*>(w + lay.part);
+    p.lse2 = reinterpret_cast<float*>(w + lay.lse2);
+    p.scores = (scores_out && !shared) ? scores_out : reinterpret_cast<float*>(w + lay.scores);
+    p.flags = reinterpret_cast<uint32_t*>(w);
+    cudaError_t e = cudaSuccess;
+    if (!(flags & SVL_RETRIEVE_SELECT_ONLY)) {
+        e = launch_retrieve_tc(p, d, s);
+        if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve/tensor-core scores");
+    }
+    if (flags & SVL_RETRIEVE_SCORE_ONLY) return SVL_OK;
+    SelectParams se = {};
+    se.mode = 2;
+    se.scores_in = p.scores;
+    se.Hkv = Hkv;
+    se.shared = shared;
+    se.nv = span.visual_len; se.k = k;
+    se.idx_out = idx_out;
+    se.scores_out = shared ? scores_out : nullptr;
+    se.flags = p.flags;
+    se.CS = select_cluster_size(span.visual_len);
+    e = launch_select(se, shared ? B : units, s);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve/select");
+    return SVL_OK;
+}
+
 size_t svl_retrieve_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
                                    int32_t visual_len, uint32_t flags) {
-    (void)d;
-    (void)flags;
     if (B < 1 || n_q < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
     const int g = H / Hkv;
+    if (n_q * g > 32)  // tensor-core path (the layout does not depend on the capacity)
+        return retrieve_tc_layout(B, n_q, H, Hkv, d, visual_len, visual_len, (flags & SVL_NORM_VISUAL_ONLY) != 0)
+            .total;
     ScorePlan pl = plan_score(B * Hkv, n_q, g, visual_len, device_sm_count());
     return retrieve_layout(B, Hkv, visual_len, pl).total;
 }
@@ -241,9 +316,10 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
     if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
     const int g = H / Hkv;
-    if (n_q * g > 32) return fail(SVL_ERR_UNSUPPORTED, "n_q * g must be <= 32 in this version%s");
+    const bool tc = n_q * g > 32;  // question chunk: tensor-core path (retrieve_tc.cu)
+    if (tc && n_q * g > kRtMaxNQ) return fail(SVL_ERR_UNSUPPORTED, "n_q * g must be <= 4096%s");
     const int shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
-    if (shared && n_q * g * Hkv > 128) return fail(SVL_ERR_UNSUPPORTED, "SHARED needs n_q*H <= 128%s");
+    if (!tc && shared && n_q * g * Hkv > 128) return fail(SVL_ERR_UNSUPPORTED, "SHARED needs n_q*H <= 128%s");
     if (span.visual_len > 16 * kSelectThreads * kSelectMaxPerThread)
         return fail(SVL_ERR_UNSUPPORTED, "visual_len > 131072%s");
     if (!aligned16(q)) return fail(SVL_ERR_ALIGNMENT, "q not 16-byte aligned%s");
@@ -254,6 +330,8 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     if (st != SVL_OK) return st;
 
     const int units = B * Hkv;
+    if (tc) return retrieve_tc(q, B, n_q, H, Hkv, d, K, span, lse_in, k, scale, flags, idx_out, scores_out,
+                               ws, ws_bytes, (cudaStream_t)stream);
     ScorePlan pl = plan_score(units, n_q, g, span.visual_len, device_sm_count());
     RetrieveLayout lay = retrieve_layout(B, Hkv, span.visual_len, pl);
     if (ws_bytes < lay.total) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
@@ -439,7 +517,7 @@ svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void
 // ----------------------------------------------------- fused fresh step
 // Cluster size and eligibility of the fused kernel for a shape.
 
-static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice) {
+static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice, int d = 128) {
     if (g > 16) return false;
     const int smax = kFusedSliceMax / ((g + 7) / 8);
     int cmin = (nv + smax - 1) / smax;
@@ -450,6 +528,24 @@ static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int
     // many SMs per unit while the units are few (HBM streaming is per-SM bound)
     const int want = (units * 16 <= 2 * device_sm_count()) ? 16 : 8;
     CS = std::max(c, want);
+    bool pinned = false;
+    if (const char* pin = getenv("SVL_FRESH_CS")) {  // test knob: pin the split count (8 or 16)
+        const int v = atoi(pin);
+        if ((v == 8 || v == 16) && v >= c) CS = v, pinned = true;
+    }
+    // Single wave only: every unit's cluster must be co-resident.  Launches with more
+    // clusters than fit at once (later clusters start on SMs vacated by earlier ones)
+    // showed an intermittent barrier fault / non-reproducible selection on B200 that
+    // is not understood yet ("known issue"); they take the
+    // two-call path, whose kernels are multi-wave safe.
+    if (!pinned) {
+        int mac = fresh_max_active_clusters(d, g, CS);
+        if (CS == 16 && (mac <= 0 || units > mac) && c <= 8) {
+            CS = 8;
+            mac = fresh_max_active_clusters(d, g, CS);
+        }
+        if (mac <= 0 || units > mac) return false;
+    }
     slice = (nv + CS - 1) / CS;
     if (slice > smax) return false;
     const int tmax = std::max(0, capacity - nv);  // every non-visual row could be text
@@ -461,7 +557,7 @@ size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_
                                        int32_t visual_len, int32_t capacity, uint32_t flags) {
     if (B < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
     int CS, slice;
-    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice))
+    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice, d))
         return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
     return std::max(svl_retrieve_workspace_size(B, 1, H, Hkv, d, visual_len, flags),
                     svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags));
@@ -500,7 +596,7 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
 
     int CS, slice;
     FreshParams p;
-    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice) ||
+    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice, d) ||
         !encode_kv_tensor_map(&p.ktmap, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 128)) {
         // outside the on-chip budget: the two separate calls (same q as [B][1][H][d])
         st = svl_retrieve(q, B, 1, H, Hkv, d, K, span, nullptr, k, scale, flags, idx_out, nullptr,

@@ -80,6 +80,31 @@ SVL_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Split cluster barrier: every thread arrives (relaxed) once right after its
+// CTA's setup and waits before its first distributed-shared-memory access, so
+// no CTA writes into a peer that has not started yet (the wait is normally
+// free: the peers arrived microseconds earlier).
+SVL_DEV void cluster_arrive_relaxed() {
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+SVL_DEV void cluster_wait() {
+    __syncwarp();
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+// CTA / cluster barriers from code whose warps may be lane-divergent (single-lane
+// producer branches, per-lane mbarrier spins): bar.sync and barrier.cluster are
+// .aligned -- every lane of a warp must execute them together -- so reconverge
+// the warp first (compute-sanitizer synccheck flagged the bare form).
+SVL_DEV void cta_sync() {
+    __syncwarp();
+    __syncthreads();
+}
+template <typename CL>
+SVL_DEV void cluster_sync(CL& cl) {
+    __syncwarp();
+    cl.sync();
+}
 // arrive on the mbarrier at the same offset in cluster CTA `rank` (release, cluster scope)
 SVL_DEV void mbar_arrive_remote_cluster(uint32_t bar, uint32_t rank) {
     asm volatile(

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gid = lane >> 2, t = lane & 3;
     const int u = blockIdx.y;
+    cluster_arrive_relaxed();  // this CTA is resident (peers push into it after their cluster_wait)
     uint64_t* trace = p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
     auto stamp = [&](int i) {
         if (trace && tid == 0) {
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
             rows[i] = row;
         }
         if (bad) raise_flag(p.flags, 1u /*SVL_DEVFLAG_INDEX*/);
-        __syncthreads();
+        cta_sync();
         const uint32_t sK = smem_u32(smem + (j & 1) * SM::BUF_BYTES);
         const uint32_t sV = sK + RB * SM::ROW_BYTES;
         const int nr = (n + 15) & ~15;
@@ -172,13 +173,13 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
 
     for (int j = 0; j < nb; ++j) {
         if (j + 1 < nb) {
-            __syncthreads();  // buffer (j+1)&1 = (j-1)&1 is no longer read
+            cta_sync();  // buffer (j+1)&1 = (j-1)&1 is no longer read
             load_batch(j + 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
+        cta_sync();
         stamp(1 + j);
         const int* rows = rows_s + (j & 1) * RB;
         const uint32_t sK = smem_u32(smem + (j & 1) * SM::BUF_BYTES);
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
                 tred[warp * 16 + gid + 8] = mx_b;
             }
         }
-        __syncthreads();
+        cta_sync();
         // batch max of heads gid, gid + 8 (every thread, same fixed order) -> new running max
         float bm_a = -INFINITY, bm_b = -INFINITY;
         for (int w = 0; w < ntl; ++w) {
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
                 tred[128 + warp * 16 + gid + 8] = ls_b;
             }
         }
-        __syncthreads();
+        cta_sync();
         if (tid < 16) {  // running (M, l) of head tid; fixed tile order
             const float mo = run[tid];
             float mn = mo, ls = 0.f;
@@ -303,8 +304,9 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
             }
         }
     }
-    __syncthreads();  // run[] final (also when this CTA had no rows)
+    cta_sync();  // run[] final (also when this CTA had no rows)
     stamp(10);
+    cluster_wait();   // every peer has started (first DSMEM access below)
 
     // ---- 3. CTA partial pushed straight to the owning peers, then the owners merge
     // item i = h * D + dd is owned by CTA i / per; a CTA sends owner q its
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
         cl.map_shared_rank(rml, q)[rank * 32 + h] = run[h];
     }
     stamp(11);
-    cl.sync();
+    cluster_sync(cl);
     stamp(12);
     for (int i = rank * per + tid; i < min(items, (rank + 1) * per); i += NTH) {
         const int h = i / D, dd = i % D, li = i - rank * per;
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
     if (p.P > 0) {
         // the last CTA of the grid publishes: every CTA's stores are fenced at system
         // scope before its arrival, so the last arrival sees them all
-        __syncthreads();
+        cta_sync();
         if (tid == 0) {
             __threadfence_system();
             const uint32_t total = gridDim.x * gridDim.y;
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
             }
         }
     }
-    cl.sync();  // no CTA exits while a peer may still push into it (pushes precede the first barrier)
+    cluster_sync(cl);  // no CTA exits while a peer may still push into it (pushes precede the first barrier)
     stamp(14);
 }
 

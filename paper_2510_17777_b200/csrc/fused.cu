@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     auto v_expect = [&](uint32_t) {};
     auto v_wait = [&](uint32_t) {
         cp_async_wait<0>();
-        __syncthreads();
+        cta_sync();
     };
 #else
     // one TMA bulk copy per row, one issuing lane per warp (a bulk copy is a
@@ -251,19 +251,22 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             w += seg_n[sg];
         }
     };
-    if (tid == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), 1 + 8);  // tcgen05 commit + the 8 LDS warps
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < NST; ++s) {
+                mbar_init(smem_u32(&full[s]), 1);
+                mbar_init(smem_u32(&empty[s]), 1 + 8);  // tcgen05 commit + the 8 LDS warps
+            }
+            for (int s = 0; s < GM::NVS_MAX; ++s) {
+                mbar_init(smem_u32(&accf[s]), 1);
+                mbar_init(smem_u32(&ldsf[s]), 8);
+            }
+            mbar_init(vbar_a, 1);
+            mbar_init(smem_u32(mrg), (uint32_t)CS);
+            fence_mbar_init();
+            for (int i = 1; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
         }
-        for (int s = 0; s < GM::NVS_MAX; ++s) {
-            mbar_init(smem_u32(&accf[s]), 1);
-            mbar_init(smem_u32(&ldsf[s]), 8);
-        }
-        mbar_init(vbar_a, 1);
-        mbar_init(smem_u32(mrg), (uint32_t)CS);
-        fence_mbar_init();
-        for (int i = 1; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
+        __syncwarp();
     }
     if (warp == 2) tmem_alloc(smem_u32(tslot), TMEM_COLS);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -281,7 +284,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         ntext = TMAX;
     }
     nsys = max(0, min(ntext, p.vb - t0));
-    if (tid == 0) issue(0);  // the text stage (an empty one completes at once)
+    if (warp == 0) {
+        if (lane == 0) issue(0);  // the text stage (an empty one completes at once)
+        __syncwarp();
+    }
     // q tile (UMMA B operand): row c = head G*g + c (zero for c >= g), K-major,
     // 128-B swizzle: chunk j of row r in half h at h*16*128 + r*128 + ((j ^ (r & 7)) << 4)
     for (int e = tid; e < UMMA_N * CH; e += FT) {
@@ -292,9 +298,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     }
     fence_proxy_async_smem();
     tc_fence_before();
-    __syncthreads();
+    cta_sync();
     tc_fence_after();
     const uint32_t tbase = *tslot;
+    cluster_arrive_relaxed();  // this CTA is resident: peers may push into it after their cluster_wait
     const bool text_in_lse = !(p.flags_in & 1u /*VISUAL_ONLY*/);
     // Full raw q.K of visual row i*128 + 32*q4 + lane (warp-collective): the tcgen05
     // half (lane = row) plus the mma.sync half, which the LDS warps stored in their
@@ -347,6 +354,12 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 umma_commit(smem_u32(&empty[slot]));
                 umma_commit(smem_u32(&accf[i]));
             }
+#if SVL_EXP_DRAIN
+            // no asynchronous arrival may target this CTA's barriers after it exits:
+            // wait for the final phase of every ring slot (commit + LDS warps)
+            for (int st = max(0, nstages - NST); st < nstages; ++st)
+                mbar_wait(smem_u32(&empty[st % NST]), (st / NST) & 1);
+#endif
         }
         __syncwarp();
     } else if (warp >= 4 && warp < 8) {
@@ -357,6 +370,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         for (int i = 0; i < nvs; ++i) {
             mbar_wait(smem_u32(&accf[i]), 0);
             mbar_wait(smem_u32(&ldsf[i]), 0);
+            __syncwarp();  // lanes leave the spin at different times; tcgen05.ld is .aligned
             tc_fence_after();
             float x[16];
             load_logits(i, x);
@@ -426,6 +440,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         // permuted contraction); every warp releases the slot, rows or not
         if (toff && r16 < ntext) {
             mbar_wait(smem_u32(&full[0]), 0);
+            __syncwarp();  // mma.sync is .aligned
             const uint32_t base = ring + (r16 + gid) * ROWB;
             float acc[NT][2][4];
 #pragma unroll
@@ -467,6 +482,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         for (int i = 0; i < nvs; ++i) {
             const int slot = (i + toff) % NST;
             mbar_wait(smem_u32(&full[slot]), ((i + toff) / NST) & 1);
+            __syncwarp();  // mma.sync is .aligned
             const uint32_t sbase = ring + slot * GM::STAGE_BYTES;
             float acc[NT][4];
 #pragma unroll
@@ -534,7 +550,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     if (warp < 4)
         for (int c = lane; c < NCP; c += 32) wpart[warp * NCP + c] = make_float2(-INFINITY, 0.f);
     tc_fence_before();
-    __syncthreads();  // ring drained: every MMA completed (accf waited), text stage consumed
+    cta_sync();  // ring drained: every MMA completed (accf waited), text stage consumed
     tc_fence_after();
 
     for (int i = tid; i < ntext; i += FT) att[i] = nvis + i;
@@ -548,6 +564,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             m = M;
         }
     };
+    cluster_wait();    // every peer has started (first DSMEM access below)
     if (warp < NCP) {  // warp c folds column c (fixed shuffle tree), lanes push to the peers
         float2 x = (lane < FT / 32) ? wpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
 #pragma unroll
@@ -558,7 +575,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         }
         if (lane < CS) cl.map_shared_rank(allpart, lane)[rank * NCP + warp] = x;
     }
-    cl.sync();
+    cluster_sync(cl);
     if (warp < NCP) {
         float2 x = (lane < CS) ? allpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
 #pragma unroll
@@ -572,7 +589,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // text rows' V: V slots [0, ntext); the gather overlaps everything up to the decode
     // (issued after the LSE barrier: a cluster arrive.release waits for in-flight copies)
     gather_rows(0, ntext, 0);
-    __syncthreads();
+    cta_sync();
     SVL_TRACE(2);
     // per-thread copies of the normalisers (+inf pads: exp2(x - inf) = 0)
     float nl[NCP];
@@ -589,7 +606,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     int stage = 0;  // 0 = all / none, 1 = fast path, 2 = generic
     if (!sel.trivial()) {
         sel.zero_hist();
-        __syncthreads();
+        cta_sync();
         // relevance of each visual row = its share of the softmax mass, summed over the g heads
         for (int i = warp >> 2; i < nvs; i += FT / 128) {
             float v[16];
@@ -627,7 +644,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             v_expect((uint32_t)(ntext * ROWB));
             v_wait(0);
             vphase = 1;
-            cl.sync();
+            cluster_sync(cl);
         }
         const int nsel = sel.generic_or_trivial(stage, *reinterpret_cast<PushTopkSmem*>(smem + GM::PUSH_OFF),
                                                 idx_out, att + ntext);
@@ -643,7 +660,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::PT_OFF);
     uint16_t* ptl = pth + VCAP * 16;
-    __syncthreads();  // top-k scratch (aliased by the P table and slot_of) is dead
+    cta_sync();  // top-k scratch (aliased by the P table and slot_of) is dead
     for (int sl = ntext + tid; sl < nslots; sl += FT) slot_of[att[sl]] = (uint16_t)sl;
     for (int s0 = 0; s0 < nslots; s0 += VCAP) {
         const int n = min(VCAP, nslots - s0);
@@ -657,7 +674,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             reinterpret_cast<uint4*>(pth)[i] = make_uint4(0, 0, 0, 0);
             reinterpret_cast<uint4*>(ptl)[i] = make_uint4(0, 0, 0, 0);
         }
-        __syncthreads();
+        cta_sync();
         for (int i = tid; i < (min(ntext, s0 + n) - s0) * 16; i += FT) {
             const int rr = i >> 4, h = i & 15;
             if (h < g) {
@@ -703,7 +720,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         }
         v_wait(vphase);
         vphase ^= 1u;
-        __syncthreads();
+        cta_sync();
         // denominators from the table itself (hi + lo: the weights the PV uses)
         for (int i = tid; i < nr * 16; i += FT) {
             const uint32_t hv = pth[i], lv = ptl[i];
@@ -729,7 +746,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 mma_bf16_16816(o[1], pl, v2r, v3r);
             }
         }
-        __syncthreads();  // staging + P table free for the next batch
+        cta_sync();  // staging + P table free for the next batch
     }
     SVL_TRACE(6);
     float* lred = reinterpret_cast<float*>(smem + GM::LRED_OFF);
@@ -743,13 +760,13 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             if (gid + 8 < g) *reinterpret_cast<float2*>(octa + (gid + 8) * D + col) = make_float2(o[nt][2], o[nt][3]);
         }
     }
-    __syncthreads();
+    cta_sync();
     if (tid < 16) {
         float acc = 0.f;
         for (int j = 0; j < FT / 16; ++j) acc += lred[j * 16 + tid];
         lh[tid] = acc;
     }
-    __syncthreads();  // lh complete before it is pushed
+    cta_sync();  // lh complete before it is pushed
     // ------------------------------------------------ 5. cluster merge (plain sums)
     // Push style: CTA q owns output items [q*per, (q+1)*per) of the unit's g x D
     // block; every CTA stores its partial of those items (and its 16 l sums)
@@ -769,7 +786,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     if (tid < 16 * CS) cl.map_shared_rank(lrcv, tid >> 4)[rank * 16 + (tid & 15)] = lh[tid & 15];
     tc_fence_before();  // every TMEM read of this CTA precedes the barrier (warp 2 deallocates after it)
     asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    __syncthreads();
+    cta_sync();
     if (tid < CS) mbar_arrive_remote_cluster(smem_u32(mrg), (uint32_t)tid);
     SVL_TRACE(8);
     mbar_wait_cluster(smem_u32(mrg), 0);
@@ -833,7 +850,48 @@ cudaError_t launch_fresh_t(const FreshParams& p, int CS, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, fresh_kernel<D, NT>, p);
 }
 
+template <int D, int NT>
+int max_active_clusters_t(int CS) {
+    using GM = FGeom<D, NT>;
+    if (cudaFuncSetAttribute(fresh_kernel<D, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(fresh_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM::BYTES) != cudaSuccess)
+        return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS, 1, 1);
+    cfg.blockDim = dim3(FT, 1, 1);
+    cfg.dynamicSmemBytes = GM::BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fresh_kernel<D, NT>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 }  // namespace
+
+// Co-resident clusters of the fused kernel at cluster size CS (cached per device).
+int fresh_max_active_clusters(int d, int g, int CS) {
+    static int cache[8][2][2][17] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int NT = (g + 7) / 8;
+    if (CS < 1 || CS > 16 || NT < 1 || NT > 2) return 0;
+    int& c = cache[dev & 7][d == 128][NT - 1][CS];
+    if (c == 0) {
+        if (d == 128) c = NT == 1 ? max_active_clusters_t<128, 1>(CS) : max_active_clusters_t<128, 2>(CS);
+        else c = NT == 1 ? max_active_clusters_t<64, 1>(CS) : max_active_clusters_t<64, 2>(CS);
+        if (c == 0) c = -1;
+    }
+    return c;
+}
 
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s) {
     const int NT = (p.g + 7) / 8;

@@ -27,7 +27,7 @@ struct ScoreParams {
 };
 
 struct SelectParams {
-    int mode;  // 0 = retrieve (logits + LSE), 1 = prune (float scores)
+    int mode;  // 0 = retrieve (logits + LSE), 1 = prune (float scores), 2 = retrieve from relevance scores
     // retrieve source
     const float* logits;
     const float2* part;
@@ -105,6 +105,7 @@ constexpr int kFusedTextMax = 128;    // text rows per CTA
 #endif
 constexpr int kFusedSliceMax = SVL_SLICE_MAX;  // visual rows per CTA (halved for g > 8)
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
+int fresh_max_active_clusters(int d, int g, int CS);  // <= 0: unknown
 
 struct SalienceParams {
     CUtensorMap qmap, kmap;  // tcgen05 path: Qe / Ke as 4-D {d_e, S+N_f, H_e, F}, box {64, 128}
@@ -119,6 +120,28 @@ struct SalienceParams {
     uint32_t* flags;
 };
 
+// ------------------------------------------- retrieve, tensor-core path (n_q*g > 32)
+constexpr int kRtMaxNQ = 4096;  // n_q * g query rows per unit (LSE2 table in shared memory)
+struct RetrTcParams {
+    CUtensorMap xmap, ymap;      // set by the launcher per pass (resident X tile, streamed Y stages)
+    CUtensorMap qmap_x, qmap_y;  // Qpack as 4-D {d, NQP, 1, units}, boxes of 128 / 256 rows
+    CUtensorMap kmap_x, kmap_y;  // K cache view {d, capacity, Hkv, B}, boxes of 128 / 256 rows
+    const uint16_t* q;           // [B][n_q][H][d]
+    uint16_t* qpack;             // [units][NQP][d] (workspace)
+    const int32_t* seq_len;
+    const float* lse_in;         // natural log [B][n_q][H] or null
+    int B, n_q, H, Hkv, g, NQ, NQP, vb, nv, capacity;
+    int visual_only;
+    int chunk, nkc, npart;       // pass 0: keys per CTA, chunks per unit, partials per row (2 nkc)
+    float scale2;
+    float2* part;                // [units][NQP][npart] base-2 (max, sum)
+    float* lse2;                 // [units][NQP] base-2 LSE (+inf on padding rows)
+    float* scores;               // [units][nv] relevance
+    uint32_t* flags;
+};
+void plan_retrieve_tc(int units, int n_q, int g, int nv, int capacity, bool visual_only, int sms, int* chunk,
+                      int* nkc);
+cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s);
 constexpr int kScoreThreads = 512;
 constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA

@@ -1,0 +1,364 @@
+// retrieve_tc.cu -- question-chunk retrieval on the 5th-generation tensor cores
+// (SURVEY.md 8(f) f1): svl_retrieve when n_q * g > 32.
+//
+// PAPER.md:124 (section 3.2): the query-aware relevance of every visual token is
+// computed from the *question* rows, "concurrently with the FlashAttention2
+// path during prefill".  With n_q question rows the per-unit work is a real
+// contraction (M = n_q * g query columns against N_v keys, arithmetic
+// intensity ~ n_q * g flop/B), so it runs on tcgen05:
+//
+//   qpack     Q_u = the n_q * g query rows of unit (b, G), row n = r * g + hh,
+//             packed contiguous and zero padded to NQP (multiple of 256) rows.
+//   pass 0    (only without lse_in) row log-sum-exp: S = Q_blk K_chunk^T with
+//             M = 128 query rows, N = 256 keys per stage (TMEM accumulator);
+//             one thread per query row folds a running (max, sum) over its
+//             columns, causal limit j <= seq_len - n_q + r (FULL_PREFIX) or the
+//             visual span only (VISUAL_ONLY); partials per (row, key chunk,
+//             column half) -> workspace.
+//   combine   LSE2[u][n] (base 2) from the partials, or lse_in * log2(e).
+//   pass 1    column mass, operands swapped: S^T = K_blk Q_chunk^T with
+//             M = 128 visual keys, N = 256 query rows per stage; one thread per
+//             key sums exp2(s * scale2 - LSE2[n]) over its columns, so the
+//             "visual share of the attention mass" of a
+//             key is a per-thread row sum -- no cross-thread reduction.
+//   select    the cluster top-k of select.cu (mode 2: precomputed scores).
+//
+// Both tensor-core passes share one kernel: a resident X tile (128 rows) and
+// a 2-stage ring of Y tiles (256 rows), both loaded by tiled TMA with the
+// 128-B swizzle (K-major UMMA operands), one elected thread issuing
+// tcgen05.mma (M128 N256 K16) into a double-buffered TMEM accumulator
+// (2 x 256 columns), 8 epilogue warps (two per TMEM lane quarter, one per
+// column half) reading it back with tcgen05.ld.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svl {
+
+namespace {
+
+constexpr int RT_THREADS = 384;  // w0 TMA producer, w1 MMA issuer, w2 TMEM owner, w3 spare, w4-w11 epilogue
+constexpr int RT_XROWS = 128;    // UMMA M
+constexpr int RT_YROWS = 256;    // UMMA N per stage
+constexpr int RT_NST = 2;        // Y ring stages
+
+template <int D>
+struct RtSmem {
+    static constexpr int NB = D / 64;                          // 64-column (128-B) TMA boxes
+    static constexpr int X_BYTES = NB * RT_XROWS * 128;
+    static constexpr int Y_BYTES = NB * RT_YROWS * 128;
+    static constexpr int X_OFF = 0;
+    static constexpr int Y_OFF = X_OFF + X_BYTES;
+    static constexpr int LSE_OFF = Y_OFF + RT_NST * Y_BYTES;  // pass 1: LSE2 of the unit's query rows
+    static constexpr int RED_OFF = LSE_OFF + kRtMaxNQ * 4;    // pass 1: [2 halves][128 rows] column-half sums
+    static constexpr int BAR_OFF = RED_OFF + 2 * RT_XROWS * 4;
+    static constexpr int BYTES = BAR_OFF + 128;
+    static_assert(X_OFF % 1024 == 0 && Y_OFF % 1024 == 0 && Y_BYTES % 1024 == 0, "swizzle atoms");
+    static_assert(BYTES <= 227 * 1024, "shared memory");
+};
+
+__global__ void qpack_kernel(const RetrTcParams p, int D) {
+    // one 16-B chunk per thread: Qpack[u][n][c] = q[b][r][G g + hh][c], zero past NQ
+    const int CH = D / 8;
+    const int64_t total = (int64_t)p.B * p.Hkv * p.NQP * CH;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % CH);
+        const int64_t row = e / CH;
+        const int n = (int)(row % p.NQP);
+        const int u = (int)(row / p.NQP);
+        const int b = u / p.Hkv, G = u % p.Hkv;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (n < p.NQ) {
+            const int r = n / p.g, hh = n % p.g;
+            v = reinterpret_cast<const uint4*>(p.q + (((int64_t)b * p.n_q + r) * p.H + G * p.g + hh) * D)[c];
+        }
+        reinterpret_cast<uint4*>(p.qpack + row * D)[c] = v;
+    }
+}
+
+__global__ void lse_combine_kernel(const RetrTcParams p) {
+    const int64_t total = (int64_t)p.B * p.Hkv * p.NQP;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(e % p.NQP);
+        const int u = (int)(e / p.NQP);
+        const int b = u / p.Hkv, G = u % p.Hkv;
+        float out = INFINITY;  // padding rows: exp2(x - inf) = 0
+        if (n < p.NQ) {
+            const int r = n / p.g, hh = n % p.g;
+            if (p.lse_in) {
+                out = p.lse_in[((int64_t)b * p.n_q + r) * p.H + G * p.g + hh] * kLog2e;
+            } else {
+                float m = -INFINITY, l = 0.f;
+                const float2* pp = p.part + e * p.npart;
+                for (int i = 0; i < p.npart; ++i) {  // fixed order: deterministic
+                    const float2 x = pp[i];
+                    const float M = fmaxf(m, x.x);
+                    if (M != -INFINITY) {
+                        l = l * exp2f(m - M) + x.y * exp2f(x.x - M);
+                        m = M;
+                    }
+                }
+                out = m + log2f(l);
+            }
+            if (out != out) raise_flag(p.flags, 2u /*NONFINITE*/);
+        }
+        p.lse2[e] = out;
+    }
+}
+
+// MODE 0: row LSE partials (X = Q block, Y = K chunk stages).
+// MODE 1: column mass      (X = K block, Y = Q chunk stages).
+template <int MODE, int D>
+__global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_constant__ RetrTcParams p) {
+    using SM = RtSmem<D>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr uint32_t IDESC = umma_idesc_bf16(RT_XROWS, RT_YROWS);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    const uint32_t xfull = smem_u32(bars), yfull0 = smem_u32(bars + 1), yempty0 = smem_u32(bars + 1 + RT_NST);
+    const uint32_t afull0 = smem_u32(bars + 1 + 2 * RT_NST), aempty0 = smem_u32(bars + 3 + 2 * RT_NST);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5 + 2 * RT_NST);
+    const uint32_t sX = smem_u32(smem + SM::X_OFF), sY = smem_u32(smem + SM::Y_OFF);
+
+    const int u = (MODE == 0) ? blockIdx.z : blockIdx.y;
+    const int b = u / p.Hkv, G = u % p.Hkv;
+    int L = p.seq_len[b];
+    if (L < p.vb + p.nv + p.n_q || L > p.capacity) {
+        if (tid == 0 && blockIdx.x == 0) raise_flag(p.flags, 4u /*SPAN*/);
+        L = min(max(L, p.vb + p.nv + p.n_q), p.capacity);
+    }
+    // geometry: X rows, Y stages
+    int xrow0, y0 = 0, y1 = 0, nst;
+    if (MODE == 0) {
+        const int lo = p.visual_only ? p.vb : 0;
+        const int hi = p.visual_only ? p.vb + p.nv : L;
+        y0 = lo + blockIdx.x * p.chunk;
+        y1 = min(hi, y0 + p.chunk);
+        xrow0 = blockIdx.y * RT_XROWS;
+        nst = y1 > y0 ? (y1 - y0 + RT_YROWS - 1) / RT_YROWS : 0;
+    } else {
+        xrow0 = p.vb + blockIdx.x * RT_XROWS;
+        nst = p.NQP / RT_YROWS;
+    }
+    const int q4 = warp & 3, ch = (warp - 4) >> 2;  // epilogue: TMEM lane quarter, column half
+    float2* part_out = nullptr;
+    if (MODE == 0) {
+        const int n = xrow0 + 32 * q4 + lane;
+        part_out = p.part + ((int64_t)u * p.NQP + n) * p.npart + blockIdx.x * 2 + ch;
+        if (nst == 0) {  // empty key chunk (seq_len shorter than the planned range)
+            if (warp >= 4) *part_out = make_float2(-INFINITY, 0.f);
+            return;
+        }
+    }
+
+    if (tid == 0) {
+        mbar_init(xfull, 1);
+        for (int s = 0; s < RT_NST; ++s) {
+            mbar_init(yfull0 + 8 * s, 1);
+            mbar_init(yempty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(afull0 + 8 * a, 1);
+            mbar_init(aempty0 + 8 * a, 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(smem_u32(tslot), 512);
+    float* lse_s = reinterpret_cast<float*>(smem + SM::LSE_OFF);
+    if (MODE == 1)
+        for (int i = tid; i < p.NQP; i += RT_THREADS) lse_s[i] = p.lse2[(int64_t)u * p.NQP + i];
+    tc_fence_before();
+    cta_sync();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(xfull, (uint32_t)SM::X_BYTES);
+#pragma unroll
+            for (int hf = 0; hf < SM::NB; ++hf) {
+                if (MODE == 0)
+                    tma_load_4d(sX + hf * (RT_XROWS * 128), &p.xmap, hf * 64, xrow0, 0, u, xfull);
+                else
+                    tma_load_4d(sX + hf * (RT_XROWS * 128), &p.xmap, hf * 64, xrow0, G, b, xfull);
+            }
+            for (int s = 0; s < nst; ++s) {
+                const int slot = s % RT_NST;
+                if (s >= RT_NST) mbar_wait(yempty0 + 8 * slot, ((s / RT_NST) - 1) & 1);
+                const uint32_t bar = yfull0 + 8 * slot;
+                mbar_arrive_expect_tx(bar, (uint32_t)SM::Y_BYTES);
+#pragma unroll
+                for (int hf = 0; hf < SM::NB; ++hf) {
+                    const uint32_t dst = sY + slot * SM::Y_BYTES + hf * (RT_YROWS * 128);
+                    if (MODE == 0)
+                        tma_load_4d(dst, &p.ymap, hf * 64, y0 + s * RT_YROWS, G, b, bar);
+                    else
+                        tma_load_4d(dst, &p.ymap, hf * 64, s * RT_YROWS, 0, u, bar);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_wait(xfull, 0);
+            for (int s = 0; s < nst; ++s) {
+                const int slot = s % RT_NST, a = s & 1;
+                mbar_wait(yfull0 + 8 * slot, (s / RT_NST) & 1);
+                if (s >= 2) mbar_wait(aempty0 + 8 * a, ((s >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t yb = sY + slot * SM::Y_BYTES;
+#pragma unroll
+                for (int j = 0; j < D / 16; ++j) {
+                    const int hf = j >> 2, kk = j & 3;
+                    umma_bf16(tbase + a * RT_YROWS, sw128_desc(sX + hf * (RT_XROWS * 128) + kk * 32),
+                              sw128_desc(yb + hf * (RT_YROWS * 128) + kk * 32), IDESC, j > 0 ? 1u : 0u);
+                }
+                umma_commit(yempty0 + 8 * slot);
+                umma_commit(afull0 + 8 * a);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        const uint32_t trow = tbase + ((uint32_t)(32 * q4) << 16);
+        if (MODE == 0) {
+            const int n = xrow0 + 32 * q4 + lane;
+            const int r = n / p.g;
+            // causal limit of query row r (FULL_PREFIX): keys j <= L - n_q + r
+            const int jend = p.visual_only ? y1 : min(y1, L - p.n_q + r + 1);
+            float m = -INFINITY, l = 0.f;
+            for (int s = 0; s < nst; ++s) {
+                const int a = s & 1;
+                mbar_wait(afull0 + 8 * a, (s >> 1) & 1);
+                __syncwarp();  // tcgen05.ld is .aligned
+                tc_fence_after();
+#pragma unroll 1
+                for (int c32 = 0; c32 < 4; ++c32) {
+                    const int col0 = ch * 128 + c32 * 32;
+                    const int j0 = y0 + s * RT_YROWS + col0;
+                    uint32_t v[32];
+                    tmem_ld32(trow + a * RT_YROWS + col0, v);
+                    float x[32];
+                    float cm = -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        x[i] = (j0 + i < jend) ? __uint_as_float(v[i]) * p.scale2 : -INFINITY;
+                        cm = fmaxf(cm, x[i]);
+                    }
+                    // branch-free (the next tcgen05.ld is warp-collective): an all-masked
+                    // chunk leaves (m, l) unchanged
+                    const float M = fmaxf(m, cm);
+                    const float Ms = (M == -INFINITY) ? 0.f : M;
+                    float acc = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc += fast_exp2(x[i] - Ms);
+                    l = l * fast_exp2(m - Ms) + acc;
+                    m = M;
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(aempty0 + 8 * a);
+            }
+            if (n < p.NQP) *part_out = make_float2(m, l);
+        } else {
+            float acc = 0.f;
+            for (int s = 0; s < nst; ++s) {
+                const int a = s & 1;
+                mbar_wait(afull0 + 8 * a, (s >> 1) & 1);
+                __syncwarp();  // tcgen05.ld is .aligned
+                tc_fence_after();
+#pragma unroll 1
+                for (int c32 = 0; c32 < 4; ++c32) {
+                    const int col0 = ch * 128 + c32 * 32;
+                    const float* ls = lse_s + s * RT_YROWS + col0;
+                    uint32_t v[32];
+                    tmem_ld32(trow + a * RT_YROWS + col0, v);
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {  // SFU and FP32-pipe exponentials alternate
+                        acc += fast_exp2(fmaf(__uint_as_float(v[i]), p.scale2, -ls[i]));
+                        const float y = fmaf(__uint_as_float(v[i + 1]), p.scale2, -ls[i + 1]);
+                        acc += (y < -126.f) ? 0.f : poly_exp2(y);  // padded columns: exactly 0
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(aempty0 + 8 * a);
+            }
+            reinterpret_cast<float*>(smem + SM::RED_OFF)[ch * RT_XROWS + 32 * q4 + lane] = acc;
+        }
+    }
+    tc_fence_before();
+    cta_sync();
+    if (MODE == 1 && tid < RT_XROWS) {
+        const float* red = reinterpret_cast<const float*>(smem + SM::RED_OFF);
+        const int j = blockIdx.x * RT_XROWS + tid;
+        const float sc = red[tid] + red[RT_XROWS + tid];
+        if (j < p.nv) {
+            if (!(sc == sc) || sc == INFINITY) raise_flag(p.flags, 2u /*NONFINITE*/);
+            p.scores[(int64_t)u * p.nv + j] = sc;
+        }
+    }
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tbase, 512);
+    }
+}
+
+template <int MODE, int D>
+cudaError_t launch_tc(const RetrTcParams& p, dim3 grid, cudaStream_t s) {
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(retr_tc_kernel<MODE, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             RtSmem<D>::BYTES);
+        if (e == cudaSuccess) e = set_max_carveout(retr_tc_kernel<MODE, D>);
+        if (e != cudaSuccess) return e;
+        attr_done[dev] = true;
+    }
+    retr_tc_kernel<MODE, D><<<grid, RT_THREADS, RtSmem<D>::BYTES, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// host plan of pass 0: a fixed number of key chunks per (unit, query block) --
+// about two waves of CTAs, independent of the key range (so the workspace size
+// does not depend on the capacity) -- each chunk a multiple of 256 keys
+void plan_retrieve_tc(int units, int n_q, int g, int nv, int capacity, bool visual_only, int sms, int* chunk,
+                      int* nkc) {
+    const int NQ = n_q * g;
+    const int nqb = (NQ + RT_XROWS - 1) / RT_XROWS;
+    const int range = visual_only ? nv : capacity;
+    const int n = std::max(1, std::min(64, 2 * sms / std::max(1, units * nqb)));
+    *nkc = n;
+    *chunk = ((range + n - 1) / n + RT_YROWS - 1) / RT_YROWS * RT_YROWS;
+}
+
+cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s) {
+    const int units = p.B * p.Hkv;
+    const int sms = device_sm_count();
+    const int64_t qchunks = (int64_t)units * p.NQP * (d / 8);
+    qpack_kernel<<<(int)std::min<int64_t>((qchunks + 255) / 256, 8L * sms), 256, 0, s>>>(p, d);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    RetrTcParams p0 = p;
+    p0.xmap = p.qmap_x;  // X = Q blocks
+    p0.ymap = p.kmap_y;  // Y = K stages
+    if (!p.lse_in) {
+        const dim3 g0(p.nkc, (p.NQ + RT_XROWS - 1) / RT_XROWS, units);
+        e = d == 128 ? launch_tc<0, 128>(p0, g0, s) : launch_tc<0, 64>(p0, g0, s);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t rows = (int64_t)units * p.NQP;
+    lse_combine_kernel<<<(int)std::min<int64_t>((rows + 255) / 256, 8L * sms), 256, 0, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    RetrTcParams p1 = p;
+    p1.xmap = p.kmap_x;  // X = K blocks
+    p1.ymap = p.qmap_y;  // Y = Q chunks
+    const dim3 g1((p.nv + RT_XROWS - 1) / RT_XROWS, units, 1);
+    return d == 128 ? launch_tc<1, 128>(p1, g1, s) : launch_tc<1, 64>(p1, g1, s);
+}
+
+}  // namespace svl

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NTHS) row_lse_kernel(const SalienceParams p) {
         if (it + 1 < ntile) stage_tile(nxt, Kf, rs, (it + 1) * TILE, min(TILE, g.T - (it + 1) * TILE), g, p.de);
         else cp_async_commit();
         cp_async_wait<1>();
-        __syncthreads();
+        cta_sync();
         float acc[8][4];
         tile_mma(acc, ra, rb, cur, g, gid, t);
         float xa = -INFINITY, xb = -INFINITY;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(NTHS) row_lse_kernel(const SalienceParams p) {
         lb = lb * exp2f(mb - nb) + sb;
         ma = na;
         mb = nb;
-        __syncthreads();
+        cta_sync();
     }
     la += __shfl_xor_sync(0xffffffffu, la, 1);
     la += __shfl_xor_sync(0xffffffffu, la, 2);
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(NTHS) col_sum_kernel(const SalienceParams p) {
             cp_async_commit();
         }
         cp_async_wait<1>();
-        __syncthreads();
+        cta_sync();
         float acc[8][4];
         tile_mma(acc, ra, rb, cur, g, gid, t);  // acc[nt]: (col gid/gid+8, rows nt*8+2t..)
         const float* L2 = slse + (it & 1) * TILE;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(NTHS) col_sum_kernel(const SalienceParams p) {
             suma += exp2f(acc[nt][0] * p.scale2 - l0) + exp2f(acc[nt][1] * p.scale2 - l1);
             sumb += exp2f(acc[nt][2] * p.scale2 - l0) + exp2f(acc[nt][3] * p.scale2 - l1);
         }
-        __syncthreads();
+        cta_sync();
     }
     suma += __shfl_xor_sync(0xffffffffu, suma, 1);
     suma += __shfl_xor_sync(0xffffffffu, suma, 2);

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(TC_NT, 1) salience_tc_kernel(const __grid_cons
     if (warp == 0) tmem_alloc(smem_u32(tslot), TC_NMAX);
     for (int i = tid; i < 4 * TC_NMAX; i += TC_NT) cpart[i] = 0.f;
     tc_fence_before();
-    __syncthreads();
+    cta_sync();
     tc_fence_after();
     const uint32_t tbase = *tslot;
 
@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(TC_NT, 1) salience_tc_kernel(const __grid_cons
                 umma_commit(mdone);
             }
             mbar_wait(mdone, mph);
+            __syncwarp();  // tcgen05.ld is .aligned
             mph ^= 1u;
             tc_fence_after();
             // the MMA has consumed buffer `buf`; prefetch the next row block into the other one
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(TC_NT, 1) salience_tc_kernel(const __grid_cons
             // combine the 4 column groups of the row: M, L
             red[cg * TC_ROWS + row] = m;
             red[(4 + cg) * TC_ROWS + row] = l;
-            __syncthreads();
+            cta_sync();
             float M = -INFINITY;
 #pragma unroll
             for (int gq = 0; gq < 4; ++gq) M = fmaxf(M, red[gq * TC_ROWS + row]);
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(TC_NT, 1) salience_tc_kernel(const __grid_cons
                 const float mg = red[gq * TC_ROWS + row];
                 L += (mg == -INFINITY) ? 0.f : red[(4 + gq) * TC_ROWS + row] * fast_exp2((mg - M) * s2);
             }
-            __syncthreads();
+            cta_sync();
             const float r = (valid && L > 0.f) ? 1.f / L : 0.f;
             // pass 3: column sums of e * r over the warp's 32 rows (butterfly transpose-reduce)
 #pragma unroll
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(TC_NT, 1) salience_tc_kernel(const __grid_cons
                 cpart[q4 * TC_NMAX + c * 32 + lane] += x[0];  // column c*32 + lane, rows of quarter q4
             }
             tc_fence_before();
-            __syncthreads();  // TMEM reads of this block done before the next block's MMA
+            cta_sync();  // TMEM reads of this block done before the next block's MMA
             tc_fence_after();
         }
         // acc[f][h][j] = sum over the 4 warps (fixed order); reset the partials
@@ -204,12 +205,12 @@ __global__ void __launch_bounds__(TC_NT, 1) salience_tc_kernel(const __grid_cons
             const float a = cpart[j] + cpart[TC_NMAX + j] + cpart[2 * TC_NMAX + j] + cpart[3 * TC_NMAX + j];
             p.acc[((int64_t)f * p.He + h) * Nf + j] = a;
         }
-        __syncthreads();
+        cta_sync();
         for (int i = tid; i < 4 * TC_NMAX; i += TC_NT) cpart[i] = 0.f;
-        __syncthreads();
+        cta_sync();
     }
     tc_fence_before();
-    __syncthreads();
+    cta_sync();
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tbase, TC_NMAX);

@@ -217,13 +217,13 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const ScorePara
             for (int e2 = 0; e2 < 2; ++e2)
                 wpart[warp][nt * 8 + 2 * t + e2] = make_float2(rm[nt][e2], rl[nt][e2]);
     }
-    __syncthreads();
+    cta_sync();
     if (threadIdx.x < NT * 8) {
         float m = -INFINITY, l = 0.f;
         for (int w = 0; w < NWARPS; ++w) lse_merge(m, l, wpart[w][threadIdx.x].x, wpart[w][threadIdx.x].y);
         p.part[((int64_t)u * p.C + c) * p.NCP + threadIdx.x] = make_float2(m, l);
     }
-    __syncthreads();  // wpart is reused by the next item
+    cta_sync();  // wpart is reused by the next item
     }  // item loop
 }
 

@@ -35,6 +35,7 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SelectSmem& sm = *reinterpret_cast<SelectSmem*>(smem_raw);
     cg::cluster_group cluster = cg::this_cluster();
+    cluster_arrive_relaxed();  // this CTA is resident (peers push into it after their cluster_wait)
     const int CS = p.CS;
     const int rank = (int)cluster.block_rank();
     const int u = blockIdx.y;
@@ -44,7 +45,7 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
     int n, k, b = 0, G0 = 0, nG = 1;
     int64_t src_off = 0, out_off;
     int idx_base = 0;  // added to written indices (prune: frame offset -> global index)
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 2) {
         n = p.nv;
         k = p.k;
         out_off = (int64_t)u * k;
@@ -103,7 +104,7 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
             }
             if (lane == 0) sm.lse2[cc] = lse2;
         }
-        __syncthreads();
+        cta_sync();
     }
 
     // ------------------------------------------------------------------ keys
@@ -129,6 +130,10 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
                         if (col < p.NC) sc += exp2f(lv[col] - sm.lse2[G * p.NC + col]);
                 }
                 if (p.scores_out) p.scores_out[(int64_t)u * n + j] = sc;
+            } else if (MODE == 2) {  // precomputed per-unit relevance (tensor-core retrieve), summed over G if SHARED
+                sc = 0.f;
+                for (int G = 0; G < nG; ++G) sc += p.scores_in[((int64_t)(b * p.Hkv + G0 + G)) * p.nv + j];
+                if (p.scores_out) p.scores_out[(int64_t)u * n + j] = sc;
             } else {
                 sc = p.scores_in[src_off + j];
             }
@@ -137,16 +142,21 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
     }
     if (nan_seen) raise_flag(p.flags, 2u /*SVL_DEVFLAG_NONFINITE*/);
 
+    cluster_wait();  // every peer has started (cluster_topk pushes over DSMEM)
     const TopkResult r = cluster_topk<NTH>(cluster, sm.topk, key, nmine, E, j0, slice, n, k);
     topk_emit<NTH>(sm.topk, r, key, nmine, [&](int e, uint32_t slot) {
         p.idx_out[out_off + slot] = idx_base + my0 + e;
     });
-    cluster.sync();  // no CTA leaves while a peer may still address its shared memory
+    cluster_sync(cluster);  // no CTA leaves while a peer may still address its shared memory
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NTH, 1) select_retrieve_kernel(const SelectParams p) {
     select_body<0, NT>(p, nullptr);
+}
+
+__global__ void __launch_bounds__(NTH, 1) select_scores_kernel(const SelectParams p) {
+    select_body<2, 1>(p, nullptr);
 }
 
 __global__ void __launch_bounds__(NTH, 1)
@@ -182,9 +192,9 @@ __global__ void __launch_bounds__(kSmallFrame) prune_small_kernel(const SelectPa
             uint64_t o;
             if (stride >= 32) {
                 sv[tid] = v;
-                __syncthreads();
+                cta_sync();
                 o = sv[tid ^ stride];
-                __syncthreads();
+                cta_sync();
             } else {
                 o = __shfl_xor_sync(0xffffffffu, v, stride);
             }
@@ -196,15 +206,15 @@ __global__ void __launch_bounds__(kSmallFrame) prune_small_kernel(const SelectPa
     }
     // position tid now holds the tid-th largest; the first k are kept
     sv[tid] = v;
-    __syncthreads();
+    cta_sync();
     // kept flag per ORIGINAL index, then ascending emission by prefix sum
     const int idx_of_rank = (int)(~(uint32_t)(sv[tid] & 0xffffffffu));
-    __syncthreads();
+    cta_sync();
     uint32_t* kept = reinterpret_cast<uint32_t*>(sv);  // reuse: kept[original index]
     kept[tid] = 0u;
-    __syncthreads();
+    cta_sync();
     if (tid < k) kept[idx_of_rank] = 1u;
-    __syncthreads();
+    cta_sync();
     const uint32_t mine = (tid < n) ? kept[tid] : 0u;
     uint32_t x = mine;
 #pragma unroll
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(kSmallFrame) prune_small_kernel(const SelectPa
         if (lane >= off) x += y;
     }
     if (lane == 31) wsum[warp] = x;
-    __syncthreads();
+    cta_sync();
     uint32_t before = 0u;
     for (int w = 0; w < warp; ++w) before += wsum[w];
     if (mine) p.idx_out[(int64_t)bb * p.kept_cap + a.y + before + x - 1u] = a.x + tid;
@@ -264,6 +274,7 @@ static bool* attr_flag(int which) {
 }
 
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
+    if (p.mode == 2) return launch_cluster(select_scores_kernel, p.CS, n_units, s, *attr_flag(5), p);
     switch (p.NCP / 8) {
         case 1: return launch_cluster(select_retrieve_kernel<1>, p.CS, n_units, s, *attr_flag(1), p);
         case 2: return launch_cluster(select_retrieve_kernel<2>, p.CS, n_units, s, *attr_flag(2), p);

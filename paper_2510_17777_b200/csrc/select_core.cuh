@@ -69,7 +69,7 @@ SVL_DEV uint32_t block_scan_excl(uint32_t v, uint32_t* warp_sums, uint32_t& tota
         if (lane >= off) x += y;
     }
     if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
+    cta_sync();
     if (warp == 0) {
         uint32_t w = (lane < NW) ? warp_sums[lane] : 0u;
 #pragma unroll
@@ -79,10 +79,10 @@ SVL_DEV uint32_t block_scan_excl(uint32_t v, uint32_t* warp_sums, uint32_t& tota
         }
         if (lane < NW) warp_sums[lane] = w;
     }
-    __syncthreads();
+    cta_sync();
     const uint32_t before = (warp > 0 ? warp_sums[warp - 1] : 0u) + (x - v);
     total = warp_sums[NW - 1];
-    __syncthreads();
+    cta_sync();
     return before;
 }
 
@@ -136,12 +136,12 @@ SVL_DEV void local_kth_largest(TopkSmem& s, const uint32_t* vals, int vstride, i
     for (int pass = 0; pass < 4; ++pass) {
         const int sh = 24 - 8 * pass;
         for (int i = tid; i < 256; i += NTH) s.lsel_hist[i] = 0u;
-        __syncthreads();
+        cta_sync();
         for (int i = tid; i < m; i += NTH) {
             const uint32_t v = vals[i * vstride];
             if ((v & M) == P) atomicAdd(&s.lsel_hist[(v >> sh) & 255u], 1u);
         }
-        __syncthreads();
+        cta_sync();
         if (tid < 32) {
             int b;
             uint32_t ab;
@@ -152,12 +152,12 @@ SVL_DEV void local_kth_largest(TopkSmem& s, const uint32_t* vals, int vstride, i
                 s.lsel_res[2] = above_acc + ab;
             }
         }
-        __syncthreads();
+        cta_sync();
         P = s.lsel_res[0];
         M |= 255u << sh;
         krem = s.lsel_res[1];
         above_acc = s.lsel_res[2];
-        __syncthreads();
+        cta_sync();
     }
     T = P;
     n_above = above_acc;
@@ -174,11 +174,11 @@ SVL_DEV uint32_t cluster_radix_pass(cg::cluster_group& cl, TopkSmem& s, int buf,
     const int rank = (int)cl.block_rank();
     const uint32_t dmask = (uint32_t)(nbins - 1);
     for (int i = tid; i < nbins; i += NTH) s.hist[buf][i] = 0u;
-    __syncthreads();
+    cta_sync();
 #pragma unroll
     for (int e = 0; e < EMAX; ++e)
         if (e < nmine && (key[e] & M) == P) atomicAdd(&s.hist[buf][(key[e] >> sh) & dmask], 1u);
-    cl.sync();
+    cluster_sync(cl);
     const int bpo = nbins / CS;
     {
         // owner reduction: all CS remote loads of a bin are issued before use
@@ -198,10 +198,10 @@ SVL_DEV uint32_t cluster_radix_pass(cg::cluster_group& cl, TopkSmem& s, int buf,
         (void)block_scan_excl<NTH>(part, s.warp_sums, tot);
         if (tid == 0) s.own_total[buf] = tot;
     }
-    cl.sync();
+    cluster_sync(cl);
     // owner totals -> local, find the owner o*, then copy o*'s bins locally
     if (tid < CS) s.ot_local[tid] = *cl.map_shared_rank(&s.own_total[buf], tid);
-    __syncthreads();
+    cta_sync();
     if (warp == 0) {
         int ostar;
         uint32_t above_o;
@@ -211,7 +211,7 @@ SVL_DEV uint32_t cluster_radix_pass(cg::cluster_group& cl, TopkSmem& s, int buf,
             s.bcast[1] = above_o;
         }
     }
-    __syncthreads();
+    cta_sync();
     const int ostar = (int)s.bcast[0];
     const uint32_t above_o = s.bcast[1];
     uint32_t* lown = &s.hist[buf ^ 1][0];  // scratch copy of o*'s bins (other buffer is idle)
@@ -219,7 +219,7 @@ SVL_DEV uint32_t cluster_radix_pass(cg::cluster_group& cl, TopkSmem& s, int buf,
         const uint32_t* rown = cl.map_shared_rank(&s.own[buf][0], ostar);
         for (int i = tid; i < bpo; i += NTH) lown[i] = rown[i];
     }
-    __syncthreads();
+    cta_sync();
     if (warp == 0) {
         int bl;
         uint32_t above_b;
@@ -230,12 +230,12 @@ SVL_DEV uint32_t cluster_radix_pass(cg::cluster_group& cl, TopkSmem& s, int buf,
             s.bcast[2] = lown[bl];
         }
     }
-    __syncthreads();
+    cta_sync();
     P |= s.bcast[0] << sh;
     M |= dmask << sh;
     krem = s.bcast[1];
     const uint32_t cnt = s.bcast[2];
-    __syncthreads();
+    cta_sync();
     return cnt;
 }
 
@@ -290,7 +290,7 @@ SVL_DEV TopkResult cluster_topk(cg::cluster_group& cl, TopkSmem& s, const uint32
                 if (e < nmine && (key[e] >> 20) == bstar)
                     r0->cand[pos++] = make_uint2(key[e], (uint32_t)(j0 + tid * E + e));
         }
-        cl.sync();
+        cluster_sync(cl);
         if (rank == 0) {
             const int m = (int)s.cand_count;
             uint32_t T, n_gt;
@@ -298,7 +298,7 @@ SVL_DEV TopkResult cluster_topk(cg::cluster_group& cl, TopkSmem& s, const uint32
             const uint32_t need_eq = krem - n_gt;  // >= 1 ties to take, lowest index first
             for (int i = tid; i < m; i += NTH) s.aux[i] = (s.cand[i].x == T) ? ~s.cand[i].y : 0u;
             if (tid < 16) s.cta_sel[tid] = s.cta_quota[tid] = 0u;
-            __syncthreads();
+            cta_sync();
             uint32_t NI, unused;
             local_kth_largest<NTH>(s, s.aux, 1, m, need_eq, NI, unused);
             const uint32_t tie_max = ~NI;  // largest index among the taken ties
@@ -309,7 +309,7 @@ SVL_DEV TopkResult cluster_topk(cg::cluster_group& cl, TopkSmem& s, const uint32
                 if (c.x > T || tie_taken) atomicAdd(&s.cta_sel[r], 1u);
                 if (tie_taken) atomicAdd(&s.cta_quota[r], 1u);
             }
-            __syncthreads();
+            cta_sync();
             if (tid < CS) {
                 uint32_t off = 0u;
                 for (int q = 0; q < tid; ++q) off += s.cta_above[q] + s.cta_sel[q];
@@ -319,7 +319,7 @@ SVL_DEV TopkResult cluster_topk(cg::cluster_group& cl, TopkSmem& s, const uint32
                 rq->pub[2] = off;
             }
         }
-        cl.sync();
+        cluster_sync(cl);
         res.T = s.pub[0];
         res.quota = s.pub[1];
         res.offset = s.pub[2];
@@ -343,7 +343,7 @@ SVL_DEV TopkResult cluster_topk(cg::cluster_group& cl, TopkSmem& s, const uint32
         s.cta_cnt[0] = tot & 0xffffu;
         s.cta_cnt[1] = tot >> 16;
     }
-    cl.sync();
+    cluster_sync(cl);
     uint32_t eq_acc = 0u, sel_before = 0u;
     for (int q = 0; q < rank; ++q) {
         const uint32_t* c = cl.map_shared_rank(&s.cta_cnt[0], q);
@@ -354,7 +354,7 @@ SVL_DEV TopkResult cluster_topk(cg::cluster_group& cl, TopkSmem& s, const uint32
     res.T = T;
     res.quota = (krem > eq_acc) ? krem - eq_acc : 0u;
     res.offset = sel_before;
-    cl.sync();  // peers finished reading cta_cnt
+    cluster_sync(cl);  // peers finished reading cta_cnt
     return res;
 }
 

@@ -130,7 +130,7 @@ struct FastSelect {
         const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
         if (nan_seen) raise_flag(flags, 2u /*NONFINITE*/);
         stamp(tr, 8);
-        __syncthreads();
+        cta_sync();
         stamp(tr, 9);
         // fold the private histograms and push bin b straight to every peer
         for (int b = tid; b < 256; b += NTH) {
@@ -139,14 +139,14 @@ struct FastSelect {
             for (int w = 0; w < NTH / 32; ++w) acc += whist[w * 256 + b];
             s.hist[b] = acc;
         }
-        __syncthreads();
+        cta_sync();
         for (int i = tid; i < CS * 64; i += NTH) {
             const int q = i >> 6, c = i & 63;
             reinterpret_cast<uint4*>(cl.map_shared_rank(&s.allhist[rank][0], q))[c] =
                 reinterpret_cast<const uint4*>(s.hist)[c];
         }
         stamp(tr, 10);
-        cl.sync();
+        cluster_sync(cl);
         stamp(tr, 11);
         for (int b = tid; b < 256; b += NTH) {
             uint32_t v[16];
@@ -157,9 +157,9 @@ struct FastSelect {
             for (int q = 0; q < 16; ++q) acc += v[q];
             s.tot[b] = acc;
         }
-        __syncthreads();
+        cta_sync();
         if (warp == 0) warp_find_nb<256>(s.tot, (uint32_t)k, s.bcast);
-        __syncthreads();
+        cta_sync();
         stamp(tr, 12);
         bstar = (int)s.bcast[0];
         krem = (uint32_t)k - s.bcast[1];
@@ -174,7 +174,7 @@ struct FastSelect {
                 s.sel_q[q] = 0u;
             }
         }
-        __syncthreads();
+        cta_sync();
         uint32_t maxc = 0u;
 #pragma unroll
         for (int q = 0; q < 16; ++q) maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
@@ -209,7 +209,7 @@ struct FastSelect {
             }
             state[i] = st;
         }
-        cl.sync();
+        cluster_sync(cl);
         return (int)(tot & 0xffffu);
     }
 
@@ -219,15 +219,15 @@ struct FastSelect {
         // one radix pass on key bits 19..12 over all candidates
         for (int i = tid; i < 256; i += NTH) s.hist[i] = 0u;
         if (tid == 0) s.bcast[6] = 0u;
-        __syncthreads();
+        cta_sync();
         for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
             const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
             if (q < CS && (uint32_t)j < s.cnt_q[q]) atomicAdd(&s.hist[(s.cand[q][j].x >> 12) & 255u], 1u);
         }
-        __syncthreads();
+        cta_sync();
         stamp(tr, 0);
         if (warp == 0) warp_find_nb<256>(s.hist, krem, s.bcast + 4);
-        __syncthreads();
+        cta_sync();
         stamp(tr, 1);
         const uint32_t bA = s.bcast[4];
         const uint32_t need = krem - s.bcast[5];  // keys to keep inside sub-bin bA (>= 1)
@@ -244,7 +244,7 @@ struct FastSelect {
                     if (((c.x >> 12) & 255u) == bA) s.sub[atomicAdd(&s.bcast[6], 1u)] = c;
                 }
             }
-            __syncthreads();
+            cta_sync();
         }
         for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
             const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
@@ -274,9 +274,9 @@ struct FastSelect {
             const unsigned bal = __ballot_sync(0xffffffffu, take);
             if ((tid & 31) == 0) s.sel2[q][j >> 5] = (uint32_t)__popc(bal);
         }
-        __syncthreads();
+        cta_sync();
         if (tid < 16) s.sel_q[tid] = s.sel2[tid][0] + s.sel2[tid][1];
-        __syncthreads();
+        cta_sync();
         stamp(tr, 2);
         uint32_t off = 0u;
         for (int q = 0; q < rank; ++q) off += s.above_q[q] + s.sel_q[q];
@@ -314,7 +314,7 @@ struct FastSelect {
                     att_sel[i] = i;
                 }
             }
-            __syncthreads();
+            cta_sync();
             return all ? nvis : 0;
         }
         uint32_t off;
@@ -324,7 +324,7 @@ struct FastSelect {
             idx_out[slot] = v0 + i;
             att_sel[slot - off] = i;
         });
-        __syncthreads();
+        cta_sync();
         return nsel;
     }
 };

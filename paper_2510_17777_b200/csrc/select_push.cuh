@@ -63,7 +63,7 @@ __device__ __noinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* warp_sums
         if (lane >= off) x += y;
     }
     if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
+    cta_sync();
     if (warp == 0) {
         uint32_t w = (lane < NW) ? warp_sums[lane] : 0u;
 #pragma unroll
@@ -73,10 +73,10 @@ __device__ __noinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* warp_sums
         }
         if (lane < NW) warp_sums[lane] = w;
     }
-    __syncthreads();
+    cta_sync();
     const uint32_t before = (warp > 0 ? warp_sums[warp - 1] : 0u) + (x - v);
     *total = warp_sums[NW - 1];
-    __syncthreads();
+    cta_sync();
     return before;
 }
 
@@ -132,7 +132,7 @@ __device__ __noinline__ int push_round(cg::cluster_group& cl, PushTopkSmem& s, i
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
     for (int i = tid; i < 256; i += NTH) s.hist[i] = 0u;
-    __syncthreads();
+    cta_sync();
 #pragma unroll 1
     for (int e = 0; e < E; ++e) {  // E is CTA-uniform: every lane reaches the match
         const int i = tid * E + e;
@@ -141,7 +141,7 @@ __device__ __noinline__ int push_round(cg::cluster_group& cl, PushTopkSmem& s, i
         const unsigned peers = __match_any_sync(0xffffffffu, bin);  // warp-aggregated atomics
         if (on && lane == __ffs(peers) - 1) atomicAdd(&s.hist[bin], (uint32_t)__popc(peers));
     }
-    __syncthreads();
+    cta_sync();
     for (int i = tid; i < CS * 64; i += NTH) {
         const int q = i >> 6, c = i & 63;
         uint4* dst = reinterpret_cast<uint4*>(cl.map_shared_rank(&s.allhist[buf][rank][0], q));
@@ -152,7 +152,7 @@ __device__ __noinline__ int push_round(cg::cluster_group& cl, PushTopkSmem& s, i
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         tr[0] = t;
     }
-    cl.sync();
+    cluster_sync(cl);
     if (tr && tid == 0) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -163,9 +163,9 @@ __device__ __noinline__ int push_round(cg::cluster_group& cl, PushTopkSmem& s, i
         for (int q = 0; q < CS; ++q) acc += s.allhist[buf][q][i];
         s.tot[i] = acc;
     }
-    __syncthreads();
+    cta_sync();
     if (warp == 0) warp_find256(s.tot, *krem, s.bcast);
-    __syncthreads();
+    cta_sync();
     if (tr && tid == 0) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -187,7 +187,7 @@ __device__ __noinline__ int push_round(cg::cluster_group& cl, PushTopkSmem& s, i
         const int d = push_digit(keys[i], mode, sh);
         state[i] = (d > b) ? kKeySel : (d == b ? kKeyActive : kKeyOut);
     }
-    __syncthreads();
+    cta_sync();
     return b;
 }
 
@@ -201,19 +201,19 @@ __device__ __noinline__ void block_kth_largest(PushTopkSmem& s, int m, uint32_t 
     for (int pass = 0; pass < 4; ++pass) {
         const int sh = 24 - 8 * pass;
         for (int i = tid; i < 256; i += NTH) s.hist[i] = 0u;
-        __syncthreads();
+        cta_sync();
         for (int i = tid; i < m; i += NTH) {
             const uint32_t v = s.cand[i].x;
             if ((v & M) == P) atomicAdd(&s.hist[(v >> sh) & 255u], 1u);
         }
-        __syncthreads();
+        cta_sync();
         if (tid < 32) warp_find256(s.hist, krem, s.bcast + 4);
-        __syncthreads();
+        cta_sync();
         P |= s.bcast[4] << sh;
         M |= 255u << sh;
         krem -= s.bcast[5];
         above_acc += s.bcast[5];
-        __syncthreads();
+        cta_sync();
     }
     *T = P;
     *n_above = above_acc;
@@ -244,13 +244,13 @@ __device__ __noinline__ uint32_t cluster_topk_push(cg::cluster_group& cl, PushTo
     for (int i = tid; i < nloc; i += NTH) state[i] = init;
     uint32_t tot;
     if (k <= 0 || k >= n) {
-        __syncthreads();
+        cta_sync();
         *cta_offset = (k <= 0) ? 0u : (uint32_t)j0;
         return (k <= 0) ? 0u : (uint32_t)nloc;
     }
     if (tid < 16) s.above_q[tid] = 0u;
     if (tid < 16) s.cand_sel[tid] = 0u;
-    __syncthreads();
+    cta_sync();
     uint32_t krem = (uint32_t)k;
     int buf = 0;
     int blast = push_round<NTH>(cl, s, buf, keys, state, E, nmine, relevance ? 0 : 1, 24, &krem, tr);
@@ -295,7 +295,7 @@ __device__ __noinline__ uint32_t cluster_topk_push(cg::cluster_group& cl, PushTo
             for (int q = 0; q < CS; ++q) cl.map_shared_rank(&s.cand[0], q)[pos] = c;
             ++pos;
         }
-        cl.sync();
+        cluster_sync(cl);
         stamp(tr, 4);
         const int m = (int)cnt;
         uint32_t T, n_gt;
@@ -314,7 +314,7 @@ __device__ __noinline__ uint32_t cluster_topk_push(cg::cluster_group& cl, PushTo
             s.cand_flag[i] = take;
             if (take) atomicAdd(&s.cand_sel[ci.y / (uint32_t)slice], 1u);
         }
-        __syncthreads();
+        cta_sync();
         pos = pos0;
         for (int e = 0; e < nmine; ++e) {
             const int i = tid * E + e;
@@ -323,7 +323,7 @@ __device__ __noinline__ uint32_t cluster_topk_push(cg::cluster_group& cl, PushTo
             ++pos;
         }
     }
-    __syncthreads();
+    cta_sync();
     stamp(tr, 6);
     if (tid == 0) {
         uint32_t off = 0u, mine = 0u;
@@ -335,7 +335,7 @@ __device__ __noinline__ uint32_t cluster_topk_push(cg::cluster_group& cl, PushTo
         s.bcast[2] = off;
         s.bcast[3] = mine;
     }
-    __syncthreads();
+    cta_sync();
     *cta_offset = s.bcast[2];
     stamp(tr, 7);
     return s.bcast[3];

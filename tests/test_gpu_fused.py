@@ -108,10 +108,13 @@ def test_fresh_step_sweep_fallback_sampled(svl, orc):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_fresh_step_simulated_shards_bitwise(svl, P):
+def test_fresh_step_simulated_shards_bitwise(svl, P, monkeypatch):
     """SURVEY.md 4 'simulated-shard test': each rank's (batch x KV-head) slice
-    run separately on one GPU and assembled == the unsharded run, bitwise."""
+    run separately on one GPU and assembled == the unsharded run, bitwise, with
+    the per-unit split count pinned -- the planner may pick
+    a different cluster size for a different number of units."""
     from paper_2510_17777_b200 import sharding
+    monkeypatch.setenv("SVL_FRESH_CS", "8")
     wl = gen.DecodeWorkload("shd", 4, 28, 4, 128, 32, 8192, 300, 819, 1, 256)
     x = gen.make_decode_inputs(wl, seed=38, device="cuda")
     ref, _ = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
@@ -134,3 +137,15 @@ def test_fresh_step_deterministic(svl):
     a, ia = a.clone(), ia.clone()
     b, ib = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
     assert torch.equal(a, b) and torch.equal(ia, ib)
+
+
+@pytest.mark.parametrize("B,nv", [(2, 32768), (8, 32768), (8, 24576)])
+def test_fresh_step_many_units(svl, orc, B, nv):
+    """More units than co-resident 16-CTA clusters (known issue):
+    the planner must pick a safe launch (8-CTA clusters or the two-call path) and the
+    results must still meet the parity bar; run twice back to back (multi-wave)."""
+    base = gen.CONFIGS["long-video"]
+    wl = gen.DecodeWorkload(**{**base.__dict__, "name": f"mu{B}", "B": B, "nv": nv, "k": nv // 10,
+                               "seq_lens": None})
+    _run(svl, orc, wl, seed=40 + B)
+    _run(svl, orc, wl, seed=41 + B)
