@@ -113,7 +113,7 @@ static RetrieveTcLayout retrieve_tc_layout(int B, int n_q, int H, int Hkv, int d
     plan_retrieve_tc((int)units, n_q, g, nv, capacity, visual_only, device_sm_count(), &l.chunk, &l.nkc);
     l.qpack = kWsHeader;
     l.part = round_up(l.qpack + units * l.NQP * d * 2, 256);
-    l.lse2 = round_up(l.part + units * l.NQP * 2 * l.nkc * sizeof(float2), 256);
+    l.lse2 = round_up(l.part + units * l.NQP * 4 * l.nkc * sizeof(float2), 256);
     l.scores = round_up(l.lse2 + units * l.NQP * sizeof(float), 256);
     l.total = round_up(l.scores + units * nv * sizeof(float), 256);
     return l;
@@ -257,7 +257,7 @@ static svl_status retrieve_tc(const void* q, int B, int n_q, int H, int Hkv, int
     p.B = B; p.n_q = n_q; p.H = H; p.Hkv = Hkv; p.g = g; p.NQ = lay.NQ; p.NQP = lay.NQP;
     p.vb = span.visual_begin; p.nv = span.visual_len; p.capacity = K.capacity;
     p.visual_only = vis_only ? 1 : 0;
-    p.chunk = lay.chunk; p.nkc = lay.nkc; p.npart = 2 * lay.nkc;
+    p.chunk = lay.chunk; p.nkc = lay.nkc; p.npart = 4 * lay.nkc;
     p.scale2 = scale * kLog2e;
     p.part = reinterpret_cast<float2*>(w + lay.part);
     p.lse2 = reinterpret_cast<float*>(w + lay.lse2);

@@ -14,7 +14,7 @@
 //             one thread per query row folds a running (max, sum) over its
 //             columns, causal limit j <= seq_len - n_q + r (FULL_PREFIX) or the
 //             visual span only (VISUAL_ONLY); partials per (row, key chunk,
-//             column half) -> workspace.
+//             column quarter) -> workspace.
 //   combine   LSE2[u][n] (base 2) from the partials, or lse_in * log2(e).
 //   pass 1    column mass, operands swapped: S^T = K_blk Q_chunk^T with
 //             M = 128 visual keys, N = 256 query rows per stage; one thread per
@@ -27,8 +27,8 @@
 // a 2-stage ring of Y tiles (256 rows), both loaded by tiled TMA with the
 // 128-B swizzle (K-major UMMA operands), one elected thread issuing
 // tcgen05.mma (M128 N256 K16) into a double-buffered TMEM accumulator
-// (2 x 256 columns), 8 epilogue warps (two per TMEM lane quarter, one per
-// column half) reading it back with tcgen05.ld.
+// (2 x 256 columns), 16 epilogue warps (four per TMEM lane quarter, 64
+// columns each) reading it back with tcgen05.ld.
 #include <algorithm>
 
 #include "common.cuh"
@@ -38,7 +38,8 @@ namespace svl {
 
 namespace {
 
-constexpr int RT_THREADS = 384;  // w0 TMA producer, w1 MMA issuer, w2 TMEM owner, w3 spare, w4-w11 epilogue
+constexpr int RT_THREADS = 640;  // w0 TMA producer, w1 MMA issuer, w2 TMEM owner, w3 spare, w4-w19 epilogue
+constexpr int RT_EPI_WARPS = 16;  // 4 per TMEM lane quarter, 64 accumulator columns each
 constexpr int RT_XROWS = 128;    // UMMA M
 constexpr int RT_YROWS = 256;    // UMMA N per stage
 constexpr int RT_NST = 2;        // Y ring stages
@@ -52,7 +53,7 @@ struct RtSmem {
     static constexpr int Y_OFF = X_OFF + X_BYTES;
     static constexpr int LSE_OFF = Y_OFF + RT_NST * Y_BYTES;  // pass 1: LSE2 of the unit's query rows
     static constexpr int RED_OFF = LSE_OFF + kRtMaxNQ * 4;    // pass 1: [2 halves][128 rows] column-half sums
-    static constexpr int BAR_OFF = RED_OFF + 2 * RT_XROWS * 4;
+    static constexpr int BAR_OFF = RED_OFF + 4 * RT_XROWS * 4;
     static constexpr int BYTES = BAR_OFF + 128;
     static_assert(X_OFF % 1024 == 0 && Y_OFF % 1024 == 0 && Y_BYTES % 1024 == 0, "swizzle atoms");
     static_assert(BYTES <= 227 * 1024, "shared memory");
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_con
     float2* part_out = nullptr;
     if (MODE == 0) {
         const int n = xrow0 + 32 * q4 + lane;
-        part_out = p.part + ((int64_t)u * p.NQP + n) * p.npart + blockIdx.x * 2 + ch;
+        part_out = p.part + ((int64_t)u * p.NQP + n) * p.npart + blockIdx.x * 4 + ch;
         if (nst == 0) {  // empty key chunk (seq_len shorter than the planned range)
             if (warp >= 4) *part_out = make_float2(-INFINITY, 0.f);
             return;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_con
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(afull0 + 8 * a, 1);
-            mbar_init(aempty0 + 8 * a, 8);
+            mbar_init(aempty0 + 8 * a, RT_EPI_WARPS);
         }
         fence_mbar_init();
     }
@@ -221,6 +222,19 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_con
         __syncwarp();
     } else if (warp >= 4) {
         const uint32_t trow = tbase + ((uint32_t)(32 * q4) << 16);
+        // one warp = 32 accumulator rows x 64 columns per stage: both 32-column loads
+        // in flight together, one wait, then the accumulator buffer is released to
+        // the MMA issuer before the exponentials are computed from registers
+        auto load64 = [&](int a, uint32_t (&va)[32], uint32_t (&vb)[32]) {
+            const uint32_t t0 = trow + a * RT_YROWS + ch * 64;
+            tmem_ld32_nowait(t0, va);
+            tmem_ld32_nowait(t0 + 32, vb);
+            tmem_wait_ld_tie(va);
+            tmem_wait_ld_tie(vb);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(aempty0 + 8 * a);
+        };
         if (MODE == 0) {
             const int n = xrow0 + 32 * q4 + lane;
             const int r = n / p.g;
@@ -232,59 +246,61 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_con
                 mbar_wait(afull0 + 8 * a, (s >> 1) & 1);
                 __syncwarp();  // tcgen05.ld is .aligned
                 tc_fence_after();
-#pragma unroll 1
-                for (int c32 = 0; c32 < 4; ++c32) {
-                    const int col0 = ch * 128 + c32 * 32;
-                    const int j0 = y0 + s * RT_YROWS + col0;
-                    uint32_t v[32];
-                    tmem_ld32(trow + a * RT_YROWS + col0, v);
-                    float x[32];
-                    float cm = -INFINITY;
+                uint32_t va[32], vb[32];
+                load64(a, va, vb);
+                const int j0 = y0 + s * RT_YROWS + ch * 64;
+                if (j0 + 64 > jend) {  // a stage crossing the causal / range limit: mask
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        x[i] = (j0 + i < jend) ? __uint_as_float(v[i]) * p.scale2 : -INFINITY;
-                        cm = fmaxf(cm, x[i]);
+                        if (j0 + i >= jend) va[i] = __float_as_uint(-INFINITY);
+                        if (j0 + 32 + i >= jend) vb[i] = __float_as_uint(-INFINITY);
                     }
-                    // branch-free (the next tcgen05.ld is warp-collective): an all-masked
-                    // chunk leaves (m, l) unchanged
-                    const float M = fmaxf(m, cm);
-                    const float Ms = (M == -INFINITY) ? 0.f : M;
-                    float acc = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) acc += fast_exp2(x[i] - Ms);
-                    l = l * fast_exp2(m - Ms) + acc;
-                    m = M;
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(aempty0 + 8 * a);
+                // max on the raw dot products (scale2 > 0), then 2^(s*scale2 - M) by one FMA +
+                // one exponential per element; 3 of 4 exponentials on the SFU, 1 on the FP32 pipe
+                float cm = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) cm = fmaxf(cm, fmaxf(__uint_as_float(va[i]), __uint_as_float(vb[i])));
+                const float M = fmaxf(m, cm * p.scale2);  // an all-masked stage leaves (m, l) unchanged
+                const float Ms = (M == -INFINITY) ? 0.f : M;
+                float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float ya = fmaf(__uint_as_float(va[i]), p.scale2, -Ms);
+                    const float yb = fmaf(__uint_as_float(vb[i]), p.scale2, -Ms);
+                    acc0 += fast_exp2(ya);
+                    acc1 += ((i & 1) == 0) ? fast_exp2(yb) : ((yb < -126.f) ? 0.f : poly_exp2(yb));
+                }
+                l = l * fast_exp2(m - Ms) + (acc0 + acc1);
+                m = M;
             }
             if (n < p.NQP) *part_out = make_float2(m, l);
         } else {
-            float acc = 0.f;
+            float acc0 = 0.f, acc1 = 0.f;
             for (int s = 0; s < nst; ++s) {
                 const int a = s & 1;
                 mbar_wait(afull0 + 8 * a, (s >> 1) & 1);
                 __syncwarp();  // tcgen05.ld is .aligned
                 tc_fence_after();
-#pragma unroll 1
-                for (int c32 = 0; c32 < 4; ++c32) {
-                    const int col0 = ch * 128 + c32 * 32;
-                    const float* ls = lse_s + s * RT_YROWS + col0;
-                    uint32_t v[32];
-                    tmem_ld32(trow + a * RT_YROWS + col0, v);
+                uint32_t va[32], vb[32];
+                load64(a, va, vb);
+                const float4* ls4 = reinterpret_cast<const float4*>(lse_s + s * RT_YROWS + ch * 64);
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {  // SFU and FP32-pipe exponentials alternate
-                        acc += fast_exp2(fmaf(__uint_as_float(v[i]), p.scale2, -ls[i]));
-                        const float y = fmaf(__uint_as_float(v[i + 1]), p.scale2, -ls[i + 1]);
-                        acc += (y < -126.f) ? 0.f : poly_exp2(y);  // padded columns: exactly 0
+                for (int i4 = 0; i4 < 8; ++i4) {  // 3 of 4 exponentials on the SFU, 1 on the FP32 pipe
+                    const float4 la = ls4[i4], lb = ls4[8 + i4];
+                    const float* lav = reinterpret_cast<const float*>(&la);
+                    const float* lbv = reinterpret_cast<const float*>(&lb);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int i = 4 * i4 + e;
+                        const float ya = fmaf(__uint_as_float(va[i]), p.scale2, -lav[e]);
+                        const float yb = fmaf(__uint_as_float(vb[i]), p.scale2, -lbv[e]);
+                        acc0 += fast_exp2(ya);
+                        acc1 += (e != 3) ? fast_exp2(yb) : ((yb < -126.f) ? 0.f : poly_exp2(yb));  // padded: 0
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(aempty0 + 8 * a);
             }
-            reinterpret_cast<float*>(smem + SM::RED_OFF)[ch * RT_XROWS + 32 * q4 + lane] = acc;
+            reinterpret_cast<float*>(smem + SM::RED_OFF)[ch * RT_XROWS + 32 * q4 + lane] = acc0 + acc1;
         }
     }
     tc_fence_before();
@@ -292,7 +308,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_con
     if (MODE == 1 && tid < RT_XROWS) {
         const float* red = reinterpret_cast<const float*>(smem + SM::RED_OFF);
         const int j = blockIdx.x * RT_XROWS + tid;
-        const float sc = red[tid] + red[RT_XROWS + tid];
+        const float sc = (red[tid] + red[RT_XROWS + tid]) + (red[2 * RT_XROWS + tid] + red[3 * RT_XROWS + tid]);
         if (j < p.nv) {
             if (!(sc == sc) || sc == INFINITY) raise_flag(p.flags, 2u /*NONFINITE*/);
             p.scores[(int64_t)u * p.nv + j] = sc;
