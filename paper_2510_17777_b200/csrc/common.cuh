@@ -139,6 +139,13 @@ SVL_DEV void tma_load_4d(uint32_t dst, const void* tmap, int c0, int c1, int c2,
         : "memory");
 }
 
+// 4-D tiled TMA prefetch of one box into L2 (no shared-memory destination, no barrier)
+SVL_DEV void tma_prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(tmap), "r"(c0),
+                 "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
 // ------------------------------------------------- tcgen05 (5th-gen tensor core)
 // TMEM allocation (one warp, .sync.aligned): the TMEM base address is written
 // to the shared word at `slot`.

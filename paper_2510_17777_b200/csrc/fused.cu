@@ -62,7 +62,10 @@ struct FGeom {
     static constexpr int SMAX = kFusedSliceMax / NT;
     static constexpr int ROWB = 2 * D;
     static constexpr int STAGE_BYTES = STAGE_ROWS * ROWB;
-    static constexpr int NST = RING / STAGE_BYTES;  // ring stages
+    static constexpr int TXT_BYTES = kFusedTextMax * ROWB;            // the CTA's text rows (own buffer)
+    static constexpr int NST = (RING - TXT_BYTES) / STAGE_BYTES;      // visual K ring stages
+    static constexpr int TXT_OFF = NST * STAGE_BYTES;
+    static_assert(TXT_OFF + TXT_BYTES <= RING, "text buffer after the ring");
     static_assert(SMAX / STAGE_ROWS * UMMA_N <= LDS_COL, "visual stages fit the TMEM allocation");
     // persistent regions
     static constexpr int QT_OFF = RING;                        // q tile [16][D], K-major SW128 (UMMA B)
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint64_t* mrg = ldsf + GM::NVS_MAX;                    // merge: CS remote arrivals
     uint64_t* vbar = ldsf + GM::NVS_MAX + 1;              // V gathers (TMA variant)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
+    uint64_t* tfull = vbar + 2;                                                 // text rows landed
     float2* wpart = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(vbar + 1) + 16);  // [16][NCP]
     float2* allpart = wpart + (FT / 32) * NCP;                   // [16][NCP] pushed by the peers
     float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
@@ -159,12 +163,13 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     const int slice = p.slice;
     const int v0 = min(p.nv, rank * slice);
     const int nvis = min(p.nv, v0 + slice) - v0;
-    // stage 0 = the text rows (possibly none), then the visual stages (tiled TMA,
-    // 128-B swizzle, tcgen05); the text stage's latency hides under the stream
+    // visual stages through the ring (tiled TMA, 128-B swizzle, tcgen05); the text rows
+    // go to their own buffer (own barrier): sharing a ring slot with them made the
+    // consumers that skip the text rows wait on a parity that a still-pending fill
+    // satisfied (a barrier fault / stale logits when the text copy landed late)
     static_assert(TMAX <= STAGE_ROWS, "text rows fit one stage");
     const int nvs = (nvis + STAGE_ROWS - 1) / STAGE_ROWS;
-    constexpr int toff = 1;
-    const int nstages = nvs + toff;
+    const int nstages = nvs;
     int L = 0, T = 0, t0 = 0, ntext = 0;  // set after griddepcontrol.wait
     const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
     const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
@@ -218,23 +223,21 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // visual stage by mma.sync from the swizzled stage -> TMEM columns LDS_COL + 16 i
     // (splitting d between the two datapaths: the tensor core's smem read of A is
     // the stream's bottleneck), w4-7 = running LSE of the visual rows from TMEM.
-    // Stage s: s = 0 is the text stage when ntext > 0, then visual stage v = s - toff.
     int nsys = 0;
-    auto issue = [&](int s) {
-        const int slot = s % NST;
+    auto issue = [&](int i) {  // visual stage i -> ring slot i % NST
+        const int slot = i % NST;
         const uint32_t dst0 = ring + slot * GM::STAGE_BYTES;
         const uint32_t bar = smem_u32(&full[slot]);
-        if (s >= toff) {
-            const int i = s - toff;
-            // 128 visual rows x D: D/64 boxes of 128 rows x 128 B (rows past the slice
-            // are loaded and ignored; past the capacity the TMA zero-fills)
-            mbar_arrive_expect_tx(bar, (uint32_t)GM::STAGE_BYTES);
+        // 128 visual rows x D: D/64 boxes of 128 rows x 128 B (rows past the slice
+        // are loaded and ignored; past the capacity the TMA zero-fills)
+        mbar_arrive_expect_tx(bar, (uint32_t)GM::STAGE_BYTES);
 #pragma unroll
-            for (int hf = 0; hf < D / 64; ++hf)
-                tma_load_4d(dst0 + hf * (STAGE_ROWS * 128), &p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b, bar);
-            return;
-        }
-        // text rows [t0, t0 + ntext): system rows, then after-visual rows
+        for (int hf = 0; hf < D / 64; ++hf)
+            tma_load_4d(dst0 + hf * (STAGE_ROWS * 128), &p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b, bar);
+    };
+    auto issue_text = [&]() {  // text rows [t0, t0 + ntext): system rows, then after-visual rows
+        const uint32_t dst0 = ring + GM::TXT_OFF;
+        const uint32_t bar = smem_u32(tfull);
         mbar_arrive_expect_tx(bar, (uint32_t)(ntext * ROWB));
         const int seg_n[2] = {nsys, ntext - nsys};
         const int seg_row0[2] = {t0, t0 + nsys + p.nv};
@@ -262,9 +265,21 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 mbar_init(smem_u32(&ldsf[s]), 8);
             }
             mbar_init(vbar_a, 1);
+            mbar_init(smem_u32(tfull), 1);
             mbar_init(smem_u32(mrg), (uint32_t)CS);
             fence_mbar_init();
-            for (int i = 1; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
+            for (int i = 0; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
+#ifndef SVL_L2PF
+#define SVL_L2PF 0  // measured: 31.6 vs 30.0 us/layer with it (long-video) -- off
+#endif
+#if SVL_L2PF
+            // the rest of the visual slice -> L2 (HBM is idle while the upstream kernel's
+            // post-stream phase runs; the ring refills below then hit L2)
+            for (int i = NST; i < nvs; ++i)
+#pragma unroll
+                for (int hf = 0; hf < D / 64; ++hf)
+                    tma_prefetch_4d(&p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b);
+#endif
         }
         __syncwarp();
     }
@@ -285,7 +300,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     }
     nsys = max(0, min(ntext, p.vb - t0));
     if (warp == 0) {
-        if (lane == 0) issue(0);  // the text stage (an empty one completes at once)
+        if (lane == 0) issue_text();  // the text rows (none: completes at once)
         __syncwarp();
     }
     // q tile (UMMA B operand): row c = head G*g + c (zero for c >= g), K-major,
@@ -332,10 +347,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {
-            if (toff) mbar_arrive(smem_u32(&empty[0]));  // text stage: no tensor-core read
             for (int i = 0; i < nvs; ++i) {
-                const int slot = (i + toff) % NST;
-                mbar_wait(smem_u32(&full[slot]), ((i + toff) / NST) & 1);
+                const int slot = i % NST;
+                mbar_wait(smem_u32(&full[slot]), (i / NST) & 1);
                 tc_fence_after();
                 if (p.trace && i < 32) {
                     uint64_t tnow;
@@ -438,10 +452,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         const int src_st = (((((gid & 3) << 1) | (gid >> 2))) << 2) | t;      // holder of row gid (perm^-1)
         // text stage (stage 0, slot 0): 8 warps x 16 rows, mma.sync over all of d (swap-AB,
         // permuted contraction); every warp releases the slot, rows or not
-        if (toff && r16 < ntext) {
-            mbar_wait(smem_u32(&full[0]), 0);
+        if (r16 < ntext) {
+            mbar_wait(smem_u32(tfull), 0);
             __syncwarp();  // mma.sync is .aligned
-            const uint32_t base = ring + (r16 + gid) * ROWB;
+            const uint32_t base = ring + GM::TXT_OFF + (r16 + gid) * ROWB;
             float acc[NT][2][4];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
@@ -475,13 +489,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 }
             }
         }
-        if (toff) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&empty[0]));
-        }
         for (int i = 0; i < nvs; ++i) {
-            const int slot = (i + toff) % NST;
-            mbar_wait(smem_u32(&full[slot]), ((i + toff) / NST) & 1);
+            const int slot = i % NST;
+            mbar_wait(smem_u32(&full[slot]), (i / NST) & 1);
             __syncwarp();  // mma.sync is .aligned
             const uint32_t sbase = ring + slot * GM::STAGE_BYTES;
             float acc[NT][4];
@@ -850,48 +860,7 @@ cudaError_t launch_fresh_t(const FreshParams& p, int CS, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, fresh_kernel<D, NT>, p);
 }
 
-template <int D, int NT>
-int max_active_clusters_t(int CS) {
-    using GM = FGeom<D, NT>;
-    if (cudaFuncSetAttribute(fresh_kernel<D, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-        cudaFuncSetAttribute(fresh_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM::BYTES) != cudaSuccess)
-        return 0;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CS, 1, 1);
-    cfg.blockDim = dim3(FT, 1, 1);
-    cfg.dynamicSmemBytes = GM::BYTES;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, fresh_kernel<D, NT>, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return n;
-}
-
 }  // namespace
-
-// Co-resident clusters of the fused kernel at cluster size CS (cached per device).
-int fresh_max_active_clusters(int d, int g, int CS) {
-    static int cache[8][2][2][17] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int NT = (g + 7) / 8;
-    if (CS < 1 || CS > 16 || NT < 1 || NT > 2) return 0;
-    int& c = cache[dev & 7][d == 128][NT - 1][CS];
-    if (c == 0) {
-        if (d == 128) c = NT == 1 ? max_active_clusters_t<128, 1>(CS) : max_active_clusters_t<128, 2>(CS);
-        else c = NT == 1 ? max_active_clusters_t<64, 1>(CS) : max_active_clusters_t<64, 2>(CS);
-        if (c == 0) c = -1;
-    }
-    return c;
-}
 
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s) {
     const int NT = (p.g + 7) / 8;

@@ -141,9 +141,9 @@ def test_fresh_step_deterministic(svl):
 
 @pytest.mark.parametrize("B,nv", [(2, 32768), (8, 32768), (8, 24576)])
 def test_fresh_step_many_units(svl, orc, B, nv):
-    """More units than co-resident 16-CTA clusters (known issue):
-    the planner must pick a safe launch (8-CTA clusters or the two-call path) and the
-    results must still meet the parity bar; run twice back to back (multi-wave)."""
+    """More clusters than fit at once (later clusters start on SMs vacated by earlier
+    ones): this exposed the text-row / ring-slot parity race fixed in fused.cu (the
+    text rows now have their own buffer and barrier); run twice back to back."""
     base = gen.CONFIGS["long-video"]
     wl = gen.DecodeWorkload(**{**base.__dict__, "name": f"mu{B}", "B": B, "nv": nv, "k": nv // 10,
                                "seq_lens": None})
