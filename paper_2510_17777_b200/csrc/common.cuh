@@ -84,9 +84,38 @@ SVL_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
 // CTA's setup and waits before its first distributed-shared-memory access, so
 // no CTA writes into a peer that has not started yet (the wait is normally
 // free: the peers arrived microseconds earlier).
-SVL_DEV void cluster_arrive_relaxed() {
+SVL_DEV void cluster_arrive_relaxed() {  // release: also publishes the CTA's mbarrier inits
     __syncwarp();
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
+}
+// Address of the same shared-memory offset in cluster CTA `rank` (shared::cluster window).
+SVL_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// Asynchronous stores into a peer CTA's shared memory that count their bytes on the
+// peer's mbarrier (complete_tx): the receiver waits on its own barrier for the bytes
+// it expects; no fence or cluster barrier on the sender's side.
+SVL_DEV void st_async_f32(uint32_t raddr, float a, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(raddr), "f"(a),
+                 "r"(rbar)
+                 : "memory");
+}
+SVL_DEV void st_async_f2(uint32_t raddr, float a, float b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "f"(a), "f"(b), "r"(rbar)
+                 : "memory");
+}
+SVL_DEV void st_async_u2(uint32_t raddr, uint2 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "r"(v.x), "r"(v.y), "r"(rbar)
+                 : "memory");
+}
+SVL_DEV void st_async_u4(uint32_t raddr, uint4 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+                 : "memory");
 }
 SVL_DEV void cluster_wait() {
     __syncwarp();
@@ -213,6 +242,22 @@ SVL_DEV void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr)
         : "memory");
+}
+// 32 lanes x 16 columns, NO wait (pair with tmem_wait_ld_tie16)
+SVL_DEV void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+}
+SVL_DEV void tmem_wait_ld_tie16(uint32_t (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+                 :
+                 : "memory");
 }
 // tcgen05.wait::ld with the loaded registers as in/out operands: no use of them can
 // be scheduled before the wait

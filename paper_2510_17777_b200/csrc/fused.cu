@@ -75,7 +75,7 @@ struct FGeom {
     static constexpr int ATT_BYTES = (SMAX + TMAX) * 4;
     static constexpr int MISC_OFF = ATT_OFF + ATT_BYTES;
     static constexpr int NVS_MAX = SMAX / STAGE_ROWS;
-    static constexpr int MISC_BYTES = 2 * NST * 8 + 2 * NVS_MAX * 8 + 8 + 8 + 16 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
+    static constexpr int MISC_BYTES = 2 * NST * 8 + 2 * NVS_MAX * 8 + 8 + 8 + 48 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
                                       16 * 4 + 64 * 4 + 64 * 8;
     static constexpr int RCV_OFF = MISC_OFF + MISC_BYTES;       // merge receive [CS][per] + l [16][16] fp32
     static constexpr int RCV_FLOATS = 16 * D + 16;              // CS * ceil(g D / CS) <= g D + CS
@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint64_t* vbar = ldsf + GM::NVS_MAX + 1;              // V gathers (TMA variant)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
     uint64_t* tfull = vbar + 2;                                                 // text rows landed
-    float2* wpart = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(vbar + 1) + 16);  // [16][NCP]
+    uint64_t* xbar = vbar + 3;  // [4] DSMEM exchanges (st.async byte counts): 0 = LSE partials
+    float2* wpart = reinterpret_cast<float2*>(vbar + 7);                        // [16][NCP]
     float2* allpart = wpart + (FT / 32) * NCP;                   // [16][NCP] pushed by the peers
     float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
     float* lh = lse2 + NCP;                                      // [16]
@@ -266,7 +267,15 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             }
             mbar_init(vbar_a, 1);
             mbar_init(smem_u32(tfull), 1);
-            mbar_init(smem_u32(mrg), (uint32_t)CS);
+            // every exchange barrier: one local arrival + the bytes the peers will store
+            mbar_init(smem_u32(&xbar[0]), 1);
+            mbar_arrive_expect_tx(smem_u32(&xbar[0]), (uint32_t)(CS * NCP * 8));
+            {
+                const int items = g * D, per = (items + CS - 1) / CS;
+                const int mine = max(0, min(per, items - rank * per));
+                mbar_init(smem_u32(mrg), 1);
+                mbar_arrive_expect_tx(smem_u32(mrg), (uint32_t)(CS * (mine + 16) * 4));
+            }
             fence_mbar_init();
             for (int i = 0; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
 #ifndef SVL_L2PF
@@ -583,9 +592,14 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             const float l2 = __shfl_xor_sync(0xffffffffu, x.y, off);
             lse_merge(x.x, x.y, m2, l2);
         }
-        if (lane < CS) cl.map_shared_rank(allpart, lane)[rank * NCP + warp] = x;
+        if (lane < CS)
+            st_async_f2(mapa_shared(smem_u32(&allpart[rank * NCP + warp]), lane), x.x, x.y,
+                        mapa_shared(smem_u32(&xbar[0]), lane));
     }
-    cluster_sync(cl);
+    // all CS partials landed (this also means every peer has finished its K stream, so
+    // the ring region that later exchanges write into is free everywhere)
+    mbar_wait(smem_u32(&xbar[0]), 0);
+    __syncwarp();
     if (warp < NCP) {
         float2 x = (lane < CS) ? allpart[lane * NCP + warp] : make_float2(-INFINITY, 0.f);
 #pragma unroll
@@ -618,6 +632,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         sel.zero_hist();
         cta_sync();
         // relevance of each visual row = its share of the softmax mass, summed over the g heads
+        // (batching a warp's TMEM loads before one wait measured slower: 30.2 vs 29.7 us/layer)
         for (int i = warp >> 2; i < nvs; i += FT / 128) {
             float v[16];
             load_full(i, v);
@@ -780,8 +795,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // ------------------------------------------------ 5. cluster merge (plain sums)
     // Push style: CTA q owns output items [q*per, (q+1)*per) of the unit's g x D
     // block; every CTA stores its partial of those items (and its 16 l sums)
-    // straight into the owner's receive buffer, then one remote mbarrier arrival
-    // per owner (release, cluster scope).  The owner waits for CS arrivals and
+    // straight into the owner's receive buffer with st.async, which counts the
+    // bytes on the owner's mbarrier.  The owner waits for the bytes it expects and
     // sums in sender order; no CTA reads a peer's shared memory, so a CTA whose
     // inbound pushes have landed may exit at once (no closing cluster barrier).
     const int items = g * D;
@@ -789,17 +804,20 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     float* rcv = reinterpret_cast<float*>(smem + GM::RCV_OFF);   // [CS][per]
     float* lrcv = rcv + GM::RCV_FLOATS;                           // [16][16]
     SVL_TRACE(7);
-    for (int i = tid; i < items; i += FT) {
-        const int q = i / per, j = i - q * per;
-        cl.map_shared_rank(rcv, q)[rank * per + j] = octa[(i / D) * D + (i % D)];
+    {
+        const uint32_t rcv_a = smem_u32(rcv), lrcv_a = smem_u32(lrcv), mrg_a = smem_u32(mrg);
+        for (int i = tid; i < items; i += FT) {
+            const int q = i / per, j = i - q * per;
+            st_async_f32(mapa_shared(rcv_a + (uint32_t)(rank * per + j) * 4u, q), octa[(i / D) * D + (i % D)],
+                         mapa_shared(mrg_a, q));
+        }
+        if (tid < 16 * CS)
+            st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + (tid & 15)) * 4u, tid >> 4), lh[tid & 15],
+                         mapa_shared(mrg_a, tid >> 4));
     }
-    if (tid < 16 * CS) cl.map_shared_rank(lrcv, tid >> 4)[rank * 16 + (tid & 15)] = lh[tid & 15];
-    tc_fence_before();  // every TMEM read of this CTA precedes the barrier (warp 2 deallocates after it)
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    cta_sync();
-    if (tid < CS) mbar_arrive_remote_cluster(smem_u32(mrg), (uint32_t)tid);
+    tc_fence_before();  // every TMEM read of this CTA precedes the dealloc below
     SVL_TRACE(8);
-    mbar_wait_cluster(smem_u32(mrg), 0);
+    mbar_wait(smem_u32(mrg), 0);
     for (int j = tid; j < per; j += FT) {
         const int i = rank * per + j;
         if (i >= items) break;
