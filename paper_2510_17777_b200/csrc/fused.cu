@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint64_t* vbar = ldsf + GM::NVS_MAX + 1;              // V gathers (TMA variant)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
     uint64_t* tfull = vbar + 2;                                                 // text rows landed
-    uint64_t* xbar = vbar + 3;  // [4] DSMEM exchanges (st.async byte counts): 0 = LSE partials
+    uint64_t* xbar = vbar + 3;  // [4] DSMEM exchanges (st.async byte counts): LSE, histograms, candidates
     float2* wpart = reinterpret_cast<float2*>(vbar + 7);                        // [16][NCP]
     float2* allpart = wpart + (FT / 32) * NCP;                   // [16][NCP] pushed by the peers
     float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
@@ -270,6 +270,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             // every exchange barrier: one local arrival + the bytes the peers will store
             mbar_init(smem_u32(&xbar[0]), 1);
             mbar_arrive_expect_tx(smem_u32(&xbar[0]), (uint32_t)(CS * NCP * 8));
+            mbar_init(smem_u32(&xbar[1]), 1);  // top-k histograms: CS x 256 words
+            mbar_arrive_expect_tx(smem_u32(&xbar[1]), (uint32_t)(CS * 1024));
+            mbar_init(smem_u32(&xbar[2]), 1);  // top-k candidates (armed once their count is known)
             {
                 const int items = g * D, per = (items + CS - 1) / CS;
                 const int mine = max(0, min(per, items - rank * per));
@@ -625,6 +628,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     FastSelect<FT> sel(cl, fs, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags,
                        reinterpret_cast<uint32_t*>(smem + GM::WHIST_OFF));
     if (p.trace) sel.tr = trs + 16;
+    sel.hbar = &xbar[1];
+    sel.cbar = &xbar[2];
     int nslots = ntext;
     uint32_t vphase = 0;
     int stage = 0;  // 0 = all / none, 1 = fast path, 2 = generic

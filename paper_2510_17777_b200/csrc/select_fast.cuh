@@ -99,6 +99,10 @@ struct FastSelect {
     uint32_t krem = 0;
     bool nan_seen = false;
     uint64_t* tr = nullptr;  // debug stamps (SVL_TRACE)
+    // st.async exchange barriers (caller-initialised, count 1): hbar armed for CS x 1 KB of
+    // histograms at init; cbar armed here once the candidate counts are known
+    uint64_t* hbar = nullptr;
+    uint64_t* cbar = nullptr;
 
     SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmem& s_, int nvis_, int v0_, int slice_, int nv_, int k_,
                        uint32_t* keys_, uint8_t* state_, uint32_t* flags_, uint32_t* whist_)
@@ -142,11 +146,12 @@ struct FastSelect {
         cta_sync();
         for (int i = tid; i < CS * 64; i += NTH) {
             const int q = i >> 6, c = i & 63;
-            reinterpret_cast<uint4*>(cl.map_shared_rank(&s.allhist[rank][0], q))[c] =
-                reinterpret_cast<const uint4*>(s.hist)[c];
+            st_async_u4(mapa_shared(smem_u32(&s.allhist[rank][4 * c]), q), reinterpret_cast<const uint4*>(s.hist)[c],
+                        mapa_shared(smem_u32(hbar), q));
         }
         stamp(tr, 10);
-        cluster_sync(cl);
+        mbar_wait(smem_u32(hbar), 0);  // all CS histograms landed
+        __syncwarp();
         stamp(tr, 11);
         for (int b = tid; b < 256; b += NTH) {
             uint32_t v[16];
@@ -175,10 +180,15 @@ struct FastSelect {
             }
         }
         cta_sync();
-        uint32_t maxc = 0u;
+        uint32_t maxc = 0u, totc = 0u;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
-        return (bstar == 0 || maxc > (uint32_t)kFastCandPerCta) ? 2 : 1;
+        for (int q = 0; q < 16; ++q) {
+            maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
+            totc += (q < CS) ? s.cnt_q[q] : 0u;
+        }
+        const int st = (bstar == 0 || maxc > (uint32_t)kFastCandPerCta) ? 2 : 1;
+        if (st == 1 && tid == 0) mbar_arrive_expect_tx(smem_u32(cbar), totc * 8u);  // the candidates to come
+        return st;
     }
 
     // V slots for every row with digit >= b* (att_sel[slot] = local row, in
@@ -204,12 +214,14 @@ struct FastSelect {
             if (d == bstar) {
                 st = (uint8_t)(peq + 1);
                 const uint2 c = make_uint2(key, (uint32_t)(v0 + i));
-                for (int q = 0; q < CS; ++q) cl.map_shared_rank(&s.cand[rank][0], q)[peq] = c;
+                const uint32_t dst = smem_u32(&s.cand[rank][peq]), bar = smem_u32(cbar);
+                for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), c, mapa_shared(bar, q));
                 ++peq;
             }
             state[i] = st;
         }
-        cluster_sync(cl);
+        mbar_wait(smem_u32(cbar), 0);  // every peer's candidates landed
+        __syncwarp();
         return (int)(tot & 0xffffu);
     }
 
