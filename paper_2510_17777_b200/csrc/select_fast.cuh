@@ -37,7 +37,7 @@ struct FastSelSmem {
     uint32_t hist[256];
     uint32_t tot[256];
     uint32_t cnt_q[16], above_q[16], sel_q[16];
-    uint32_t sel2[16][kFastCandPerCta / 32];
+    uint32_t sel2[16][kFastCandPerCta / 32];  // ballot masks of the kept candidates
     uint2 sub[kFastSub];
     uint32_t warp_sums[32];
     uint32_t bcast[16];
@@ -97,6 +97,7 @@ struct FastSelect {
     uint32_t* whist;  // [NTH/32][256] private histograms (scratch, dead after the push)
     int bstar = 0;
     uint32_t krem = 0;
+    uint32_t pre_gt = 0, pre_eq = 0;  // rows above b* / in b* before this thread's rows (CTA-local)
     bool nan_seen = false;
     uint64_t* tr = nullptr;  // debug stamps (SVL_TRACE)
     // st.async exchange barriers (caller-initialised, count 1): hbar armed for CS x 1 KB of
@@ -206,6 +207,8 @@ struct FastSelect {
         uint32_t tot;
         const uint32_t pre = block_scan_excl<NTH>(ge | (eq << 16), s.warp_sums, &tot);
         uint32_t pge = pre & 0xffffu, peq = pre >> 16;
+        pre_gt = pge - peq;
+        pre_eq = peq;
         for (int i = i0; i < i1; ++i) {
             const uint32_t key = keys[i];
             const int d = rel_digit(key);
@@ -284,10 +287,10 @@ struct FastSelect {
                 s.cflag[q][j] = take;
             }
             const unsigned bal = __ballot_sync(0xffffffffu, take);
-            if ((tid & 31) == 0) s.sel2[q][j >> 5] = (uint32_t)__popc(bal);
+            if ((tid & 31) == 0) s.sel2[q][j >> 5] = bal;
         }
         cta_sync();
-        if (tid < 16) s.sel_q[tid] = s.sel2[tid][0] + s.sel2[tid][1];
+        if (tid < 16) s.sel_q[tid] = (uint32_t)(__popc(s.sel2[tid][0]) + __popc(s.sel2[tid][1]));
         cta_sync();
         stamp(tr, 2);
         uint32_t off = 0u;
@@ -295,21 +298,26 @@ struct FastSelect {
         int i0, i1;
         my_rows(i0, i1);
         stamp(tr, 5);
-        uint32_t mine = 0u;
+        // output slot of a kept row = off + (rows above b* before it) + (kept b* candidates
+        // before it); both prefixes come from the slot-assignment scan and the candidate
+        // ballot masks, so no second block scan
+        const uint32_t m0 = s.sel2[rank][0], m1 = s.sel2[rank][1];
+        auto kept_cands_before = [&](uint32_t e) -> uint32_t {
+            return e >= 32u ? (uint32_t)__popc(m0) + (uint32_t)__popc(m1 & ((1u << (e - 32u)) - 1u))
+                            : (uint32_t)__popc(m0 & ((1u << e) - 1u));
+        };
+        uint32_t gtc = pre_gt, eqc = pre_eq;
         for (int i = i0; i < i1; ++i) {
             const int d = rel_digit(keys[i]);
-            mine += (d > bstar) || (d == bstar && s.cflag[rank][state[i] - 1]);
-        }
-        uint32_t tot;
-        stamp(tr, 3);
-        uint32_t pos = off + block_scan_excl<NTH>(mine, s.warp_sums, &tot);
-        stamp(tr, 4);
-        for (int i = i0; i < i1; ++i) {
-            const int d = rel_digit(keys[i]);
-            const bool kept = (d > bstar) || (d == bstar && s.cflag[rank][state[i] - 1]);
-            if (kept) idx_out[pos++] = v0 + i;
+            bool kept = d > bstar;
+            if (d == bstar) kept = s.cflag[rank][eqc] != 0;
+            if (kept) idx_out[off + gtc + kept_cands_before(eqc)] = v0 + i;
+            gtc += d > bstar;
+            eqc += d == bstar;
             state[i] = kept ? kKeySel : kKeyOut;
         }
+        stamp(tr, 3);
+        stamp(tr, 4);
     }
 
     // stage 0: k <= 0 or k >= nv; stage 2: generic exact radix.  Writes
