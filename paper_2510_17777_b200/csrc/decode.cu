@@ -23,6 +23,8 @@
 // No second kernel and no global partials.
 #include <cooperative_groups.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -47,7 +49,8 @@ struct DecodeSmem {
     static constexpr int RUN_OFF = PT_OFF + 2 * RB * 16 * 2;  // running M, l, al [3][16]
     static constexpr int RCV_OFF = RUN_OFF + 64 * 4;      // [CS][per] pushed o (CS * per <= 16 D + 16)
     static constexpr int RML_OFF = RCV_OFF + (16 * D + 16) * 4;  // [16][32] pushed M, l
-    static constexpr int BYTES = RML_OFF + 16 * 32 * 4;
+    static constexpr int MB_OFF = RML_OFF + 16 * 32 * 4;     // merge mbarrier (st.async byte count)
+    static constexpr int BYTES = MB_OFF + 16;
 };
 
 // swizzles (physical 16-byte chunk within a row)
@@ -68,7 +71,19 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gid = lane >> 2, t = lane & 3;
     const int u = blockIdx.y;
+    const uint32_t mb = smem_u32(smem + SM::MB_OFF);
+    if (tid == 0) {  // merge barrier: one local arrival + the bytes every peer will store
+        const int items = p.g * D, per = (items + CS - 1) / CS;
+        const int mine = max(0, min(per, items - rank * per));
+        mbar_init(mb, 1);
+        mbar_arrive_expect_tx(mb, (uint32_t)(CS * (mine + 32) * 4));
+        fence_mbar_init();
+    }
     cluster_arrive_relaxed();  // this CTA is resident (peers push into it after their cluster_wait)
+    // programmatic dependent launch: everything above overlaps the upstream kernel's tail;
+    // nothing it may write (seq_len, idx, q, the appended K/V row) is read before this
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint64_t* trace = p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
     auto stamp = [&](int i) {
         if (trace && tid == 0) {
@@ -323,16 +338,16 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
                 const int h = gid + 8 * (e >> 1), dd = warp * 16 + nt * 8 + 2 * t + (e & 1);
                 if (h < p.g) {
                     const int i = h * D + dd, q = i / per;
-                    cl.map_shared_rank(rcv, q)[rank * per + (i - q * per)] = o[nt][e];
+                    st_async_f32(mapa_shared(smem_u32(&rcv[rank * per + (i - q * per)]), q), o[nt][e], mapa_shared(mb, q));
                 }
             }
     }
     for (int i = tid; i < 32 * CS; i += NTH) {  // M[0, 16) and l[16, 32) of every head to every peer
         const int q = i >> 5, h = i & 31;
-        cl.map_shared_rank(rml, q)[rank * 32 + h] = run[h];
+        st_async_f32(mapa_shared(smem_u32(&rml[rank * 32 + h]), q), run[h], mapa_shared(mb, q));
     }
     stamp(11);
-    cluster_sync(cl);
+    mbar_wait(mb, 0);  // the bytes of every peer landed (st.async counts them on this barrier)
     stamp(12);
     for (int i = rank * per + tid; i < min(items, (rank + 1) * per); i += NTH) {
         const int h = i / D, dd = i % D, li = i - rank * per;
@@ -372,7 +387,8 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
             }
         }
     }
-    cluster_sync(cl);  // no CTA exits while a peer may still push into it (pushes precede the first barrier)
+    // no closing cluster barrier: nobody reads a peer's shared memory, and every CTA waited
+    // for all the bytes pushed into it before getting here
     stamp(14);
 }
 
@@ -414,13 +430,15 @@ cudaError_t launch_decode_t(const DecodeParams& p, cudaStream_t s) {
     cfg.blockDim = dim3(NTH);
     cfg.dynamicSmemBytes = SM::BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = p.S;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see griddepcontrol in the kernel
+    attr[1].val.programmaticStreamSerializationAllowed = getenv("SVL_NO_PDL") ? 0 : 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, decode_kernel<D>, p);
 }
 
