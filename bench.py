@@ -424,6 +424,23 @@ def main():
     ms_select = timed(g_select, sub, 10)
     ms_decode = timed(g_decode, sub, 10)
 
+    # ---- pack-once: once per round, then the steady
+    # steps attend the dense packed cache instead of gathering the kept rows
+    packed = [svl.pack_kv(Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l]) for l in range(LAYERS)]
+    ident = torch.arange(wl.k, dtype=torch.int32, device=dev).expand(wl.B, wl.Hkv, wl.k).contiguous()
+    ws_p = svl.Workspace(dev)
+    ws_p.get(256)
+    g_pack = graph_of(lambda: [svl.pack_kv(Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l], Kp=packed[l][0],
+                                           Vp=packed[l][1], ws=ws_p) for l in range(LAYERS)])
+    g_decode_packed = graph_of(lambda: [svl.sparse_decode_attn(qds[l], packed[l][0], packed[l][1], packed[l][2],
+                                                               wl.vb, wl.k, ident, out=outs[l], ws=ws_d)
+                                        for l in range(LAYERS)])
+    ms_pack = timed(g_pack, sub, 10)
+    ms_decode_packed = timed(g_decode_packed, sub, 10)
+    T_att = wl.vb + wl.t_after
+    pack_bytes = 2 * (2 * wl.B * wl.Hkv * (wl.k + T_att) * wl.d * 2)  # read + write of K and V rows
+    del packed
+
     # ---- e2e through the public API with host buffers (pinned)
     q_host = torch.stack(qs).cpu().pin_memory()
     qd_host = torch.stack(qds).cpu().pin_memory()
@@ -548,6 +565,8 @@ def main():
     steady_us = ms_decode * 1e3 / LAYERS
     steady_bytes = nbytes["decode"]
     amort_us = (ms_step * 1e3 / LAYERS + (ROUND_STEPS - 1) * steady_us) / ROUND_STEPS
+    pack_us, steady_packed_us = ms_pack * 1e3 / LAYERS, ms_decode_packed * 1e3 / LAYERS
+    amort_packed_us = (ms_step * 1e3 / LAYERS + pack_us + (ROUND_STEPS - 1) * steady_packed_us) / ROUND_STEPS
 
     # ---- roofline of the dominant kernel (the fused fresh step)
     peak, peak_src = peaks()
@@ -591,6 +610,12 @@ def main():
                        "what": "svl_sparse_decode_attn alone (selected + text K/V), indices reused"},
             "amortized_us_per_layer": amort_us,
             "amortized_what": f"(1 fresh step + {ROUND_STEPS - 1} steady steps) / {ROUND_STEPS} per round",
+            "pack_once": {"what": "svl_pack_kv once per round (kept visual + text K/V -> dense cache), then "
+                                  "svl_sparse_decode_attn over the packed cache (SURVEY.md 8(f) f2)",
+                          "pack_us_per_layer": pack_us,
+                          "pack_GB_s": pack_bytes / (pack_us * 1e-6) / 1e9,
+                          "steady_packed_us_per_layer": steady_packed_us,
+                          "amortized_packed_us_per_layer": amort_packed_us},
             "roofline": {"bound": "hbm", "kernel": "fresh_kernel (svl_fresh_decode_step)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -157,6 +157,29 @@ size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32
                                         int32_t visual_len, int32_t capacity, uint32_t flags);
 
 /*
+ * svl_pack_kv -- pack-once of the retained KV cache (
+ * PAPER.md:124 "compactly packed into a contiguous memory region";
+ * SPEC.md:315-323).  For every unit (b, G) writes into the packed views Kp, Vp:
+ *   rows [0, vb)            = K/V rows [0, vb)                     (system text)
+ *   rows [vb, vb + k)       = K/V rows vb + vis_idx[b][G][m], m ascending
+ *   rows [vb + k, vb + k + seq_len[b] - vb - N_v) = K/V rows [vb + N_v, seq_len[b])
+ * so svl_sparse_decode_attn over (Kp, Vp) with visual_len = k, vis_idx = 0..k-1
+ * and seq_len - N_v + k attends the same rows in the same order as over (K, V)
+ * with vis_idx (bitwise-identical results).  The caller computes the packed
+ * seq_len and appends later tokens to the packed views.
+ *
+ * K, V     source views (identical capacity); span = the source visual span.
+ * vis_idx  device int32 [B][U][k] ascending in [0, N_v) (U = 1 with
+ *          SVL_SELECT_SHARED); violations set SVL_DEVFLAG_INDEX and are clamped.
+ * Kp, Vp   destination views, capacity >= vb + k + (K.capacity - vb - N_v);
+ *          must not overlap the sources.
+ * No workspace beyond the header word (device flags); asynchronous on `stream`.
+ */
+svl_status svl_pack_kv(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
+                       const int32_t* vis_idx, int32_t k, uint32_t flags, svl_kv Kp, svl_kv Vp,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * svl_sparse_decode_attn_push -- svl_sparse_decode_attn for one rank's shard of a
  * head-sharded multi-GPU decode (SURVEY.md 8(b) b7, 8(e) e3 "fused variant"),
  * with the all-gather of the head outputs folded into the kernel: the merged

@@ -465,6 +465,45 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     return SVL_OK;
 }
 
+svl_status svl_pack_kv(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
+                       const int32_t* vis_idx, int32_t k, uint32_t flags, svl_kv Kp, svl_kv Vp, void* ws,
+                       size_t ws_bytes, void* stream) {
+    if (!span.seq_len || (k > 0 && !vis_idx)) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags & ~(SVL_SELECT_SHARED)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (B < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, Hkv must be >= 1%s");
+    if (span.visual_begin < 0 || span.visual_len < 0 ||
+        (int64_t)span.visual_begin + span.visual_len > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span outside the KV capacity%s");
+    if (K.capacity != V.capacity || Kp.capacity != Vp.capacity) return fail(SVL_ERR_SHAPE, "K/V capacities differ%s");
+    if (k < 0 || k > span.visual_len) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, visual_len]%s");
+    const int64_t need = (int64_t)span.visual_begin + k + (K.capacity - span.visual_begin - span.visual_len);
+    if (Kp.capacity < need) return fail(SVL_ERR_SHAPE, "packed capacity < vb + k + (capacity - vb - N_v)%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st == SVL_OK) st = check_kv(V, B, Hkv, d, "V");
+    if (st == SVL_OK) st = check_kv(Kp, B, Hkv, d, "Kp");
+    if (st == SVL_OK) st = check_kv(Vp, B, Hkv, d, "Vp");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws) || ws_bytes < kWsHeader) return fail(SVL_ERR_WORKSPACE, "workspace NULL, misaligned or too small%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+    PackParams p;
+    p.K = static_cast<const uint16_t*>(K.data); p.V = static_cast<const uint16_t*>(V.data);
+    p.ksb = K.stride_b; p.ksh = K.stride_h; p.kst = K.stride_t;
+    p.vsb = V.stride_b; p.vsh = V.stride_h; p.vst = V.stride_t;
+    p.Kp = static_cast<uint16_t*>(const_cast<void*>(Kp.data)); p.Vp = static_cast<uint16_t*>(const_cast<void*>(Vp.data));
+    p.pksb = Kp.stride_b; p.pksh = Kp.stride_h; p.pkst = Kp.stride_t;
+    p.pvsb = Vp.stride_b; p.pvsh = Vp.stride_h; p.pvst = Vp.stride_t;
+    p.seq_len = span.seq_len;
+    p.idx = vis_idx;
+    p.B = B; p.Hkv = Hkv; p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k; p.capacity = K.capacity;
+    p.shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
+    p.flags = static_cast<uint32_t*>(ws);
+    cudaError_t e = launch_pack(p, d, (int)need, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_pack_kv");
+    return SVL_OK;
+}
+
 svl_status svl_sparse_decode_attn(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
                                   svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
                                   int32_t k, uint32_t flags, float scale, float* out,

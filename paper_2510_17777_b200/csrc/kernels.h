@@ -141,6 +141,20 @@ struct RetrTcParams {
 void plan_retrieve_tc(int units, int n_q, int g, int nv, int capacity, bool visual_only, int sms, int* chunk,
                       int* nkc);
 cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s);
+// ------------------------------------------------------ pack-once
+struct PackParams {
+    const uint16_t* K;
+    const uint16_t* V;
+    int64_t ksb, ksh, kst, vsb, vsh, vst;
+    uint16_t* Kp;
+    uint16_t* Vp;
+    int64_t pksb, pksh, pkst, pvsb, pvsh, pvst;
+    const int32_t* seq_len;
+    const int32_t* idx;  // [B][U][k]
+    int B, Hkv, vb, nv, k, capacity, shared;
+    uint32_t* flags;
+};
+cudaError_t launch_pack(const PackParams& p, int d, int max_rows, cudaStream_t s);
 constexpr int kScoreThreads = 512;
 constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA

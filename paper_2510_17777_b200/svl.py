@@ -34,7 +34,7 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
            "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
-           "svl_wait_flags"]
+           "svl_wait_flags", "svl_pack_kv"]
 
 
 class SvlError(RuntimeError):
@@ -72,6 +72,9 @@ def lib():
                                    P, P, P, SZ, P]
         L.svl_retrieve_workspace_size.restype = SZ
         L.svl_retrieve_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, U32]
+        L.svl_pack_kv.restype = ctypes.c_int
+        L.svl_pack_kv.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, I32, U32, svl_kv, svl_kv,
+                                  P, SZ, P]
         L.svl_sparse_decode_attn.restype = ctypes.c_int
         L.svl_sparse_decode_attn.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, P,
                                              I32, U32, F, P, P, P, SZ, P]
@@ -220,6 +223,26 @@ def retrieve(q: torch.Tensor, K: torch.Tensor, seq_len: torch.Tensor, visual_beg
         _cuda(scores_out, "scores_out", torch.float32) if scores_out is not None else None,
         w.data_ptr(), w.numel(), _stream(stream)))
     return idx_out
+
+
+def pack_kv(K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor, visual_begin: int,
+            visual_len: int, vis_idx: torch.Tensor, flags: int = 0, Kp: Optional[torch.Tensor] = None,
+            Vp: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None, stream=None):
+    """svl_pack_kv (pack-once).  Returns (Kp, Vp, seq_len_packed):
+    the packed caches [B][Hkv][vb + k + cap - vb - N_v][d] and seq_len - N_v + k."""
+    B, Hkv, cap, d = K.shape
+    k = vis_idx.shape[-1]
+    pcap = visual_begin + k + (cap - visual_begin - visual_len)
+    if Kp is None:
+        Kp = torch.empty(B, Hkv, pcap, d, dtype=K.dtype, device=K.device)
+    if Vp is None:
+        Vp = torch.empty(B, Hkv, pcap, d, dtype=V.dtype, device=V.device)
+    w = _ws(ws, K.device).get(256)
+    _check(lib().svl_pack_kv(kv_view(K, "K"), kv_view(V, "V"), B, Hkv, d,
+                             span(visual_begin, visual_len, seq_len),
+                             _cuda(vis_idx, "vis_idx", torch.int32), k, flags, kv_view(Kp, "Kp"),
+                             kv_view(Vp, "Vp"), w.data_ptr(), w.numel(), _stream(stream)))
+    return Kp, Vp, (seq_len - visual_len + k).to(torch.int32)
 
 
 def sparse_decode_attn(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor,
