@@ -29,6 +29,8 @@
 // tcgen05.mma (M128 N256 K16) into a double-buffered TMEM accumulator
 // (2 x 256 columns), 16 epilogue warps (four per TMEM lane quarter, 64
 // columns each) reading it back with tcgen05.ld.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -320,6 +322,154 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_tc_kernel(const __grid_con
     }
 }
 
+
+// Column mass with the query tile RESIDENT (NQP == 256: n_q * g <= 256, e.g. a
+// 32-row question at g = 7): one 256-row Q tile per unit stays in shared memory
+// and the CTA walks key blocks kb = blockIdx.x, += gridDim.x through a 2-slot
+// X ring, so the per-CTA setup (TMEM, barriers, Q and LSE loads) is paid once
+// instead of once per 128 keys.  Same math and summation order as mode 1.
+template <int D>
+struct RqSmem {
+    static constexpr int NB = D / 64;
+    static constexpr int X_BYTES = NB * RT_XROWS * 128;
+    static constexpr int Y_BYTES = NB * RT_YROWS * 128;
+    static constexpr int X_OFF = 0;                               // [2 slots] K blocks
+    static constexpr int Y_OFF = X_OFF + 2 * X_BYTES;             // the unit's Q tile
+    static constexpr int LSE_OFF = Y_OFF + Y_BYTES;               // LSE2 [256]
+    static constexpr int RED_OFF = LSE_OFF + RT_YROWS * 4;        // [2 items][4 quarters][128 rows]
+    static constexpr int BAR_OFF = RED_OFF + 2 * 4 * RT_XROWS * 4;
+    static constexpr int BYTES = BAR_OFF + 128;
+    static_assert(Y_OFF % 1024 == 0 && X_BYTES % 1024 == 0, "swizzle atoms");
+    static_assert(BYTES <= 227 * 1024, "shared memory");
+};
+
+template <int D>
+__global__ void __launch_bounds__(RT_THREADS, 1) retr_mass_qres_kernel(const __grid_constant__ RetrTcParams p) {
+    using SM = RqSmem<D>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr uint32_t IDESC = umma_idesc_bf16(RT_XROWS, RT_YROWS);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    const uint32_t yfull = smem_u32(bars), xfull0 = smem_u32(bars + 1), xempty0 = smem_u32(bars + 3);
+    const uint32_t afull0 = smem_u32(bars + 5), aempty0 = smem_u32(bars + 7);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
+    const uint32_t sX = smem_u32(smem + SM::X_OFF), sY = smem_u32(smem + SM::Y_OFF);
+    float* lse_s = reinterpret_cast<float*>(smem + SM::LSE_OFF);
+    float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);
+    const int u = blockIdx.y, b = u / p.Hkv, G = u % p.Hkv;
+    const int nkb = (p.nv + RT_XROWS - 1) / RT_XROWS;
+    const int nit = blockIdx.x < nkb ? (nkb - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (nit == 0) return;
+    const int q4 = warp & 3, ch = (warp - 4) >> 2;
+
+    if (tid == 0) {
+        mbar_init(yfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(xfull0 + 8 * i, 1);
+            mbar_init(xempty0 + 8 * i, 1);
+            mbar_init(afull0 + 8 * i, 1);
+            mbar_init(aempty0 + 8 * i, RT_EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(smem_u32(tslot), 512);
+    for (int i = tid; i < RT_YROWS; i += RT_THREADS) lse_s[i] = p.lse2[(int64_t)u * p.NQP + i];
+    tc_fence_before();
+    cta_sync();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(yfull, (uint32_t)SM::Y_BYTES);
+#pragma unroll
+            for (int hf = 0; hf < SM::NB; ++hf)
+                tma_load_4d(sY + hf * (RT_YROWS * 128), &p.ymap, hf * 64, 0, 0, u, yfull);
+            for (int j = 0; j < nit; ++j) {
+                const int slot = j & 1, kb = blockIdx.x + j * gridDim.x;
+                if (j >= 2) mbar_wait(xempty0 + 8 * slot, ((j >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(xfull0 + 8 * slot, (uint32_t)SM::X_BYTES);
+#pragma unroll
+                for (int hf = 0; hf < SM::NB; ++hf)
+                    tma_load_4d(sX + slot * SM::X_BYTES + hf * (RT_XROWS * 128), &p.xmap, hf * 64,
+                                p.vb + kb * RT_XROWS, G, b, xfull0 + 8 * slot);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_wait(yfull, 0);
+            for (int j = 0; j < nit; ++j) {
+                const int slot = j & 1, a = j & 1;
+                mbar_wait(xfull0 + 8 * slot, (j >> 1) & 1);
+                if (j >= 2) mbar_wait(aempty0 + 8 * a, ((j >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t xb = sX + slot * SM::X_BYTES;
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const int hf = k >> 2, kk = k & 3;
+                    umma_bf16(tbase + a * RT_YROWS, sw128_desc(xb + hf * (RT_XROWS * 128) + kk * 32),
+                              sw128_desc(sY + hf * (RT_YROWS * 128) + kk * 32), IDESC, k > 0 ? 1u : 0u);
+                }
+                umma_commit(xempty0 + 8 * slot);
+                umma_commit(afull0 + 8 * a);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        const uint32_t trow = tbase + ((uint32_t)(32 * q4) << 16);
+        const float4* ls4 = reinterpret_cast<const float4*>(lse_s + ch * 64);
+        for (int j = 0; j < nit; ++j) {
+            const int a = j & 1;
+            mbar_wait(afull0 + 8 * a, (j >> 1) & 1);
+            __syncwarp();  // tcgen05.ld is .aligned
+            tc_fence_after();
+            uint32_t va[32], vb[32];
+            const uint32_t t0 = trow + a * RT_YROWS + ch * 64;
+            tmem_ld32_nowait(t0, va);
+            tmem_ld32_nowait(t0 + 32, vb);
+            tmem_wait_ld_tie(va);
+            tmem_wait_ld_tie(vb);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(aempty0 + 8 * a);
+            float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+            for (int i4 = 0; i4 < 8; ++i4) {  // 3 of 4 exponentials on the SFU, 1 on the FP32 pipe
+                const float4 la = ls4[i4], lb = ls4[8 + i4];
+                const float* lav = reinterpret_cast<const float*>(&la);
+                const float* lbv = reinterpret_cast<const float*>(&lb);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int i = 4 * i4 + e;
+                    const float ya = fmaf(__uint_as_float(va[i]), p.scale2, -lav[e]);
+                    const float yb = fmaf(__uint_as_float(vb[i]), p.scale2, -lbv[e]);
+                    acc0 += fast_exp2(ya);
+                    acc1 += (e != 3) ? fast_exp2(yb) : ((yb < -126.f) ? 0.f : poly_exp2(yb));
+                }
+            }
+            float* rj = red + (j & 1) * (4 * RT_XROWS);
+            rj[ch * RT_XROWS + 32 * q4 + lane] = acc0 + acc1;
+            asm volatile("bar.sync 1, %0;" ::"n"(RT_EPI_WARPS * 32) : "memory");  // the 16 epilogue warps
+            if (ch == 0) {
+                const int row = 32 * q4 + lane;
+                const int jj = (blockIdx.x + j * gridDim.x) * RT_XROWS + row;
+                const float sc = (rj[row] + rj[RT_XROWS + row]) + (rj[2 * RT_XROWS + row] + rj[3 * RT_XROWS + row]);
+                if (jj < p.nv) {
+                    if (!(sc == sc) || sc == INFINITY) raise_flag(p.flags, 2u /*NONFINITE*/);
+                    p.scores[(int64_t)u * p.nv + jj] = sc;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cta_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tbase, 512);
+    }
+}
+
 template <int MODE, int D>
 cudaError_t launch_tc(const RetrTcParams& p, dim3 grid, cudaStream_t s) {
     static bool attr_done[64] = {};
@@ -373,7 +523,26 @@ cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s) {
     RetrTcParams p1 = p;
     p1.xmap = p.kmap_x;  // X = K blocks
     p1.ymap = p.qmap_y;  // Y = Q chunks
-    const dim3 g1((p.nv + RT_XROWS - 1) / RT_XROWS, units, 1);
+    const int nkb = (p.nv + RT_XROWS - 1) / RT_XROWS;
+    if (p.NQP == RT_YROWS && !getenv("SVL_RT_NO_QRES")) {  // Q tile resident, CTAs walk key blocks
+        const int per_unit = std::max(1, std::min(nkb, (2 * sms + units - 1) / units));
+        const dim3 g2(per_unit, units, 1);
+        static bool attr_done[64][2] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && !attr_done[dev][d == 128]) {
+            e = d == 128 ? cudaFuncSetAttribute(retr_mass_qres_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                RqSmem<128>::BYTES)
+                         : cudaFuncSetAttribute(retr_mass_qres_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                RqSmem<64>::BYTES);
+            if (e != cudaSuccess) return e;
+            attr_done[dev][d == 128] = true;
+        }
+        if (d == 128) retr_mass_qres_kernel<128><<<g2, RT_THREADS, RqSmem<128>::BYTES, s>>>(p1);
+        else retr_mass_qres_kernel<64><<<g2, RT_THREADS, RqSmem<64>::BYTES, s>>>(p1);
+        return cudaGetLastError();
+    }
+    const dim3 g1(nkb, units, 1);
     return d == 128 ? launch_tc<1, 128>(p1, g1, s) : launch_tc<1, 64>(p1, g1, s);
 }
 

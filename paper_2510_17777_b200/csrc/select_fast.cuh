@@ -126,7 +126,15 @@ struct FastSelect {
     SVL_DEV void add_key(int i, float score) {
         const uint32_t key = float_key(score, nan_seen);
         keys[i] = key;
+#if SVL_HIST_MATCH
+        // lanes with the same bin aggregate first (one atomic per distinct bin per warp)
+        const int dg = rel_digit(key);
+        const unsigned peers = __match_any_sync(__activemask(), dg);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1)
+            atomicAdd(&whist[(threadIdx.x >> 5) * 256 + dg], (uint32_t)__popc(peers));
+#else
         atomicAdd(&whist[(threadIdx.x >> 5) * 256 + rel_digit(key)], 1u);
+#endif
     }
 
     // returns 1 (fast path) or 2 (generic path); all threads, after the add_key pass
