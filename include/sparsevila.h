@@ -107,7 +107,10 @@ typedef struct {
  *               index, written ascending, relative to visual_begin.
  *
  * q        device bf16 [B][n_q][H][d] contiguous (post-RoPE; reading A10).
- *          n_q*g <= 32 in this version.
+ *          n_q*g <= 4096.  n_q*g <= 32 runs the CUDA-core GEMV path; larger
+ *          n_q*g (a question chunk) runs the tensor-core path
+ *          (tcgen05 row-LSE pass + column-mass pass), which
+ *          needs K encodable as a TMA tensor map (SVL_ERR_UNSUPPORTED if not).
  * K        device KV view (see svl_kv).
  * span     visual span + device seq_len[B]; visual_len <= 131072.
  * lse_in   device fp32 [B][n_q][H] or NULL.

@@ -101,7 +101,8 @@ def test_retrieve_host_validation(svl, case, status):
     elif case == "span_capacity":
         args["sp"] = svl.svl_span(50, 60, P)
     elif case == "big_group":
-        args["n_q"] = 5
+        args["n_q"] = 600           # n_q * g = 4200 > 4096 query rows per unit
+        args["K"] = _kv(cap=1000)
     rc = L.svl_retrieve(*args.values())
     assert rc == status, (rc, L.svl_last_error_message())
     assert L.svl_last_error_message()
@@ -215,3 +216,34 @@ def test_push_host_validation(svl, case, status):
     assert rc == status, (rc, L.svl_last_error_message())
     rc = L.svl_wait_flags(P_, 0 if case == "P0" else 2, 0 if case == "epoch0" else 1, None, None)
     assert rc == 1
+
+
+@pytest.mark.parametrize("case,status", [
+    ("small_packed", 2), ("k_gt_nv", 1), ("bad_flags", 1), ("null_idx", 1), ("bad_d", 5), ("null_ws", 4),
+    ("cap_mismatch", 2)])
+def test_pack_host_validation(svl, case, status):
+    """svl_pack_kv: host-checkable errors return before any launch."""
+    L = svl.lib()
+    P = 0x10000
+    sv = svl_mod()
+    # source capacity 100, span [10, 70): packed capacity needed = 10 + k + 30
+    args = dict(K=_kv(), V=_kv(), B=1, Hkv=4, d=128, sp=sv.svl_span(10, 60, P), idx=P, k=20, flags=0,
+                Kp=_kv(cap=60), Vp=_kv(cap=60), ws=P, wsb=1 << 20, st=None)
+    if case == "small_packed":
+        args["Kp"], args["Vp"] = _kv(cap=59), _kv(cap=59)
+    elif case == "k_gt_nv":
+        args["k"] = 61
+    elif case == "bad_flags":
+        args["flags"] = 4
+    elif case == "null_idx":
+        args["idx"] = None
+    elif case == "bad_d":
+        args["d"] = 96
+        for key in ("K", "V", "Kp", "Vp"):
+            args[key] = _kv(cap=100 if key in ("K", "V") else 60, d=96)
+    elif case == "null_ws":
+        args["ws"] = None
+    elif case == "cap_mismatch":
+        args["Vp"] = _kv(cap=61)
+    rc = L.svl_pack_kv(*args.values())
+    assert rc == status, (rc, L.svl_last_error_message())
