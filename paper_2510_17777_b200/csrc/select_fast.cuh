@@ -226,7 +226,8 @@ struct FastSelect {
                 st = (uint8_t)(peq + 1);
                 const uint2 c = make_uint2(key, (uint32_t)(v0 + i));
                 const uint32_t dst = smem_u32(&s.cand[rank][peq]), bar = smem_u32(cbar);
-                for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), c, mapa_shared(bar, q));
+                if (peq < (uint32_t)kFastCandPerCta)  // always true on this path (threshold() checked); defensive
+                    for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), c, mapa_shared(bar, q));
                 ++peq;
             }
             state[i] = st;

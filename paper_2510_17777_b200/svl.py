@@ -72,9 +72,10 @@ def lib():
                                    P, P, P, SZ, P]
         L.svl_retrieve_workspace_size.restype = SZ
         L.svl_retrieve_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, U32]
-        L.svl_pack_kv.restype = ctypes.c_int
-        L.svl_pack_kv.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, I32, U32, svl_kv, svl_kv,
-                                  P, SZ, P]
+        if hasattr(L, "svl_pack_kv"):  # (older experiment builds predate it; the ABI test checks it)
+            L.svl_pack_kv.restype = ctypes.c_int
+            L.svl_pack_kv.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, I32, U32, svl_kv, svl_kv,
+                                      P, SZ, P]
         L.svl_sparse_decode_attn.restype = ctypes.c_int
         L.svl_sparse_decode_attn.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, P,
                                              I32, U32, F, P, P, P, SZ, P]
