@@ -526,6 +526,24 @@ def main():
                    "bf16_peak_tflops": bf16_peak,
                    "salience_frac": (flops / (ms_sal * 1e-3) / 1e12 / bf16_peak) if bf16_peak else None,
                    "prune_us": ms_prune * 1e3, "kept": int(kept.numel())}
+        # f4(i): unified RoPE remap of the kept tokens (pre-RoPE K rotated to their new
+        # contiguous positions, V compacted) on the LLM cache the prune feeds: 4 KV heads, d 128
+        rw = gen.CONFIGS[WORKLOAD]
+        nvp, kp_ = int(pw.F * pw.Nf), int(kept.numel())
+        capr = rw.vb + nvp + rw.t_after
+        Kpre = torch.randn(1, rw.Hkv, capr, rw.d, device=dev).to(torch.bfloat16)
+        Vpre = torch.randn(1, rw.Hkv, capr, rw.d, device=dev).to(torch.bfloat16)
+        seqr = torch.tensor([capr], dtype=torch.int32, device=dev)
+        kept_rel = kept.view(1, -1).contiguous()
+        Kro, Vro, _ = svl.rope_remap(Kpre, Vpre, seqr, rw.vb, nvp, kept_rel, 1000000.0)
+        g_rope = graph_of(lambda: svl.rope_remap(Kpre, Vpre, seqr, rw.vb, nvp, kept_rel, 1000000.0,
+                                                 K_out=Kro, V_out=Vro, ws=ws_p))
+        ms_rope = timed(g_rope, 50, 5)
+        rope_bytes = 2 * 2 * rw.Hkv * (rw.vb + kp_ + rw.t_after) * rw.d * 2  # K, V rows read + written
+        prefill.update({"rope_remap_us": ms_rope * 1e3, "rope_remap_GB_s": rope_bytes / (ms_rope * 1e-3) / 1e9,
+                        "rope_remap_what": f"svl_rope_remap: {nvp} visual -> {kp_} kept + {rw.vb + rw.t_after} "
+                                           f"text rows, {rw.Hkv} KV heads, d {rw.d}, base 1e6 (SURVEY 8(f) f4(i))"})
+        del Kpre, Vpre, Kro, Vro
 
     # ---- question-chunk retrieval on tcgen05: svl_retrieve
     # with n_q question rows on the long-video cache, FULL_PREFIX normalisation computed in-kernel

@@ -160,6 +160,32 @@ size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32
                                         int32_t visual_len, int32_t capacity, uint32_t flags);
 
 /*
+ * svl_rope_remap -- unified RoPE remap after prefill pruning (SURVEY.md 8(f)
+ * f4(i); "retain a contiguous range of position indices
+ * corresponding to the preserved visual tokens").
+ * For each batch row b (L = seq_len[b]) the compacted cache row w, which is
+ * also its new position, takes
+ *   old row w                      for w < vb                 (system text)
+ *   old row vb + kept[b][w - vb]   for vb <= w < vb + k       (kept visual)
+ *   old row w - k + N_v            for vb + k <= w < L - N_v + k  (later text)
+ * K_out[b][G][w] = RoPE(K_pre[b][G][old], position w), rotate-half pairs
+ * (c, c + d/2), theta_c = w * rope_base^(-2c/d) (angles in double, rotation
+ * fp32, bf16 RNE output); V_out[b][G][w] = V[b][G][old] (skipped if V.data is
+ * NULL).  The new seq_len is L - N_v + k (the caller's).  Applied once at
+ * prefill-prune time; decode-stage retrieval does not remap.
+ *
+ * K_pre    PRE-RoPE keys at their original rows; V the values (or data NULL).
+ * span     the original visual span and device seq_len [B].
+ * kept     device int32 [B][k] ascending in [0, N_v) (svl_prefill_prune's output
+ *          relative to vb); violations set SVL_DEVFLAG_INDEX and are clamped.
+ * K_out, V_out  destination views, capacity >= vb + k + (K_pre.capacity - vb - N_v),
+ *          not overlapping the sources.
+ */
+svl_status svl_rope_remap(svl_kv K_pre, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
+                          const int32_t* kept, int32_t k, double rope_base, svl_kv K_out, svl_kv V_out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * svl_pack_kv -- pack-once of the retained KV cache (
  * PAPER.md:124 "compactly packed into a contiguous memory region";
  * SPEC.md:315-323).  For every unit (b, G) writes into the packed views Kp, Vp:

@@ -62,6 +62,7 @@ def lib():
         L.o_salience.argtypes = [P, P, I, I, I, I, I, I, D, P, I]
         L.o_prune.restype = I
         L.o_prune.argtypes = [P, I, I, P, I, D, P, I, P]
+        L.o_rope_remap.argtypes = [P, I, I, I, I, P, I, I, P, I, D, P, I, P]
         _lib = L
     return _lib
 
@@ -192,3 +193,22 @@ def prune(saliency, s: float, frame_offsets=None):
                        _ptr(kept), cap, ctypes.addressof(tot))
     _check(rc, "o_prune")
     return kept[:, :tot.value], tot.value
+
+
+def rope_remap(K_pre, seq_len, vb: int, nv: int, kept, base: float, cap_out: int | None = None):
+    """Unified RoPE remap after pruning.  K_pre bf16 [B][Hkv][cap][d]
+    (pre-RoPE keys at their original rows); kept int32 [B][k] ascending, relative to vb.
+    Returns (K_post float64 [B][Hkv][cap_out][d] unrounded, rows int32 [B][cap_out] old row or -1)."""
+    Kc = K_pre.contiguous()
+    B, Hkv, cap, d = Kc.shape
+    kp = np.ascontiguousarray(np.asarray(kept, dtype=np.int32))
+    k = kp.shape[-1]
+    sl = np.ascontiguousarray(np.asarray(seq_len, dtype=np.int32))
+    cap_out = cap - nv + k if cap_out is None else cap_out
+    out = np.zeros((B, Hkv, cap_out, d), np.float64)
+    rows = np.zeros((B, cap_out), np.int32)
+    ku = _u16(Kc)
+    rc = lib().o_rope_remap(_ptr(ku), B, Hkv, d, cap, _ptr(sl), vb, nv, _ptr(kp), k, base, _ptr(out),
+                            cap_out, _ptr(rows))
+    _check(rc, "o_rope_remap")
+    return out, rows

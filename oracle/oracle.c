@@ -417,3 +417,61 @@ int o_prune(const float* sal, int B, int N, const int32_t* frame_offsets, int n_
     free(tmp);
     return err;
 }
+
+/* ---------------------------------------------------------------------------
+ * Unified RoPE remap after prefill pruning (PAPER.md:127
+ * "we simply retain a contiguous range of position indices corresponding to
+ * the preserved visual tokens"; SPEC.md:421-427 remap_unified
+ * "remap recomputes post-RoPE keys from stored pre-RoPE keys").
+ *
+ * Plan (per batch row b, seq_len L = seq_len[b]):
+ *   new row / position w in [0, vb)             <- old row w          (system text)
+ *   w = vb + i, i < k                           <- old row vb + kept[b][i]
+ *   w in [vb + k, vb + k + (L - vb - nv))       <- old row w - k + nv (later text)
+ * so kept visual token i gets position vb + i, the text start moves from vb + nv
+ * to vb + k (delta = k - nv <= 0).
+ * Rotation (rotate-half convention of the cited model family, pairs (c, c + d/2)):
+ *   theta_c = p * base^(-2c/d),  c < d/2
+ *   out[c]       = x[c] cos theta_c - x[c + d/2] sin theta_c
+ *   out[c + d/2] = x[c + d/2] cos theta_c + x[c] sin theta_c
+ * in double, NOT rounded (the test compares the kernel's bf16 within one ulp).
+ * rows_out[b][w] = the old row copied into w (or -1 past the packed length).
+ * --------------------------------------------------------------------------- */
+int o_rope_remap(const uint16_t* Kpre, int B, int Hkv, int d, int cap, const int32_t* seq_len, int vb, int nv,
+                 const int32_t* kept, int k, double base, double* Kout, int cap_out, int32_t* rows_out) {
+    if (B < 1 || Hkv < 1 || d < 2 || (d & 1) || vb < 0 || nv < 0 || k < 0 || k > nv || !(base > 1.0))
+        return O_ERR_ARG;
+    for (int b = 0; b < B; ++b) {
+        const int L = seq_len[b];
+        if (L < vb + nv || L > cap) return O_ERR_SHAPE;
+        const int n_out = vb + k + (L - vb - nv);
+        if (n_out > cap_out) return O_ERR_SHAPE;
+        for (int i = 0; i < k; ++i) {
+            const int x = kept[(int64_t)b * k + i];
+            if (x < 0 || x >= nv || (i > 0 && kept[(int64_t)b * k + i - 1] >= x)) return O_ERR_ORDER;
+        }
+        for (int w = 0; w < cap_out; ++w) {
+            int old = -1;
+            if (w < vb) old = w;
+            else if (w < vb + k) old = vb + kept[(int64_t)b * k + (w - vb)];
+            else if (w < n_out) old = w - k + nv;
+            rows_out[(int64_t)b * cap_out + w] = old;
+            for (int G = 0; G < Hkv; ++G) {
+                double* o = Kout + (((int64_t)b * Hkv + G) * cap_out + w) * d;
+                if (old < 0) {
+                    for (int c = 0; c < d; ++c) o[c] = 0.0;
+                    continue;
+                }
+                const uint16_t* xk = Kpre + (((int64_t)b * Hkv + G) * cap + old) * d;
+                const double p = (double)w;  /* unified: the new position is the new row */
+                for (int c = 0; c < d / 2; ++c) {
+                    const double theta = p * pow(base, -2.0 * (double)c / (double)d);
+                    const double x1 = bf(xk[c]), x2 = bf(xk[c + d / 2]);
+                    o[c] = x1 * cos(theta) - x2 * sin(theta);
+                    o[c + d / 2] = x2 * cos(theta) + x1 * sin(theta);
+                }
+            }
+        }
+    }
+    return 0;
+}

@@ -155,6 +155,23 @@ struct PackParams {
     uint32_t* flags;
 };
 cudaError_t launch_pack(const PackParams& p, int d, int max_rows, cudaStream_t s);
+// -------------------------------------------- RoPE remap
+struct RopeParams {
+    const uint16_t* K;  // pre-RoPE keys
+    int64_t ksb, ksh, kst;
+    const uint16_t* V;  // nullable
+    int64_t vsb, vsh, vst;
+    uint16_t* Ko;
+    int64_t osb, osh, ost;
+    uint16_t* Vo;
+    int64_t vosb, vosh, vost;
+    const int32_t* seq_len;
+    const int32_t* kept;  // [B][k]
+    int B, Hkv, d, vb, nv, k, capacity;
+    double log2_base;
+    uint32_t* flags;
+};
+cudaError_t launch_rope_remap(const RopeParams& p, int max_rows, cudaStream_t s);
 constexpr int kScoreThreads = 512;
 constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA

@@ -34,7 +34,7 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
            "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
-           "svl_wait_flags", "svl_pack_kv"]
+           "svl_wait_flags", "svl_pack_kv", "svl_rope_remap"]
 
 
 class SvlError(RuntimeError):
@@ -72,6 +72,10 @@ def lib():
                                    P, P, P, SZ, P]
         L.svl_retrieve_workspace_size.restype = SZ
         L.svl_retrieve_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, U32]
+        if hasattr(L, "svl_rope_remap"):
+            L.svl_rope_remap.restype = ctypes.c_int
+            L.svl_rope_remap.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, I32, D, svl_kv, svl_kv,
+                                         P, SZ, P]
         if hasattr(L, "svl_pack_kv"):  # (older experiment builds predate it; the ABI test checks it)
             L.svl_pack_kv.restype = ctypes.c_int
             L.svl_pack_kv.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, I32, U32, svl_kv, svl_kv,
@@ -224,6 +228,29 @@ def retrieve(q: torch.Tensor, K: torch.Tensor, seq_len: torch.Tensor, visual_beg
         _cuda(scores_out, "scores_out", torch.float32) if scores_out is not None else None,
         w.data_ptr(), w.numel(), _stream(stream)))
     return idx_out
+
+
+def rope_remap(K_pre: torch.Tensor, V: Optional[torch.Tensor], seq_len: torch.Tensor, visual_begin: int,
+               visual_len: int, kept: torch.Tensor, rope_base: float = 10000.0,
+               K_out: Optional[torch.Tensor] = None, V_out: Optional[torch.Tensor] = None,
+               ws: Optional[Workspace] = None, stream=None):
+    """svl_rope_remap (unified RoPE remap after pruning).
+    kept int32 [B][k] relative to visual_begin.  Returns (K_out, V_out or None, seq_len_new)."""
+    B, Hkv, cap, d = K_pre.shape
+    k = kept.shape[-1]
+    ocap = visual_begin + k + (cap - visual_begin - visual_len)
+    if K_out is None:
+        K_out = torch.zeros(B, Hkv, ocap, d, dtype=K_pre.dtype, device=K_pre.device)
+    if V is not None and V_out is None:
+        V_out = torch.zeros(B, Hkv, ocap, d, dtype=V.dtype, device=V.device)
+    null_kv = svl_kv(None, 0, 0, 0, 0)
+    w = _ws(ws, K_pre.device).get(256)
+    _check(lib().svl_rope_remap(kv_view(K_pre, "K_pre"), kv_view(V, "V") if V is not None else null_kv, B, Hkv, d,
+                                span(visual_begin, visual_len, seq_len), _cuda(kept, "kept", torch.int32), k,
+                                float(rope_base), kv_view(K_out, "K_out"),
+                                kv_view(V_out, "V_out") if V is not None else null_kv,
+                                w.data_ptr(), w.numel(), _stream(stream)))
+    return K_out, V_out, (seq_len - visual_len + k).to(torch.int32)
 
 
 def pack_kv(K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor, visual_begin: int,

@@ -429,3 +429,51 @@ def test_oracle_thread_count_bitwise(orc):
     b = orc.retrieve(x["q"], x["K"], x["seq_len"], 4, 128, 16, nthreads=4)
     for u, v in zip(a, b):
         assert np.array_equal(u, v)
+
+
+# ---------------------------------------------------------------- f4(i) RoPE remap pins
+def _rope_inputs(B, Hkv, cap, d, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randn(B, Hkv, cap, d, generator=g).to(torch.bfloat16)
+
+
+def test_rope_remap_spec_example_plan(orc):
+    """visual span 10..20, kept {12, 15, 19} -> new {10, 11, 12}, text 21 -> 13."""
+    K = _rope_inputs(1, 1, 40, 8, 0)
+    _, rows = orc.rope_remap(K, [30], 10, 11, [[2, 5, 9]], 10000.0)
+    assert list(rows[0][:13]) == list(range(10)) + [12, 15, 19]
+    assert rows[0][13] == 21                      # the text start moved from 21 to 13
+    assert list(rows[0][13:22]) == list(range(21, 30)) and rows[0][22] == -1
+
+
+def test_rope_remap_matches_complex_rotation(orc):
+    """Rotate-half RoPE == multiplying (x[c] + i x[c + d/2]) by e^{i p base^(-2c/d)}
+    (a different formulation, Python complex arithmetic)."""
+    import cmath
+    d, base = 16, 10000.0
+    K = _rope_inputs(1, 2, 24, d, 1)
+    out, rows = orc.rope_remap(K, [24], 4, 10, [[0, 3, 7, 9]], base)
+    Kd = K.double().numpy()
+    for G in range(2):
+        for w in range(18):
+            old = rows[0][w]
+            for c in range(d // 2):
+                z = complex(Kd[0, G, old, c], Kd[0, G, old, c + d // 2]) * cmath.exp(1j * w * base ** (-2 * c / d))
+                assert abs(out[0, G, w, c] - z.real) < 1e-12 and abs(out[0, G, w, c + d // 2] - z.imag) < 1e-12
+
+
+def test_rope_remap_relative_position_and_norm(orc):
+    """RoPE's defining property: a rotated query-key dot product depends only on the
+    position difference; rotations preserve the norm; position 0 is the identity."""
+    d = 64
+    K = _rope_inputs(1, 1, 40, d, 2)
+    for a, b_ in ((1, 5), (2, 9)):             # put the same (q, k) pair at rows (a, a+1) and (b, b+1)
+        K[0, 0, b_] = K[0, 0, a]
+        K[0, 0, b_ + 1] = K[0, 0, a + 1]
+    out, _ = orc.rope_remap(K, [30], 12, 8, [[1, 4]], 500000.0)
+    x = K.double().numpy()[0, 0]
+    assert np.array_equal(out[0, 0, 0], x[0])                                   # p = 0
+    for w in range(12):
+        assert abs(np.linalg.norm(out[0, 0, w]) - np.linalg.norm(x[w])) < 1e-9 * np.linalg.norm(x[w])
+    assert abs(out[0, 0, 1] @ out[0, 0, 2] - out[0, 0, 5] @ out[0, 0, 6]) < 1e-9
+    assert abs(out[0, 0, 2] @ out[0, 0, 3] - out[0, 0, 9] @ out[0, 0, 10]) < 1e-9
