@@ -30,9 +30,10 @@ __global__ void __launch_bounds__(256) rope_remap_kernel(const RopeParams p) {
         L = min(max(L, p.vb + p.nv), p.capacity);
     }
     const int n_out = p.vb + p.k + (L - p.vb - p.nv);
-    const int64_t total = (int64_t)n_out * half;
+    const int hp = half / 2;  // one thread per (row, two adjacent pairs c, c + 1): 4-byte accesses
+    const int64_t total = (int64_t)n_out * hp;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(e / half), c = (int)(e % half);
+        const int w = (int)(e / hp), c = 2 * (int)(e % hp);
         int old;
         if (w < p.vb) {
             old = w;
@@ -45,24 +46,26 @@ __global__ void __launch_bounds__(256) rope_remap_kernel(const RopeParams p) {
         } else {
             old = w - p.k + p.nv;
         }
-        double sn, cs;
-        sincos((double)w * exp2(-2.0 * (double)c / (double)p.d * p.log2_base), &sn, &cs);
+        double sn0, cs0, sn1, cs1;
+        sincos((double)w * exp2(-2.0 * (double)c / (double)p.d * p.log2_base), &sn0, &cs0);
+        sincos((double)w * exp2(-2.0 * (double)(c + 1) / (double)p.d * p.log2_base), &sn1, &cs1);
         for (int G = 0; G < p.Hkv; ++G) {
-            const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh +
-                                                                             (int64_t)old * p.kst);
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.Ko + (int64_t)b * p.osb + (int64_t)G * p.osh +
-                                                                 (int64_t)w * p.ost);
+            const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(
+                p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh + (int64_t)old * p.kst);
+            __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(p.Ko + (int64_t)b * p.osb + (int64_t)G * p.osh +
+                                                                  (int64_t)w * p.ost);
             // rotation in double too (fp32 loses the small results of x1 cos - x2 sin to
             // cancellation): the output is the bf16 rounding of the exact value
-            const double x1 = (double)__bfloat162float(x[c]), x2 = (double)__bfloat162float(x[c + half]);
-            o[c] = __double2bfloat16(x1 * cs - x2 * sn);
-            o[c + half] = __double2bfloat16(x2 * cs + x1 * sn);
+            const float2 a = __bfloat1622float2(x[c / 2]), z = __bfloat1622float2(x[(c + half) / 2]);
+            const double a0 = a.x, a1 = a.y, z0 = z.x, z1 = z.y;
+            o[c / 2] = __halves2bfloat162(__double2bfloat16(a0 * cs0 - z0 * sn0), __double2bfloat16(a1 * cs1 - z1 * sn1));
+            o[(c + half) / 2] =
+                __halves2bfloat162(__double2bfloat16(z0 * cs0 + a0 * sn0), __double2bfloat16(z1 * cs1 + a1 * sn1));
             if (p.V) {
-                const uint32_t* v = reinterpret_cast<const uint32_t*>(p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh +
-                                                                      (int64_t)old * p.vst);
-                uint32_t* vo = reinterpret_cast<uint32_t*>(p.Vo + (int64_t)b * p.vosb + (int64_t)G * p.vosh +
-                                                           (int64_t)w * p.vost);
-                vo[c] = v[c];  // d/2 words of 2 bf16 = the whole row
+                const uint2* v = reinterpret_cast<const uint2*>(p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh +
+                                                                (int64_t)old * p.vst);
+                uint2* vo = reinterpret_cast<uint2*>(p.Vo + (int64_t)b * p.vosb + (int64_t)G * p.vosh + (int64_t)w * p.vost);
+                vo[c / 2] = v[c / 2];  // d/4 chunks of 8 bytes = the whole row
             }
         }
     }
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(256) rope_remap_kernel(const RopeParams p) {
 }  // namespace
 
 cudaError_t launch_rope_remap(const RopeParams& p, int max_rows, cudaStream_t s) {
-    const int64_t per_b = (int64_t)max_rows * (p.d / 2);
+    const int64_t per_b = (int64_t)max_rows * (p.d / 4);
     const int blocks = (int)std::min<int64_t>((per_b + 255) / 256, 4096);
     rope_remap_kernel<<<dim3(blocks, p.B), 256, 0, s>>>(p);
     return cudaGetLastError();

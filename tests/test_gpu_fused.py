@@ -149,3 +149,27 @@ def test_fresh_step_many_units(svl, orc, B, nv):
                                "seq_lens": None})
     _run(svl, orc, wl, seed=40 + B)
     _run(svl, orc, wl, seed=41 + B)
+
+
+def test_multi_turn_eviction_is_a_seq_len_rollback(svl):
+    """SURVEY.md 8(f) f4(ii) / SPEC.md:306-314 evict_round: evicting a round's question and
+    answer rows (multi-turn) is a seq_len rollback of the after-visual text.
+    Append a round (new K/V rows past seq_len), decode, roll seq_len back: the fresh step is
+    bitwise the pre-round one (the visual cache and everything below seq_len untouched)."""
+    wl = gen.CONFIGS["multi-turn"]
+    x = gen.make_decode_inputs(wl, seed=61, device="cuda")
+    a, ia = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    a, ia = a.clone(), ia.clone()
+    room = wl.capacity - int(x["seq_len"].max())
+    n_round = min(12, room)
+    assert n_round > 0
+    g = torch.Generator(device="cuda").manual_seed(62)
+    for b in range(wl.B):  # the round's rows: written past each batch row's seq_len
+        L = int(x["seq_len"][b])
+        x["K"][b, :, L:L + n_round] = torch.randn(wl.Hkv, n_round, wl.d, generator=g, device="cuda").to(torch.bfloat16)
+        x["V"][b, :, L:L + n_round] = torch.randn(wl.Hkv, n_round, wl.d, generator=g, device="cuda").to(torch.bfloat16)
+    longer = (x["seq_len"] + n_round).to(torch.int32)
+    c, ic = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], longer, wl.vb, wl.nv, wl.k)
+    assert not torch.equal(c, a)  # the round's rows are attended
+    b_, ib = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    assert torch.equal(b_, a) and torch.equal(ib, ia)
