@@ -12,11 +12,14 @@
 // index, ascending output, bitwise reproducible.
 #include <cooperative_groups.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "select_core.cuh"
+#include "select_fast.cuh"
 
 namespace svl {
 
@@ -150,6 +153,140 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
     cluster_sync(cluster);  // no CTA leaves while a peer may still address its shared memory
 }
 
+// ----------------------------------------------------------------------------
+// Retrieve selection with the fused kernel's two-exchange top-k (select_fast.cuh):
+// relevance keys in shared memory, a 256-bin value-adaptive histogram and the
+// threshold bin's candidates all-gathered with st.async, the exact cut resolved
+// locally; massive ties fall back to the generic push radix.  Same result as
+// select_body (ties to the lower index, ascending output).  Rows are read
+// thread-strided (coalesced), keys kept per CTA slice (<= kFsSliceMax).
+constexpr int kFsSliceMax = 8192;
+struct FsLayout {
+    // [FastSelSmem | private histograms] is dead once threshold() has run, so the generic
+    // fallback's scratch aliases it; the fallback's V-slot output (unused here) aliases the
+    // keys, which are dead once its radix passes are done.  ~87 KB: two CTAs per SM.
+    static constexpr int FS_OFF = 0;
+    static constexpr int WHIST_OFF = (int)((sizeof(FastSelSmem) + 15) / 16 * 16);
+    static constexpr int PUSH_OFF = 0;
+    static constexpr int KEYS_OFF = WHIST_OFF + 16 * 256 * 4 > (int)((sizeof(PushTopkSmem) + 15) / 16 * 16)
+                                        ? WHIST_OFF + 16 * 256 * 4
+                                        : (int)((sizeof(PushTopkSmem) + 15) / 16 * 16);
+    static constexpr int STATE_OFF = KEYS_OFF + kFsSliceMax * 4;
+    static constexpr int LSE_OFF = STATE_OFF + kFsSliceMax;
+    static constexpr int BAR_OFF = LSE_OFF + 128 * 4;
+    static constexpr int BYTES = BAR_OFF + 32;
+    static_assert(BYTES <= 113 * 1024, "two CTAs per SM");
+};
+
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int u = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FsLayout::BAR_OFF);
+    if (tid == 0) {
+        mbar_init(smem_u32(&bars[0]), 1);  // histograms: CS x 1 KB
+        mbar_arrive_expect_tx(smem_u32(&bars[0]), (uint32_t)(CS * 1024));
+        mbar_init(smem_u32(&bars[1]), 1);  // candidates (armed in threshold())
+        fence_mbar_init();
+    }
+    cluster_arrive_relaxed();
+    const int n = p.nv, k = p.k;
+    const int64_t out_off = (int64_t)u * k;
+    int b, G0, nG;
+    if (p.shared) {
+        b = u; G0 = 0; nG = p.Hkv;
+    } else {
+        b = u / p.Hkv; G0 = u % p.Hkv; nG = 1;
+    }
+    const int slice = (n + CS - 1) / CS;
+    const int j0 = min(n, rank * slice);
+    const int nloc = min(n, j0 + slice) - j0;
+    float* lse2s = reinterpret_cast<float*>(smem + FsLayout::LSE_OFF);
+    if (MODE == 0) {  // normalisers: lse_in, or the cluster of chunk partials (fixed fold order)
+        const int ncols = p.NC * nG;
+        for (int cc = warp; cc < ncols; cc += NTH / 32) {
+            const int G = G0 + cc / p.NC, col = cc % p.NC;
+            float lse2;
+            if (p.lse_in) {
+                const int r = col / p.g, h = G * p.g + col % p.g;
+                lse2 = p.lse_in[((int64_t)b * p.n_q + r) * p.H + h] * kLog2e;
+            } else {
+                const int uu = b * p.Hkv + G;
+                float m = -INFINITY, l = 0.f;
+                for (int i = lane; i < p.C; i += 32) {
+                    const float2 pr = p.part[((int64_t)uu * p.C + i) * p.NCP + col];
+                    const float M = fmaxf(m, pr.x);
+                    if (M != -INFINITY) {
+                        l = l * exp2f(m - M) + pr.y * exp2f(pr.x - M);
+                        m = M;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+                    const float l2 = __shfl_xor_sync(0xffffffffu, l, off);
+                    const float M = fmaxf(m, m2);
+                    if (M != -INFINITY) {
+                        l = l * exp2f(m - M) + l2 * exp2f(m2 - M);
+                        m = M;
+                    }
+                }
+                lse2 = m + log2f(l);
+            }
+            if (lane == 0) lse2s[cc] = lse2;
+        }
+    }
+    FastSelect<NTH> sel(cl, *reinterpret_cast<FastSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0, slice, n, k,
+                        reinterpret_cast<uint32_t*>(smem + FsLayout::KEYS_OFF), smem + FsLayout::STATE_OFF, p.flags,
+                        reinterpret_cast<uint32_t*>(smem + FsLayout::WHIST_OFF));
+    sel.hbar = &bars[0];
+    sel.cbar = &bars[1];
+    int stage = 0;
+    if (!sel.trivial()) {
+        sel.zero_hist();
+        cta_sync();
+        for (int i = tid; i < nloc; i += NTH) {
+            const int j = j0 + i;
+            float sc = 0.f;
+            if (MODE == 0) {
+                for (int G = 0; G < nG; ++G) {
+                    const float4* lr = reinterpret_cast<const float4*>(
+                        p.logits + (((int64_t)(b * p.Hkv + G0 + G)) * p.nv + j) * (NT * 8));
+                    float4 v[2 * NT];
+#pragma unroll
+                    for (int q = 0; q < 2 * NT; ++q) v[q] = lr[q];
+                    const float* lv = reinterpret_cast<const float*>(v);
+#pragma unroll
+                    for (int col = 0; col < NT * 8; ++col)
+                        if (col < p.NC) sc += exp2f(lv[col] - lse2s[G * p.NC + col]);
+                }
+            } else {
+                for (int G = 0; G < nG; ++G) sc += p.scores_in[((int64_t)(b * p.Hkv + G0 + G)) * p.nv + j];
+            }
+            if (p.scores_out) p.scores_out[(int64_t)u * n + j] = sc;
+            sel.add_key(i, sc);
+        }
+        cluster_wait();  // every peer has started and armed its barriers
+        stage = sel.threshold();
+    } else {
+        cluster_wait();
+    }
+    int32_t* idx_out = p.idx_out + out_off;
+    if (stage == 1) {
+        sel.assign_slots_and_push_candidates(nullptr);
+        sel.resolve_and_emit(idx_out);
+    } else {
+        // (every CTA takes the same stage) the generic scratch aliases FastSelSmem, which a
+        // slower peer may still be reading in threshold(): meet before anyone pushes into it
+        if (stage == 2) cluster_sync(cl);
+        sel.generic_or_trivial(stage, *reinterpret_cast<PushTopkSmem*>(smem + FsLayout::PUSH_OFF), idx_out,
+                               reinterpret_cast<int*>(smem + FsLayout::KEYS_OFF));
+    }
+    cluster_sync(cl);  // no CTA leaves while a peer may still address its shared memory
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NTH, 1) select_retrieve_kernel(const SelectParams p) {
     select_body<0, NT>(p, nullptr);
@@ -267,13 +404,48 @@ static cudaError_t launch_cluster(Kern kern, int CS, int n_units, cudaStream_t s
 }
 
 static bool* attr_flag(int which) {
-    static bool done[8][64] = {};
+    static bool done[16][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     return &done[which][dev & 63];
 }
 
+template <typename Kern>
+static cudaError_t launch_fast(Kern kern, const SelectParams& p, int n_units, cudaStream_t s, bool& attr_done) {
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FsLayout::BYTES);
+        if (e == cudaSuccess) e = set_max_carveout(kern);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.CS, n_units, 1);
+    cfg.blockDim = dim3(NTH, 1, 1);
+    cfg.dynamicSmemBytes = FsLayout::BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
+    const bool fast = !getenv("SVL_OLD_SELECT") && (p.nv + p.CS - 1) / p.CS <= kFsSliceMax;
+    if (fast) {
+        if (p.mode == 2) return launch_fast(select_fast_kernel<2, 1>, p, n_units, s, *attr_flag(6));
+        switch (p.NCP / 8) {
+            case 1: return launch_fast(select_fast_kernel<0, 1>, p, n_units, s, *attr_flag(7));
+            case 2: return launch_fast(select_fast_kernel<0, 2>, p, n_units, s, *attr_flag(8));
+            case 3: return launch_fast(select_fast_kernel<0, 3>, p, n_units, s, *attr_flag(9));
+            case 4: return launch_fast(select_fast_kernel<0, 4>, p, n_units, s, *attr_flag(10));
+        }
+        return cudaErrorInvalidValue;
+    }
     if (p.mode == 2) return launch_cluster(select_scores_kernel, p.CS, n_units, s, *attr_flag(5), p);
     switch (p.NCP / 8) {
         case 1: return launch_cluster(select_retrieve_kernel<1>, p.CS, n_units, s, *attr_flag(1), p);

@@ -221,7 +221,7 @@ struct FastSelect {
             const uint32_t key = keys[i];
             const int d = rel_digit(key);
             uint8_t st = 0;
-            if (d >= bstar) att_sel[pge++] = i;
+            if (d >= bstar && att_sel) att_sel[pge++] = i;  // (null: the caller needs no V slots)
             if (d == bstar) {
                 st = (uint8_t)(peq + 1);
                 const uint2 c = make_uint2(key, (uint32_t)(v0 + i));

@@ -82,7 +82,7 @@ __device__ __noinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* warp_sums
 
 // One warp, 256 bins ascending in shared memory: the bin holding the
 // `need`-th largest element (scanning from the top) and the count above it.
-__device__ __noinline__ void warp_find256(const uint32_t* bins, uint32_t need, uint32_t* out) {
+static __device__ __noinline__ void warp_find256(const uint32_t* bins, uint32_t need, uint32_t* out) {
     const int lane = threadIdx.x & 31;
     uint32_t c[8];
     uint32_t grp = 0u;
