@@ -579,6 +579,28 @@ def main():
                 "bound": "exp2 (SFU + FP32-pipe polynomial) at d = 128: one exponential per 256 flop",
                 "bf16_peak_tflops": bf16_peak_q, "runs": runs}
 
+    # ---- throughput sweep (BASELINE configs[4]: B = 16, 64k visual, k = 10 %): the fresh
+    # step at 64k per unit runs the two-call path (score -> select -> decode); 3 rotating
+    # layers of 1.3 GB each (> L2), single GPU
+    sweep = None
+    if rank == 0 and world == 1 and not args.profile:
+        sw = gen.CONFIGS["sweep"]
+        sxs = [gen.make_decode_inputs(sw, seed=900 + i, device=dev) for i in range(3)]
+        ws_s = svl.Workspace(dev)
+        ws_s.get(svl.fresh_decode_workspace_size(sw.B, sw.H, sw.Hkv, sw.d, sw.k, sw.nv, sw.capacity))
+        sidx = torch.empty(sw.B, sw.Hkv, sw.k, dtype=torch.int32, device=dev)
+        sout = torch.empty(sw.B, sw.H, sw.d, device=dev)
+        g_sweep = graph_of(lambda: [svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], sw.vb, sw.nv,
+                                                          sw.k, idx_out=sidx, out=sout, ws=ws_s) for x in sxs])
+        ms_sw = timed(g_sweep, 20, 3) / len(sxs)
+        sw_bytes = step_bytes(sw)["total"]
+        sweep = {"config": "throughput sweep: B 16, 65536 visual, k 6554, 28/4 heads, d 128 (BASELINE configs[4])",
+                 "us_per_layer": ms_sw * 1e3, "GB_s": sw_bytes / (ms_sw * 1e-3) / 1e9,
+                 "hbm_frac_of_measured": sw_bytes / (ms_sw * 1e-3) / 1e9 / peaks()[0],
+                 "bytes_per_layer": sw_bytes,
+                 "path": "svl_fresh_decode_step -> two calls at 64k per unit (score, select, decode kernels)"}
+        del sxs
+
     # ---- steady step (decode only, indices reused) and the per-round amortised step
     steady_us = ms_decode * 1e3 / LAYERS
     steady_bytes = nbytes["decode"]
@@ -640,6 +662,7 @@ def main():
                          "algorithmic_bytes_per_launch": nbytes["fused"]},
             "prefill": prefill,
             "question_retrieve": qret,
+            "throughput_sweep": sweep,
             "cpu_baseline": cpu,
             "e2e": {"value": nbytes["total"] * LAYERS * world / (e2e_ms * 1e-3) / 1e9,
                     "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
