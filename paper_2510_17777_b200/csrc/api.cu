@@ -121,10 +121,17 @@ static RetrieveTcLayout retrieve_tc_layout(int B, int n_q, int H, int Hkv, int d
 
 // --------------------------------------------------------------- decode plan
 static int plan_splits(int units, int n_att_max, int sms) {
-    // CTAs per unit = cluster size: the largest power of two <= 16 that keeps the
-    // grid within ~2 waves, and at least one 16-row tile per CTA
+    // CTAs per unit = cluster size: the largest power of two <= 16 that keeps the grid
+    // within ONE wave (one 159 KB CTA per SM) and at least one 16-row tile per CTA.
+    // Measured: the gather is per-SM bound, so a second partial wave costs more than
+    // the longer per-CTA row lists (multi-turn B = 8: 16.1 us at 4 splits vs 26.8 at 8;
+    // sweep B = 16: 92 us at 2 vs 98 at 4, 134 at 8)
     int S = 16;
-    while (S > 1 && (units * S > 2 * sms || S * 16 > n_att_max)) S >>= 1;
+    while (S > 1 && (units * S > sms || S * 16 > n_att_max)) S >>= 1;
+    if (const char* e = getenv("SVL_DECODE_S")) {  // experiment knob
+        const int v = atoi(e);
+        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) S = v;
+    }
     return S;
 }
 

@@ -22,7 +22,10 @@ def svl():
 
 
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
-def test_push_gather_equals_unsharded(svl, P):
+def test_push_gather_equals_unsharded(svl, P, monkeypatch):
+    # per-unit split count pinned: the planner sizes the splits by the
+    # number of units, which differs between a shard and the whole batch
+    monkeypatch.setenv("SVL_DECODE_S", "8")
     wl = gen.DecodeWorkload("push", 4, 28, 4, 128, 32, 8192, 300, 819, 1, 256)
     x = gen.make_decode_inputs(wl, seed=41, device="cuda")
     idx = svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k).clone()
