@@ -607,7 +607,7 @@ svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void
 // ----------------------------------------------------- fused fresh step
 // Cluster size and eligibility of the fused kernel for a shape.
 
-static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice) {
+static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice, int d) {
     if (g > 16) return false;
     const int smax = kFusedSliceMax / ((g + 7) / 8);
     int cmin = (nv + smax - 1) / smax;
@@ -618,9 +618,21 @@ static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int
     // many SMs per unit while the units are few (HBM streaming is per-SM bound)
     const int want = (units * 16 <= 2 * device_sm_count()) ? 16 : 8;
     CS = std::max(c, want);
+    bool pinned = false;
     if (const char* pin = getenv("SVL_FRESH_CS")) {  // test knob: pin the split count (8 or 16)
         const int v = atoi(pin);
-        if ((v == 8 || v == 16) && v >= c) CS = v;
+        if ((v == 8 || v == 16) && v >= c) CS = v, pinned = true;
+    }
+    if (const char* f = getenv("SVL_FUSED")) {  // experiment knob: 0 = always the two-call path
+        if (atoi(f) == 0) return false;
+    }
+    // The fused kernel only while every unit's cluster is co-resident (one wave).  Beyond
+    // that the two-call kernels, which spread over every SM, are faster (measured, us/layer
+    // fused vs two-call: 32k B=2 56.8 vs 50.7, 16k B=4 67.2 vs 52.4, 4k B=8 55.9 vs 38.9;
+    // B=1: 32k 28.1 vs 34.2, 4k 17.3 vs 23.6)
+    if (!pinned) {
+        const int mac = fresh_max_active_clusters(d, g, CS);
+        if (mac <= 0 || units > mac) return false;
     }
     slice = (nv + CS - 1) / CS;
     if (slice > smax) return false;
@@ -633,7 +645,7 @@ size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_
                                        int32_t visual_len, int32_t capacity, uint32_t flags) {
     if (B < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
     int CS, slice;
-    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice))
+    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice, d))
         return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
     return std::max(svl_retrieve_workspace_size(B, 1, H, Hkv, d, visual_len, flags),
                     svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags));
@@ -672,7 +684,7 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
 
     int CS, slice;
     FreshParams p;
-    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice) ||
+    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice, d) ||
         !encode_kv_tensor_map(&p.ktmap, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 128)) {
         // outside the on-chip budget: the two separate calls (same q as [B][1][H][d])
         st = svl_retrieve(q, B, 1, H, Hkv, d, K, span, nullptr, k, scale, flags, idx_out, nullptr,

@@ -883,7 +883,48 @@ cudaError_t launch_fresh_t(const FreshParams& p, int CS, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, fresh_kernel<D, NT>, p);
 }
 
+template <int D, int NT>
+int max_active_clusters_t(int CS) {
+    using GM = FGeom<D, NT>;
+    if (cudaFuncSetAttribute(fresh_kernel<D, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(fresh_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM::BYTES) != cudaSuccess)
+        return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS, 1, 1);
+    cfg.blockDim = dim3(FT, 1, 1);
+    cfg.dynamicSmemBytes = GM::BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fresh_kernel<D, NT>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 }  // namespace
+
+// Co-resident clusters of the fused kernel at cluster size CS (cached per device; <= 0: unknown).
+int fresh_max_active_clusters(int d, int g, int CS) {
+    static int cache[8][2][2][17] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    const int NT = (g + 7) / 8;
+    if (CS < 1 || CS > 16 || NT < 1 || NT > 2) return 0;
+    int& c = cache[dev & 7][d == 128][NT - 1][CS];
+    if (c == 0) {
+        if (d == 128) c = NT == 1 ? max_active_clusters_t<128, 1>(CS) : max_active_clusters_t<128, 2>(CS);
+        else c = NT == 1 ? max_active_clusters_t<64, 1>(CS) : max_active_clusters_t<64, 2>(CS);
+        if (c == 0) c = -1;
+    }
+    return c;
+}
 
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s) {
     const int NT = (p.g + 7) / 8;

@@ -105,6 +105,7 @@ constexpr int kFusedTextMax = 128;    // text rows per CTA
 #endif
 constexpr int kFusedSliceMax = SVL_SLICE_MAX;  // visual rows per CTA (halved for g > 8)
 cudaError_t launch_fresh(const FreshParams& p, int d, int CS, cudaStream_t s);
+int fresh_max_active_clusters(int d, int g, int CS);  // <= 0: unknown
 
 struct SalienceParams {
     CUtensorMap qmap, kmap;  // tcgen05 path: Qe / Ke as 4-D {d_e, S+N_f, H_e, F}, box {64, 128}

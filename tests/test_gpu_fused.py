@@ -139,11 +139,14 @@ def test_fresh_step_deterministic(svl):
     assert torch.equal(a, b) and torch.equal(ia, ib)
 
 
+@pytest.mark.parametrize("pin", [None, "16"])
 @pytest.mark.parametrize("B,nv", [(2, 32768), (8, 32768), (8, 24576)])
-def test_fresh_step_many_units(svl, orc, B, nv):
+def test_fresh_step_many_units(svl, orc, B, nv, pin, monkeypatch):
     """More clusters than fit at once (later clusters start on SMs vacated by earlier
     ones): this exposed the text-row / ring-slot parity race fixed in fused.cu (the
     text rows now have their own buffer and barrier); run twice back to back."""
+    if pin:  # force the fused kernel into a multi-wave launch (the planner would take two calls)
+        monkeypatch.setenv("SVL_FRESH_CS", pin)
     base = gen.CONFIGS["long-video"]
     wl = gen.DecodeWorkload(**{**base.__dict__, "name": f"mu{B}", "B": B, "nv": nv, "k": nv // 10,
                                "seq_lens": None})
