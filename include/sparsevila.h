@@ -254,8 +254,8 @@ svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void
  * svl_sparse_decode_attn with the SAME query, fused: the decode step that
  * re-retrieves its visual tokens.  Because the retrieval
  * logits s = scale*q.K_j are exactly the decode logits, K is read from HBM
- * once: one thread-block cluster per (b, KV group) streams K with TMA bulk
- * copies, keeps the logits on chip, selects the top-k over DSMEM and attends
+ * once: one thread-block cluster per (b, KV group) streams K with tiled TMA into
+ * tcgen05 (logits in TMEM), selects the top-k over DSMEM and attends
  * over [text rows] U [kept visual rows] (see fused.cu).  Results equal
  * svl_retrieve + svl_sparse_decode_attn up to fp32 rounding of the LSE.
  *
@@ -265,8 +265,12 @@ svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void
  *          later svl_sparse_decode_attn steady steps).
  * out      device fp32 [B][H][d]; lse_out device fp32 [B][H] or NULL.
  * Shapes outside the fused kernel's on-chip budget (visual_len > 32768 with
- * g <= 8, > 16384 with 8 < g <= 16, or more than 4096 text rows) run the two
- * separate calls instead (same kernels as svl_retrieve / svl_sparse_decode_attn).
+ * g <= 8, > 16384 with 8 < g <= 16, or more than 4096 text rows), and batches
+ * with more (b, KV group) units than co-resident clusters (the fused kernel
+ * uses one 8- or 16-CTA cluster per unit; past one wave the two calls, which
+ * spread over every SM, are faster), run the two separate calls instead (same
+ * kernels as svl_retrieve / svl_sparse_decode_attn).  The workspace must be
+ * sized by svl_fresh_decode_workspace_size, which covers either path.
  */
 svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
                                  svl_kv K, svl_kv V, svl_span span, int32_t k, float scale,
