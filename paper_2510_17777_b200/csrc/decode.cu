@@ -36,6 +36,10 @@ namespace {
 
 constexpr int NTH = kDecodeThreads;  // 256: 8 warps, one 16-row tile each per batch
 constexpr int RB = kDecodeRowsMax;   // 128 rows per batch
+#ifndef SVL_DECODE_NBUF
+#define SVL_DECODE_NBUF 2  // measured: 3 buffers (220 KB) gave no gain (9.5 vs 9.4 us long-video, 92.4 vs 92.9 sweep)
+#endif
+constexpr int NBUF = SVL_DECODE_NBUF;  // gather buffers (NBUF - 1 batches in flight)
 constexpr int NW = NTH / 32;
 
 template <int D>
@@ -43,8 +47,8 @@ struct DecodeSmem {
     static constexpr int CH = D / 8;  // 16-byte chunks per row
     static constexpr int ROW_BYTES = D * 2;
     static constexpr int BUF_BYTES = 2 * RB * ROW_BYTES;  // K + V of one batch
-    static constexpr int ROWS_OFF = 2 * BUF_BYTES;        // two buffers
-    static constexpr int SL_OFF = ROWS_OFF + 2 * RB * 4;  // tile max / sum [2][128] fp32
+    static constexpr int ROWS_OFF = NBUF * BUF_BYTES;     // NBUF gather buffers
+    static constexpr int SL_OFF = ROWS_OFF + NBUF * RB * 4;  // tile max / sum [2][128] fp32
     static constexpr int PT_OFF = SL_OFF + RB * 16 * 4;   // P hi + lo [RB][16] bf16
     static constexpr int RUN_OFF = PT_OFF + 2 * RB * 16 * 2;  // running M, l, al [3][16]
     static constexpr int RCV_OFF = RUN_OFF + 64 * 4;      // [CS][per] pushed o (CS * per <= 16 D + 16)
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     cg::cluster_group cl = cg::this_cluster();
     const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-    int* rows_s = reinterpret_cast<int*>(smem + SM::ROWS_OFF);  // [2][RB]
+    int* rows_s = reinterpret_cast<int*>(smem + SM::ROWS_OFF);  // [NBUF][RB]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gid = lane >> 2, t = lane & 3;
@@ -111,9 +115,9 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
     const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
     const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
 
-    // batch j: row ids into rows_s[j & 1], then the K/V gather (one commit group)
+    // batch j: row ids into rows_s[j % NBUF], then the K/V gather (one commit group)
     auto load_batch = [&](int j) {
-        int* rows = rows_s + (j & 1) * RB;
+        int* rows = rows_s + (j % NBUF) * RB;
         const int a = w0 + j * RB, n = min(RB, w1 - a);
         bool bad = false;
         for (int i = tid; i < RB; i += NTH) {
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
         }
         if (bad) raise_flag(p.flags, 1u /*SVL_DEVFLAG_INDEX*/);
         cta_sync();
-        const uint32_t sK = smem_u32(smem + (j & 1) * SM::BUF_BYTES);
+        const uint32_t sK = smem_u32(smem + (j % NBUF) * SM::BUF_BYTES);
         const uint32_t sV = sK + RB * SM::ROW_BYTES;
         const int nr = (n + 15) & ~15;
         for (int i = tid; i < nr * CH; i += NTH) {
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
         cp_async_commit();
     };
 
-    if (nb > 0) load_batch(0);
+    for (int j = 0; j < min(nb, NBUF - 1); ++j) load_batch(j);  // NBUF - 1 batches in flight
 
     // q A-fragments (heads gid, gid+8 of the group; zero beyond g)
     uint4 qa[NCH], qb[NCH];
@@ -187,17 +191,19 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const DecodeParams p) {
     static_assert(D / 16 <= NW, "one warp per 16 output columns");
 
     for (int j = 0; j < nb; ++j) {
-        if (j + 1 < nb) {
-            cta_sync();  // buffer (j+1)&1 = (j-1)&1 is no longer read
-            load_batch(j + 1);
-            cp_async_wait<1>();
+        if (j + NBUF - 1 < nb) {
+            cta_sync();  // buffer (j + NBUF - 1) % NBUF = (j - 1) % NBUF is no longer read
+            load_batch(j + NBUF - 1);
+            cp_async_wait<NBUF - 1>();
+        } else if (NBUF > 2 && j + 1 < nb) {
+            cp_async_wait<1>();  // batches j and j + 1 outstanding (no more issued)
         } else {
             cp_async_wait<0>();
         }
         cta_sync();
         stamp(1 + j);
-        const int* rows = rows_s + (j & 1) * RB;
-        const uint32_t sK = smem_u32(smem + (j & 1) * SM::BUF_BYTES);
+        const int* rows = rows_s + (j % NBUF) * RB;
+        const uint32_t sK = smem_u32(smem + (j % NBUF) * SM::BUF_BYTES);
         const uint32_t sV = sK + RB * SM::ROW_BYTES;
         const int n = min(RB, w1 - (w0 + j * RB));
         const int nr = (n + 15) & ~15;
