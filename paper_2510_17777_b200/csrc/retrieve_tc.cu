@@ -80,9 +80,14 @@ __global__ void qpack_kernel(const RetrTcParams p, int D) {
     }
 }
 
+// One warp per query row: lanes fold a lane-strided share of the row's chunk
+// partials, then a fixed butterfly -- deterministic, and the row's partials are
+// read coalesced.
 __global__ void lse_combine_kernel(const RetrTcParams p) {
+    const int lane = threadIdx.x & 31;
     const int64_t total = (int64_t)p.B * p.Hkv * p.NQP;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); e < total; e += nwarps) {
         const int n = (int)(e % p.NQP);
         const int u = (int)(e / p.NQP);
         const int b = u / p.Hkv, G = u % p.Hkv;
@@ -94,7 +99,7 @@ __global__ void lse_combine_kernel(const RetrTcParams p) {
             } else {
                 float m = -INFINITY, l = 0.f;
                 const float2* pp = p.part + e * p.npart;
-                for (int i = 0; i < p.npart; ++i) {  // fixed order: deterministic
+                for (int i = lane; i < p.npart; i += 32) {
                     const float2 x = pp[i];
                     const float M = fmaxf(m, x.x);
                     if (M != -INFINITY) {
@@ -102,11 +107,21 @@ __global__ void lse_combine_kernel(const RetrTcParams p) {
                         m = M;
                     }
                 }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+                    const float l2 = __shfl_xor_sync(0xffffffffu, l, off);
+                    const float M = fmaxf(m, m2);
+                    if (M != -INFINITY) {
+                        l = l * exp2f(m - M) + l2 * exp2f(m2 - M);
+                        m = M;
+                    }
+                }
                 out = m + log2f(l);
             }
-            if (out != out) raise_flag(p.flags, 2u /*NONFINITE*/);
+            if (lane == 0 && out != out) raise_flag(p.flags, 2u /*NONFINITE*/);
         }
-        p.lse2[e] = out;
+        if (lane == 0) p.lse2[e] = out;
     }
 }
 
@@ -517,7 +532,7 @@ cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     const int64_t rows = (int64_t)units * p.NQP;
-    lse_combine_kernel<<<(int)std::min<int64_t>((rows + 255) / 256, 8L * sms), 256, 0, s>>>(p);
+    lse_combine_kernel<<<(int)std::min<int64_t>((rows + 7) / 8, 8L * sms), 256, 0, s>>>(p);  // 8 rows / block
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     RetrTcParams p1 = p;
