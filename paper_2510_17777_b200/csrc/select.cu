@@ -160,15 +160,13 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
 // locally; massive ties fall back to the generic push radix.  Same result as
 // select_body (ties to the lower index, ascending output).  Rows are read
 // thread-strided (coalesced), keys kept per CTA slice (<= kFsSliceMax).
-constexpr int kFsSliceMax = 4096;
-constexpr int kFsCands = 256;  // threshold-bin candidates per CTA (4096 keys per CTA: the fused kernel's 64 overflow)
-using FsSelSmem = FastSelSmemT<kFsCands>;
+constexpr int kFsSliceMax = 8192;
 struct FsLayout {
     // [FastSelSmem | private histograms] is dead once threshold() has run, so the generic
     // fallback's scratch aliases it; the fallback's V-slot output (unused here) aliases the
-    // keys, which are dead once its radix passes are done.  two CTAs per SM.
+    // keys, which are dead once its radix passes are done.  ~87 KB: two CTAs per SM.
     static constexpr int FS_OFF = 0;
-    static constexpr int WHIST_OFF = (int)((sizeof(FsSelSmem) + 15) / 16 * 16);
+    static constexpr int WHIST_OFF = (int)((sizeof(FastSelSmem) + 15) / 16 * 16);
     static constexpr int PUSH_OFF = 0;
     static constexpr int KEYS_OFF = WHIST_OFF + 16 * 256 * 4 > (int)((sizeof(PushTopkSmem) + 15) / 16 * 16)
                                         ? WHIST_OFF + 16 * 256 * 4
@@ -240,7 +238,7 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
             if (lane == 0) lse2s[cc] = lse2;
         }
     }
-    FastSelect<NTH, kFsCands> sel(cl, *reinterpret_cast<FsSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0, slice, n, k,
+    FastSelect<NTH> sel(cl, *reinterpret_cast<FastSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0, slice, n, k,
                         reinterpret_cast<uint32_t*>(smem + FsLayout::KEYS_OFF), smem + FsLayout::STATE_OFF, p.flags,
                         reinterpret_cast<uint32_t*>(smem + FsLayout::WHIST_OFF));
     sel.hbar = &bars[0];
@@ -283,9 +281,6 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
         // (every CTA takes the same stage) the generic scratch aliases FastSelSmem, which a
         // slower peer may still be reading in threshold(): meet before anyone pushes into it
         if (stage == 2) cluster_sync(cl);
-#if SVL_EXP_FLAG_STAGE2
-        if (stage == 2 && tid == 0 && rank == 0) raise_flag(p.flags, 0x100u);
-#endif
         sel.generic_or_trivial(stage, *reinterpret_cast<PushTopkSmem*>(smem + FsLayout::PUSH_OFF), idx_out,
                                reinterpret_cast<int*>(smem + FsLayout::KEYS_OFF));
     }
