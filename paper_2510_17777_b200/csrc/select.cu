@@ -160,13 +160,18 @@ SVL_DEV void select_body(const SelectParams& p, const PruneTable* tabp) {
 // locally; massive ties fall back to the generic push radix.  Same result as
 // select_body (ties to the lower index, ascending output).  Rows are read
 // thread-strided (coalesced), keys kept per CTA slice (<= kFsSliceMax).
-constexpr int kFsSliceMax = 8192;
+// threshold-bin candidates per CTA: 64 as in the fused kernel for relevance keys (mode 0),
+// 256 for question-chunk scores (mode 2: sums over n_q * g rows concentrate near the cut
+// and overflow 64 -> the generic radix); the slice bound keeps two CTAs per SM
+template <int CANDS>
 struct FsLayout {
+    static constexpr int kFsSliceMax = CANDS > 64 ? 4096 : 8192;
+    using FsSelSmem = FastSelSmemT<CANDS>;
     // [FastSelSmem | private histograms] is dead once threshold() has run, so the generic
     // fallback's scratch aliases it; the fallback's V-slot output (unused here) aliases the
-    // keys, which are dead once its radix passes are done.  ~87 KB: two CTAs per SM.
+    // keys, which are dead once its radix passes are done.  two CTAs per SM.
     static constexpr int FS_OFF = 0;
-    static constexpr int WHIST_OFF = (int)((sizeof(FastSelSmem) + 15) / 16 * 16);
+    static constexpr int WHIST_OFF = (int)((sizeof(FsSelSmem) + 15) / 16 * 16);
     static constexpr int PUSH_OFF = 0;
     static constexpr int KEYS_OFF = WHIST_OFF + 16 * 256 * 4 > (int)((sizeof(PushTopkSmem) + 15) / 16 * 16)
                                         ? WHIST_OFF + 16 * 256 * 4
@@ -178,8 +183,9 @@ struct FsLayout {
     static_assert(BYTES <= 113 * 1024, "two CTAs per SM");
 };
 
-template <int MODE, int NT>
+template <int MODE, int NT, int CANDS>
 __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams p) {
+    using FsLayout = svl::FsLayout<CANDS>;
     extern __shared__ __align__(16) uint8_t smem[];
     cg::cluster_group cl = cg::this_cluster();
     const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
@@ -238,7 +244,8 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
             if (lane == 0) lse2s[cc] = lse2;
         }
     }
-    FastSelect<NTH> sel(cl, *reinterpret_cast<FastSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0, slice, n, k,
+    FastSelect<NTH, CANDS> sel(cl, *reinterpret_cast<typename FsLayout::FsSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0,
+                               slice, n, k,
                         reinterpret_cast<uint32_t*>(smem + FsLayout::KEYS_OFF), smem + FsLayout::STATE_OFF, p.flags,
                         reinterpret_cast<uint32_t*>(smem + FsLayout::WHIST_OFF));
     sel.hbar = &bars[0];
@@ -281,6 +288,9 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
         // (every CTA takes the same stage) the generic scratch aliases FastSelSmem, which a
         // slower peer may still be reading in threshold(): meet before anyone pushes into it
         if (stage == 2) cluster_sync(cl);
+#if SVL_EXP_FLAG_STAGE2
+        if (stage == 2 && tid == 0 && rank == 0) raise_flag(p.flags, 0x100u);
+#endif
         sel.generic_or_trivial(stage, *reinterpret_cast<PushTopkSmem*>(smem + FsLayout::PUSH_OFF), idx_out,
                                reinterpret_cast<int*>(smem + FsLayout::KEYS_OFF));
     }
@@ -410,8 +420,9 @@ static bool* attr_flag(int which) {
     return &done[which][dev & 63];
 }
 
-template <typename Kern>
+template <int CANDS, typename Kern>
 static cudaError_t launch_fast(Kern kern, const SelectParams& p, int n_units, cudaStream_t s, bool& attr_done) {
+    using FsLayout = svl::FsLayout<CANDS>;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FsLayout::BYTES);
@@ -435,14 +446,16 @@ static cudaError_t launch_fast(Kern kern, const SelectParams& p, int n_units, cu
 }
 
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
-    const bool fast = !getenv("SVL_OLD_SELECT") && (p.nv + p.CS - 1) / p.CS <= kFsSliceMax;
-    if (fast) {
-        if (p.mode == 2) return launch_fast(select_fast_kernel<2, 1>, p, n_units, s, *attr_flag(6));
+    const int slice = (p.nv + p.CS - 1) / p.CS;
+    const bool fast = !getenv("SVL_OLD_SELECT");
+    if (fast && p.mode == 2 && slice <= FsLayout<256>::kFsSliceMax)
+        return launch_fast<256>(select_fast_kernel<2, 1, 256>, p, n_units, s, *attr_flag(6));
+    if (fast && p.mode == 0 && slice <= FsLayout<64>::kFsSliceMax) {
         switch (p.NCP / 8) {
-            case 1: return launch_fast(select_fast_kernel<0, 1>, p, n_units, s, *attr_flag(7));
-            case 2: return launch_fast(select_fast_kernel<0, 2>, p, n_units, s, *attr_flag(8));
-            case 3: return launch_fast(select_fast_kernel<0, 3>, p, n_units, s, *attr_flag(9));
-            case 4: return launch_fast(select_fast_kernel<0, 4>, p, n_units, s, *attr_flag(10));
+            case 1: return launch_fast<64>(select_fast_kernel<0, 1, 64>, p, n_units, s, *attr_flag(7));
+            case 2: return launch_fast<64>(select_fast_kernel<0, 2, 64>, p, n_units, s, *attr_flag(8));
+            case 3: return launch_fast<64>(select_fast_kernel<0, 3, 64>, p, n_units, s, *attr_flag(9));
+            case 4: return launch_fast<64>(select_fast_kernel<0, 4, 64>, p, n_units, s, *attr_flag(10));
         }
         return cudaErrorInvalidValue;
     }

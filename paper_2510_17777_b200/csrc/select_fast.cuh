@@ -31,18 +31,20 @@ namespace svl {
 constexpr int kFastCandPerCta = 64;
 constexpr int kFastSub = 256;  // sub-bin members ranked by a short list
 
-struct FastSelSmem {
+template <int CANDS>
+struct FastSelSmemT {
     uint32_t allhist[16][256];
-    uint2 cand[16][kFastCandPerCta];
+    uint2 cand[16][CANDS];
     uint32_t hist[256];
     uint32_t tot[256];
     uint32_t cnt_q[16], above_q[16], sel_q[16];
-    uint32_t sel2[16][kFastCandPerCta / 32];  // ballot masks of the kept candidates
+    uint32_t sel2[16][CANDS / 32];  // ballot masks of the kept candidates
     uint2 sub[kFastSub];
     uint32_t warp_sums[32];
     uint32_t bcast[16];
-    uint8_t cflag[16][kFastCandPerCta];
+    uint8_t cflag[16][CANDS];
 };
+using FastSelSmem = FastSelSmemT<kFastCandPerCta>;
 
 SVL_DEV int rel_digit(uint32_t key) {  // == push_digit(key, 0, .)
     const int e = (int)((key >> 23) & 0xffu);
@@ -86,10 +88,11 @@ __device__ __noinline__ void warp_find_nb(const uint32_t* bins, uint32_t need, u
     }
 }
 
-template <int NTH>
+// CANDS: candidates of the threshold bin a CTA may hold (more -> the generic radix)
+template <int NTH, int CANDS = kFastCandPerCta>
 struct FastSelect {
     cg::cluster_group& cl;
-    FastSelSmem& s;
+    FastSelSmemT<CANDS>& s;
     int nvis, v0, slice, nv, k;
     uint32_t* keys;
     uint8_t* state;
@@ -105,7 +108,7 @@ struct FastSelect {
     uint64_t* hbar = nullptr;
     uint64_t* cbar = nullptr;
 
-    SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmem& s_, int nvis_, int v0_, int slice_, int nv_, int k_,
+    SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmemT<CANDS>& s_, int nvis_, int v0_, int slice_, int nv_, int k_,
                        uint32_t* keys_, uint8_t* state_, uint32_t* flags_, uint32_t* whist_)
         : cl(cl_), s(s_), nvis(nvis_), v0(v0_), slice(slice_), nv(nv_), k(k_), keys(keys_), state(state_),
           flags(flags_), whist(whist_) {}
@@ -195,7 +198,7 @@ struct FastSelect {
             maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
             totc += (q < CS) ? s.cnt_q[q] : 0u;
         }
-        const int st = (bstar == 0 || maxc > (uint32_t)kFastCandPerCta) ? 2 : 1;
+        const int st = (bstar == 0 || maxc > (uint32_t)CANDS) ? 2 : 1;
         if (st == 1 && tid == 0) mbar_arrive_expect_tx(smem_u32(cbar), totc * 8u);  // the candidates to come
         return st;
     }
@@ -223,10 +226,10 @@ struct FastSelect {
             uint8_t st = 0;
             if (d >= bstar && att_sel) att_sel[pge++] = i;  // (null: the caller needs no V slots)
             if (d == bstar) {
-                st = (uint8_t)(peq + 1);
+                st = (uint8_t)(CANDS > 254 ? min(peq + 1u, 255u) : peq + 1u);  // candidate marker
                 const uint2 c = make_uint2(key, (uint32_t)(v0 + i));
                 const uint32_t dst = smem_u32(&s.cand[rank][peq]), bar = smem_u32(cbar);
-                if (peq < (uint32_t)kFastCandPerCta)  // always true on this path (threshold() checked); defensive
+                if (peq < (uint32_t)CANDS)  // always true on this path (threshold() checked); defensive
                     for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), c, mapa_shared(bar, q));
                 ++peq;
             }
@@ -244,8 +247,8 @@ struct FastSelect {
         for (int i = tid; i < 256; i += NTH) s.hist[i] = 0u;
         if (tid == 0) s.bcast[6] = 0u;
         cta_sync();
-        for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
-            const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
+        for (int sl = tid; sl < 16 * CANDS; sl += NTH) {
+            const int q = sl / CANDS, j = sl % CANDS;
             if (q < CS && (uint32_t)j < s.cnt_q[q]) atomicAdd(&s.hist[(s.cand[q][j].x >> 12) & 255u], 1u);
         }
         cta_sync();
@@ -257,12 +260,12 @@ struct FastSelect {
         const uint32_t need = krem - s.bcast[5];  // keys to keep inside sub-bin bA (>= 1)
         // (no shared atomics here: fire-and-forget ATOMS on a few hot counters
         // serialise and stall every later shared access of the CTA by microseconds)
-        static_assert(kFastCandPerCta % 32 == 0 && NTH % kFastCandPerCta == 0, "one q per warp");
+        static_assert(CANDS % 32 == 0 && NTH % CANDS == 0, "one q per warp");
         // the members of sub-bin bA (usually a handful) compacted into sub[]
         const uint32_t nsub = s.hist[bA];
         if (nsub <= (uint32_t)kFastSub) {
-            for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
-                const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
+            for (int sl = tid; sl < 16 * CANDS; sl += NTH) {
+                const int q = sl / CANDS, j = sl % CANDS;
                 if (q < CS && (uint32_t)j < s.cnt_q[q]) {
                     const uint2 c = s.cand[q][j];
                     if (((c.x >> 12) & 255u) == bA) s.sub[atomicAdd(&s.bcast[6], 1u)] = c;
@@ -270,8 +273,8 @@ struct FastSelect {
             }
             cta_sync();
         }
-        for (int sl = tid; sl < 16 * kFastCandPerCta; sl += NTH) {
-            const int q = sl / kFastCandPerCta, j = sl % kFastCandPerCta;
+        for (int sl = tid; sl < 16 * CANDS; sl += NTH) {
+            const int q = sl / CANDS, j = sl % CANDS;
             bool take = false;
             if (q < CS && (uint32_t)j < s.cnt_q[q]) {
                 const uint2 c = s.cand[q][j];
@@ -299,7 +302,14 @@ struct FastSelect {
             if ((tid & 31) == 0) s.sel2[q][j >> 5] = bal;
         }
         cta_sync();
-        if (tid < 16) s.sel_q[tid] = (uint32_t)(__popc(s.sel2[tid][0]) + __popc(s.sel2[tid][1]));
+        if constexpr (CANDS == 64) {  // (the fused kernel's instance: kept verbatim, it is latency-critical)
+            if (tid < 16) s.sel_q[tid] = (uint32_t)(__popc(s.sel2[tid][0]) + __popc(s.sel2[tid][1]));
+        } else if (tid < 16) {
+            uint32_t c = 0u;
+#pragma unroll
+            for (int w = 0; w < CANDS / 32; ++w) c += (uint32_t)__popc(s.sel2[tid][w]);
+            s.sel_q[tid] = c;
+        }
         cta_sync();
         stamp(tr, 2);
         uint32_t off = 0u;
@@ -310,10 +320,18 @@ struct FastSelect {
         // output slot of a kept row = off + (rows above b* before it) + (kept b* candidates
         // before it); both prefixes come from the slot-assignment scan and the candidate
         // ballot masks, so no second block scan
-        const uint32_t m0 = s.sel2[rank][0], m1 = s.sel2[rank][1];
+        const uint32_t* msk = s.sel2[rank];
+        const uint32_t m0 = msk[0], m1 = msk[1];
         auto kept_cands_before = [&](uint32_t e) -> uint32_t {
-            return e >= 32u ? (uint32_t)__popc(m0) + (uint32_t)__popc(m1 & ((1u << (e - 32u)) - 1u))
-                            : (uint32_t)__popc(m0 & ((1u << e) - 1u));
+            if constexpr (CANDS == 64) {
+                return e >= 32u ? (uint32_t)__popc(m0) + (uint32_t)__popc(m1 & ((1u << (e - 32u)) - 1u))
+                                : (uint32_t)__popc(m0 & ((1u << e) - 1u));
+            } else {
+                uint32_t c = 0u;
+                for (uint32_t w = 0; w < (e >> 5); ++w) c += (uint32_t)__popc(msk[w]);
+                if (e & 31u) c += (uint32_t)__popc(msk[e >> 5] & ((1u << (e & 31u)) - 1u));
+                return c;
+            }
         };
         uint32_t gtc = pre_gt, eqc = pre_eq;
         for (int i = i0; i < i1; ++i) {
