@@ -511,7 +511,12 @@ void plan_retrieve_tc(int units, int n_q, int g, int nv, int capacity, bool visu
     const int NQ = n_q * g;
     const int nqb = (NQ + RT_XROWS - 1) / RT_XROWS;
     const int range = visual_only ? nv : capacity;
-    const int n = std::max(1, std::min(64, 2 * sms / std::max(1, units * nqb)));
+    // CTA budget in waves (measured on the long-video cache, FULL_PREFIX, us: n_q = 32: 1 wave
+    // 61.8 vs 2 waves 65.8; n_q = 128: 148.8 vs 154.3; n_q = 512 (112 query blocks): 4 waves
+    // 414 vs 2 waves 450): few query blocks -> one wave of long key chunks, many -> 4 waves
+    int waves = (units * nqb * 2 >= sms) ? 4 : 1;
+    if (const char* e = getenv("SVL_RT_WAVES")) waves = std::max(1, std::min(4, atoi(e)));  // experiment knob
+    const int n = std::max(1, std::min(64, waves * sms / std::max(1, units * nqb)));
     *nkc = n;
     *chunk = ((range + n - 1) / n + RT_YROWS - 1) / RT_YROWS * RT_YROWS;
 }
