@@ -429,7 +429,7 @@ def main():
     packed = [svl.pack_kv(Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l]) for l in range(LAYERS)]
     ident = torch.arange(wl.k, dtype=torch.int32, device=dev).expand(wl.B, wl.Hkv, wl.k).contiguous()
     ws_p = svl.Workspace(dev)
-    ws_p.get(256)
+    ws_p.get(1024)
     g_pack = graph_of(lambda: [svl.pack_kv(Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l], Kp=packed[l][0],
                                            Vp=packed[l][1], ws=ws_p) for l in range(LAYERS)])
     g_decode_packed = graph_of(lambda: [svl.sparse_decode_attn(qds[l], packed[l][0], packed[l][1], packed[l][2],

@@ -15,9 +15,13 @@
  *  - Stateless and re-entrant.  The only globals are a thread-local
  *    last-error string and an immutable per-device attribute cache.
  *  - Scratch comes from a caller-supplied device `workspace` of at least
- *    svl_*_workspace_size(...) bytes, 256-byte aligned, which must be zero
- *    filled once before its first use (svl_workspace_init); every call leaves
- *    its counters at zero again.  A workspace serves one call at a time.
+ *    svl_*_workspace_size(...) bytes (SVL_WORKSPACE_HEADER_BYTES for the calls
+ *    without a size function), 256-byte aligned, which must be zero filled
+ *    once before its first use (svl_workspace_init).  Its header
+ *    (SVL_WORKSPACE_HEADER_BYTES) holds the device flag word and small
+ *    self-maintained counters; calls never write another call's header words,
+ *    so one workspace may serve any sequence of calls on one stream.  Two calls
+ *    that may run concurrently need distinct workspaces.
  *  - bf16 tensors are IEEE bfloat16 bit patterns (uint16).  Row pointers and
  *    row strides must be 16-byte aligned.  Head dims d in {64, 128}.
  *
@@ -46,6 +50,8 @@ typedef enum {
     SVL_ERR_CUDA = 6              /* a CUDA runtime call or kernel launch failed               */
 } svl_status;
 
+#define SVL_WORKSPACE_HEADER_BYTES 1024u
+
 /* Device-side precondition bits, OR-ed into the workspace flag word
  * (svl_read_device_flags).  Offending elements are skipped / treated as the
  * lowest key so kernels never fault. */
@@ -63,6 +69,19 @@ typedef enum {
  * SCORE_ONLY call with identical arguments.  Neither bit = both phases. */
 #define SVL_RETRIEVE_SCORE_ONLY 0x100u
 #define SVL_RETRIEVE_SELECT_ONLY 0x200u
+/* svl_fresh_decode_step: always run the two separate calls (svl_retrieve then
+ * svl_sparse_decode_attn) instead of the fused kernel (A/B measurements, tests). */
+#define SVL_FRESH_UNFUSED 0x400u
+/* Split-count pin, flags bits 24..31 (0 = the planner's choice).
+ * svl_sparse_decode_attn(_push): exactly n CTAs per (b, KV group) unit
+ * (B*Hkv*n must not exceed the co-resident CTA count when n > 1, else
+ * SVL_ERR_UNSUPPORTED); svl_fresh_decode_step: a cluster of n CTAs per unit
+ * (n = 8 or 16; the fused kernel then runs even past one wave).  Results are a
+ * deterministic function of the inputs and the split count, so a sharded run
+ * reproduces the unsharded one bitwise when both pin the same n
+ * (SURVEY.md 8(e) e5).  The workspace-size calls take the same flags. */
+#define SVL_PIN_SPLITS(n) (((uint32_t)(n) & 0xffu) << 24)
+#define SVL_PIN_SPLITS_MASK 0xff000000u
 
 /* Salience modes */
 #define SVL_SAL_SUMMARY 0       /* S == 1 summary token (CLIP)               */
@@ -140,8 +159,15 @@ size_t svl_retrieve_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hk
  * token's K/V before the call (reading A9).
  *   out[b,h,:] = sum_j softmax(scale * q.K_j)_j V_j   (fp32, reading A18)
  *   lse[b,h]   = natural-log log-sum-exp of the attended logits
- * Split-K flash-decoding with a log-sum-exp merge across splits; the merge
- * order is fixed, results are bitwise reproducible.
+ * Split-K flash-decoding with a log-sum-exp merge across splits: the grid
+ * (S splits per unit) is sized to the co-resident CTA count and launched
+ * cooperatively; each split stores its partial (o, m, l) to the workspace
+ * tagged with the unit's call epoch (a counter in the workspace header that
+ * the unit's first CTA advances once per call), and every split merges a
+ * 1/S slice of the unit's outputs as soon as the tagged partials it needs are
+ * visible.  The merge order is fixed: results are bitwise reproducible for a
+ * given split count.
+ * flags    SVL_SELECT_SHARED, SVL_PIN_SPLITS(n).
  *
  * q        device bf16 [B][H][d] contiguous; g = H/Hkv <= 16.
  * K, V     device KV views with identical capacity.
@@ -202,7 +228,7 @@ svl_status svl_rope_remap(svl_kv K_pre, svl_kv V, int32_t B, int32_t Hkv, int32_
  *          SVL_SELECT_SHARED); violations set SVL_DEVFLAG_INDEX and are clamped.
  * Kp, Vp   destination views, capacity >= vb + k + (K.capacity - vb - N_v);
  *          must not overlap the sources.
- * No workspace beyond the header word (device flags); asynchronous on `stream`.
+ * Workspace: SVL_WORKSPACE_HEADER_BYTES (device flags); asynchronous on `stream`.
  */
 svl_status svl_pack_kv(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
                        const int32_t* vis_idx, int32_t k, uint32_t flags, svl_kv Kp, svl_kv Vp,
@@ -228,7 +254,7 @@ svl_status svl_pack_kv(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d, sv
  * peer_flags HOST array [P] of device pointers: rank r's flag row uint32 [P].
  * rank, P    this rank, 1 <= P <= 8 (one NVLink/NVSwitch node).
  * epoch      > 0, increasing per call (flags compare modulo 2^32).
- * The workspace header's word 1 is a CTA counter (zero between calls).
+ * The workspace header's word 3 is the kernel's self-resetting CTA counter.
  */
 svl_status svl_sparse_decode_attn_push(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
                                        svl_kv K, svl_kv V, svl_span span, const int32_t* vis_idx,
@@ -260,7 +286,8 @@ svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void
  * svl_retrieve + svl_sparse_decode_attn up to fp32 rounding of the LSE.
  *
  * q        device bf16 [B][H][d] contiguous (the current token, post-RoPE).
- * flags    SVL_NORM_VISUAL_ONLY or 0 (SVL_SELECT_SHARED -> UNSUPPORTED).
+ * flags    SVL_NORM_VISUAL_ONLY, SVL_FRESH_UNFUSED, SVL_PIN_SPLITS(8 or 16)
+ *          (SVL_SELECT_SHARED -> UNSUPPORTED).
  * idx_out  device int32 [B][Hkv][k]: the kept visual indices (reusable by
  *          later svl_sparse_decode_attn steady steps).
  * out      device fp32 [B][H][d]; lse_out device fp32 [B][H] or NULL.

@@ -120,19 +120,41 @@ static RetrieveTcLayout retrieve_tc_layout(int B, int n_q, int H, int Hkv, int d
 }
 
 // --------------------------------------------------------------- decode plan
-static int plan_splits(int units, int n_att_max, int sms) {
-    // CTAs per unit = cluster size: the largest power of two <= 16 that keeps the grid
-    // within ONE wave (one 159 KB CTA per SM) and at least one 16-row tile per CTA.
-    // Measured: the gather is per-SM bound, so a second partial wave costs more than
-    // the longer per-CTA row lists (multi-turn B = 8: 16.1 us at 4 splits vs 26.8 at 8;
-    // sweep B = 16: 92 us at 2 vs 98 at 4, 134 at 8)
-    int S = 16;
-    while (S > 1 && (units * S > sms || S * 16 > n_att_max)) S >>= 1;
-    if (const char* e = getenv("SVL_DECODE_S")) {  // experiment knob
-        const int v = atoi(e);
-        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) S = v;
+// Splits per unit.  The grid (units x S CTAs) never exceeds the co-resident CTA
+// count (the split merge is a grid-wide barrier), so S = floor(SMs * occ / units)
+// for occ in {1, 2} CTAs per SM, at least kDecodeMinRows attended rows per CTA;
+// of the two the one with the smaller per-SM row load (ties: more CTAs).
+constexpr int kDecodeMinRows = 32;
+#ifndef SVL_DECODE_OCC
+#define SVL_DECODE_OCC 2  // (the kernel's shared memory allows one CTA per SM today)
+#endif
+static int decode_slots(int d) { return device_sm_count() * std::max(1, decode_ctas_per_sm(d)); }
+
+static int plan_splits(int units, int n_att_max, int d, uint32_t flags) {
+    if (const int pin = (int)(flags >> 24)) return pin;
+    const int sms = device_sm_count();
+    const int occ_max = std::min(SVL_DECODE_OCC, std::max(1, decode_ctas_per_sm(d)));
+    const int smax = std::max(1, n_att_max / kDecodeMinRows);
+    int bestS = 1;
+    long best = -1;
+    for (int occ = 1; occ <= occ_max; ++occ) {
+        const int S = std::max(1, std::min(smax, sms * occ / std::max(units, 1)));
+        if (S > 1 && (long)units * S > (long)sms * occ) continue;
+        const long ctas = (long)units * S;
+        const long rows = (n_att_max + S - 1) / S;
+        const long cost = ((ctas + sms - 1) / sms) * rows;
+        if (best < 0 || cost < best || (cost == best && S > bestS)) {
+            best = cost;
+            bestS = S;
+        }
     }
-    return S;
+    return bestS;
+}
+
+static size_t decode_ws_bytes(int units, int S, int d) {
+    if (S <= 1) return kWsHeader;
+    const size_t stride = (d == 128) ? kDecodePartStride<128> : kDecodePartStride<64>;
+    return kWsHeader + (size_t)units * S * stride * sizeof(uint64_t);
 }
 
 }  // namespace svl
@@ -172,7 +194,10 @@ bool encode_kv_tensor_map(CUtensorMap* map, const void* data, int d, int capacit
 
 extern "C" {
 
-const char* svl_version(void) { return "libsparsevila 0.1 sm_100a (tensor-core mma.sync swap-AB, cluster radix select)"; }
+const char* svl_version(void) {
+    return "libsparsevila 0.2 sm_100a (fused fresh step: TMA + tcgen05 K stream, cluster top-k over DSMEM; "
+           "steady decode: all-SM split-K gather with a grid-barrier merge)";
+}
 
 const char* svl_status_string(svl_status s) {
     switch (s) {
@@ -388,10 +413,10 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
 size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                         int32_t visual_len, int32_t capacity, uint32_t flags) {
     (void)flags;
-    if (B < 1 || Hkv < 1 || H % Hkv || capacity < 1) return 0;
-    (void)d; (void)k; (void)visual_len;
-    // flag word only: the split merge is on chip (cluster DSMEM); + debug trace
-    return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
+    if (B < 1 || Hkv < 1 || H % Hkv || capacity < 1 || k < 0 || visual_len < 0) return 0;
+    const int n_att_max = std::max(1, k + std::max(0, capacity - visual_len));
+    const int units = B * Hkv;
+    return decode_ws_bytes(units, plan_splits(units, n_att_max, d, flags), d);
 }
 
 struct PushArgs {
@@ -408,7 +433,7 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
                                      const PushArgs& push, const char* name) {
     if (!q || (!out && push.P == 0) || !span.seq_len || (k > 0 && !vis_idx))
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
-    if (flags & ~(SVL_SELECT_SHARED)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
     if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
     if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
     if (span.visual_begin < 0 || span.visual_len < 0 ||
@@ -432,8 +457,10 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
 
     const int units = B * Hkv;
     const int n_att_max = std::max(1, k + std::max(0, K.capacity - span.visual_len));
-    const int S = plan_splits(units, n_att_max, device_sm_count());
-    if (ws_bytes < kWsHeader) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    const int S = plan_splits(units, n_att_max, d, flags);
+    if (S > 1 && ((long)units * S > decode_slots(d) || units > kWsEpochs))
+        return fail(SVL_ERR_UNSUPPORTED, "pinned split count: B*Hkv*n exceeds the co-resident CTA count%s");
+    if (ws_bytes < decode_ws_bytes(units, S, d)) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
 
     DecodeParams p;
     p.q = static_cast<const uint16_t*>(q);
@@ -452,9 +479,14 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     p.out = out;
     p.lse_out = lse_out;
     p.flags = static_cast<uint32_t*>(ws);
-    p.trace = (getenv("SVL_TRACE") && ws_bytes >= kWsHeader + ((size_t)1 << 20))
-                  ? reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader)
-                  : nullptr;
+    p.part = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader);
+    p.sync = static_cast<uint32_t*>(ws);  // header: word 0 is the flag word
+    p.epochs = static_cast<uint32_t*>(ws) + kWsEpochWord;
+    p.trace = nullptr;
+#if SVL_TRACE_BUILD  // phase-stamp builds (tools/trace_decode.py): the last 1 MB of a larger workspace
+    if (ws_bytes >= decode_ws_bytes(units, S, d) + ((size_t)1 << 20))
+        p.trace = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + ws_bytes - ((size_t)1 << 20));
+#endif
     p.P = push.P;
     p.rank = push.rank;
     p.b0 = push.b0;
@@ -466,7 +498,6 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
         p.peer_out[r] = (r < push.P) ? push.peer_out[r] : nullptr;
         p.peer_flags[r] = (r < push.P) ? push.peer_flags[r] : nullptr;
     }
-    p.done = static_cast<uint32_t*>(ws) + 1;  // header word 1
     cudaError_t e = launch_decode(p, d, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, name);
     return SVL_OK;
@@ -577,7 +608,8 @@ svl_status svl_sparse_decode_attn_push(const void* q, int32_t B, int32_t H, int3
     for (int r = 0; r < P; ++r)
         if (!peer_out[r] || !peer_flags[r] || !aligned16(peer_out[r]))
             return fail(SVL_ERR_INVALID_ARGUMENT, "NULL or misaligned peer buffer%s");
-    if (b0 < 0 || h0 < 0 || b0 + B > B_total || h0 + H > H_total || H_total % (H / std::max(Hkv, 1)))
+    if (B < 1 || H < 1 || Hkv < 1 || H % Hkv) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1 and H %% Hkv == 0%s");
+    if (b0 < 0 || h0 < 0 || b0 + B > B_total || h0 + H > H_total || H_total % (H / Hkv))
         return fail(SVL_ERR_SHAPE, "shard (b0, h0, B, H) outside (B_total, H_total)%s");
     PushArgs push;
     push.P = P;
@@ -607,8 +639,8 @@ svl_status svl_wait_flags(const uint32_t* flags, int32_t P, uint32_t epoch, void
 // ----------------------------------------------------- fused fresh step
 // Cluster size and eligibility of the fused kernel for a shape.
 
-static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice, int d) {
-    if (g > 16) return false;
+static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int& slice, int d, uint32_t flags) {
+    if (g > 16 || (flags & SVL_FRESH_UNFUSED)) return false;
     const int smax = kFusedSliceMax / ((g + 7) / 8);
     int cmin = (nv + smax - 1) / smax;
     if (cmin > 16) return false;
@@ -619,12 +651,8 @@ static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int
     const int want = (units * 16 <= 2 * device_sm_count()) ? 16 : 8;
     CS = std::max(c, want);
     bool pinned = false;
-    if (const char* pin = getenv("SVL_FRESH_CS")) {  // test knob: pin the split count (8 or 16)
-        const int v = atoi(pin);
+    if (const int v = (int)(flags >> 24)) {  // SVL_PIN_SPLITS(8 or 16)
         if ((v == 8 || v == 16) && v >= c) CS = v, pinned = true;
-    }
-    if (const char* f = getenv("SVL_FUSED")) {  // experiment knob: 0 = always the two-call path
-        if (atoi(f) == 0) return false;
     }
     // The fused kernel only while every unit's cluster is co-resident (one wave).  Beyond
     // that the two-call kernels, which spread over every SM, are faster (measured, us/layer
@@ -645,10 +673,11 @@ size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_
                                        int32_t visual_len, int32_t capacity, uint32_t flags) {
     if (B < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;
     int CS, slice;
-    if (fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice, d))
-        return getenv("SVL_TRACE") ? kWsHeader + ((size_t)1 << 20) : kWsHeader;
-    return std::max(svl_retrieve_workspace_size(B, 1, H, Hkv, d, visual_len, flags),
-                    svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags));
+    // (the fused plan needs the header only; the size covers the two-call path too, which
+    // the step also takes when the K view cannot be encoded as a TMA tensor map)
+    (void)CS; (void)slice;
+    return std::max(svl_retrieve_workspace_size(B, 1, H, Hkv, d, visual_len, flags & SVL_NORM_VISUAL_ONLY),
+                    svl_sparse_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, 0u));
 }
 
 svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hkv, int32_t d,
@@ -657,9 +686,9 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
                                  void* ws, size_t ws_bytes, void* stream) {
     if (!q || !out || !span.seq_len || (k > 0 && !idx_out))
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
-    if (flags & ~SVL_NORM_VISUAL_ONLY)
+    if (flags & ~(SVL_NORM_VISUAL_ONLY | SVL_FRESH_UNFUSED | SVL_PIN_SPLITS_MASK))
         return fail((flags & SVL_SELECT_SHARED) ? SVL_ERR_UNSUPPORTED : SVL_ERR_INVALID_ARGUMENT,
-                    "svl_fresh_decode_step accepts only SVL_NORM_VISUAL_ONLY%s");
+                    "svl_fresh_decode_step accepts SVL_NORM_VISUAL_ONLY, SVL_FRESH_UNFUSED, SVL_PIN_SPLITS%s");
     if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
     if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
     if (span.visual_len < 1) return fail(SVL_ERR_SHAPE, "no visual rows to retrieve from%s");
@@ -684,11 +713,11 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
 
     int CS, slice;
     FreshParams p;
-    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice, d) ||
+    if (!fresh_plan(B, Hkv, g, span.visual_len, K.capacity, CS, slice, d, flags) ||
         !encode_kv_tensor_map(&p.ktmap, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 128)) {
         // outside the on-chip budget: the two separate calls (same q as [B][1][H][d])
-        st = svl_retrieve(q, B, 1, H, Hkv, d, K, span, nullptr, k, scale, flags, idx_out, nullptr,
-                          ws, ws_bytes, stream);
+        st = svl_retrieve(q, B, 1, H, Hkv, d, K, span, nullptr, k, scale, flags & SVL_NORM_VISUAL_ONLY, idx_out,
+                          nullptr, ws, ws_bytes, stream);
         if (st != SVL_OK) return st;
         return svl_sparse_decode_attn(q, B, H, Hkv, d, K, V, span, idx_out, k, 0u, scale, out,
                                       lse_out, ws, ws_bytes, stream);
@@ -702,15 +731,17 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
     p.B = B; p.H = H; p.Hkv = Hkv; p.g = g;
     p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k; p.capacity = K.capacity;
     p.slice = slice;
-    p.flags_in = flags;
+    p.flags_in = flags & SVL_NORM_VISUAL_ONLY;
     p.scale2 = scale * kLog2e;
     p.idx_out = idx_out;
     p.out = out;
     p.lse_out = lse_out;
     p.flags = static_cast<uint32_t*>(ws);
-    p.trace = (getenv("SVL_TRACE") && ws_bytes >= kWsHeader + ((size_t)1 << 20))
-                  ? reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader)
-                  : nullptr;
+    p.trace = nullptr;
+#if SVL_TRACE_BUILD  // phase-stamp builds (tools/trace_fresh.py): 1 MB after the header
+    if (ws_bytes >= kWsHeader + ((size_t)1 << 20))
+        p.trace = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + kWsHeader);
+#endif
     cudaError_t e = launch_fresh(p, d, CS, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "svl_fresh_decode_step");
     return SVL_OK;
@@ -813,7 +844,7 @@ svl_status svl_salience(const void* Qe, const void* Ke, int32_t F, int32_t S, in
     // INTRA_VISUAL with no summary rows and frames of <= 512 tokens: the tcgen05 kernel
     // ([F][T][H_e][d_e] as 4-D {d_e, T, H_e, F} tensor maps); otherwise the mma.sync passes
     const int64_t T = (int64_t)S + N_f;
-    p.use_tc = (mode == SVL_SAL_INTRA_VISUAL && S == 0 && N_f <= 512 && d_e % 8 == 0 && !getenv("SVL_SALIENCE_NO_TC") &&
+    p.use_tc = (mode == SVL_SAL_INTRA_VISUAL && S == 0 && N_f <= 512 && d_e % 8 == 0 &&
                 encode_kv_tensor_map(&p.qmap, Qe, d_e, (int)T, H_e, F, T * H_e * d_e, d_e, (int64_t)H_e * d_e, 128) &&
                 encode_kv_tensor_map(&p.kmap, Ke, d_e, (int)T, H_e, F, T * H_e * d_e, d_e, (int64_t)H_e * d_e, 128))
                    ? 1 : 0;

@@ -378,8 +378,13 @@ SVL_DEV uint32_t float_key(float f, bool& nonfinite_nan) {
 }
 
 // ------------------------------------------------------------------ flags
-// Workspace header: word 0 = device flag word (SVL_DEVFLAG_*).
-constexpr size_t kWsHeader = 256;
+// Workspace header (SVL_WORKSPACE_HEADER_BYTES): word 0 = device flag word
+// (SVL_DEVFLAG_*); word 3 = the push decode's grid-departure counter; words
+// [kWsEpochWord, kWsEpochWord + kWsEpochs) = the steady decode's per-unit call
+// epochs (decode.cu).  Self-maintained; zero-filled once by the caller.
+constexpr size_t kWsHeader = 1024;
+constexpr int kWsEpochWord = 64;
+constexpr int kWsEpochs = 192;
 SVL_DEV void raise_flag(uint32_t* ws_flags, uint32_t bit) { atomicOr(ws_flags, bit); }
 
 }  // namespace svl

@@ -160,10 +160,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     if (p.trace && tid == 0) trs[30] = clock64();
 
     // ------------------------------------------------------------ geometry
-    // The visual slice does not depend on anything an upstream kernel writes, so its
-    // first stages are requested before griddepcontrol.wait (programmatic dependent
-    // launch: this prologue overlaps the previous kernel's tail); seq_len, q and the
-    // text rows (the current token's K) are read only after the wait.
+    // Programmatic dependent launch: the prologue (barrier init, TMEM allocation, L2
+    // prefetch of the first visual stages) overlaps the previous kernel's tail; every
+    // read of data an upstream kernel may write (seq_len, q, K, V) follows the wait.
     const int slice = p.slice;
     const int v0 = min(p.nv, rank * slice);
     const int nvis = min(p.nv, v0 + slice) - v0;
@@ -283,18 +282,13 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 mbar_arrive_expect_tx(smem_u32(mrg), (uint32_t)(CS * (mine + 16) * 4));
             }
             fence_mbar_init();
-            for (int i = 0; i < min(NST, nstages); ++i) issue(i);  // visual stages: upstream-independent
-#ifndef SVL_L2PF
-#define SVL_L2PF 0  // measured: 31.6 vs 30.0 us/layer with it (long-video) -- off
-#endif
-#if SVL_L2PF
-            // the rest of the visual slice -> L2 (HBM is idle while the upstream kernel's
-            // post-stream phase runs; the ring refills below then hit L2)
-            for (int i = NST; i < nvs; ++i)
+            // before the PDL wait only L2 prefetches of the first stages (a hint: the data
+            // is read into shared memory after the wait, so an upstream kernel that writes
+            // visual K rows -- svl_rope_remap, svl_pack_kv -- is always seen)
+            for (int i = 0; i < min(NST, nstages); ++i)
 #pragma unroll
                 for (int hf = 0; hf < D / 64; ++hf)
                     tma_prefetch_4d(&p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b);
-#endif
         }
         __syncwarp();
     }
@@ -315,7 +309,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     }
     nsys = max(0, min(ntext, p.vb - t0));
     if (warp == 0) {
-        if (lane == 0) issue_text();  // the text rows (none: completes at once)
+        if (lane == 0) {
+            for (int i = 0; i < min(NST, nstages); ++i) issue(i);  // the first visual stages
+            issue_text();  // the text rows (none: completes at once)
+        }
         __syncwarp();
     }
     // q tile (UMMA B operand): row c = head G*g + c (zero for c >= g), K-major,
@@ -921,7 +918,7 @@ cudaError_t launch_fresh_t(const FreshParams& p, int CS, cudaStream_t s) {
     // K stages) may start while the previous kernel on the stream drains; the kernel
     // executes griddepcontrol.wait before reading anything that kernel may write
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = getenv("SVL_NO_PDL") ? 0 : 1;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fresh_kernel<D, NT>, p);

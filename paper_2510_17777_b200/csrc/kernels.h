@@ -63,12 +63,15 @@ struct DecodeParams {
     const int32_t* seq_len;
     const int32_t* idx;  // [B][U][k]
     int B, H, Hkv, g, vb, nv, k, shared, capacity;
-    int S;         // splits per unit = CTAs of the unit's cluster (<= 16)
+    int S;         // splits (CTAs) per unit; the grid (S x units) is co-resident
     float scale2;  // scale * log2(e)
     float* out;    // [B][H][d]
     float* lse_out;
     uint32_t* flags;
-    uint64_t* trace;  // debug: per-CTA phase timestamps (SVL_TRACE=1), else null
+    uint64_t* part;    // workspace: split partials [units * S][kDecodePartStride] (bits, tag) pairs (S > 1)
+    uint32_t* sync;    // workspace header: word 3 = the push variant's departure counter (self-resetting)
+    uint32_t* epochs;  // workspace header: per-unit call epochs [units] (tags of the partials)
+    uint64_t* trace; // SVL_TRACE_BUILD only: per-CTA phase stamps [grid][16] (else null)
     // push variant (svl_sparse_decode_attn_push): P > 0 => the merged out tile is also
     // stored into every peer's gathered [B_total][H_total][d] buffer at (b0, h0), and
     // the last CTA raises peer_flags[r][rank] = epoch (release, system scope)
@@ -76,8 +79,11 @@ struct DecodeParams {
     uint32_t epoch;
     float* peer_out[kMaxPeers];
     uint32_t* peer_flags[kMaxPeers];
-    uint32_t* done;  // workspace counter (header word 1): CTAs finished this call
 };
+template <int D>
+constexpr int kDecodePartStride = 16 * D + 32;  // o [16][D], M [16], l [16] (64-bit tagged fp32)
+constexpr int kDecodeMaxSplits = 256;           // splits per unit (merge staging: S * slice <= g D + S)
+int decode_ctas_per_sm(int d);                  // co-resident decode CTAs per SM
 cudaError_t launch_wait_flags(const uint32_t* flags, int P, uint32_t epoch, uint32_t* ws_flags, cudaStream_t s);
 
 struct FreshParams {
@@ -177,7 +183,7 @@ constexpr int kScoreThreads = 512;
 constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA
 constexpr int kDecodeThreads = 256;  // 8 warps x one 16-row tile per batch
-constexpr int kDecodeRowsMax = 128;  // rows per double-buffered gather batch
+constexpr int kDecodeRowsMax = 128;  // rows per gather batch
 
 cudaError_t launch_score(const ScoreParams& p, int d, int NT, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s);

@@ -515,7 +515,9 @@ void plan_retrieve_tc(int units, int n_q, int g, int nv, int capacity, bool visu
     // 61.8 vs 2 waves 65.8; n_q = 128: 148.8 vs 154.3; n_q = 512 (112 query blocks): 4 waves
     // 414 vs 2 waves 450): few query blocks -> one wave of long key chunks, many -> 4 waves
     int waves = (units * nqb * 2 >= sms) ? 4 : 1;
-    if (const char* e = getenv("SVL_RT_WAVES")) waves = std::max(1, std::min(4, atoi(e)));  // experiment knob
+#ifdef SVL_RT_WAVES
+    waves = SVL_RT_WAVES;  // A/B builds only
+#endif
     const int n = std::max(1, std::min(64, waves * sms / std::max(1, units * nqb)));
     *nkc = n;
     *chunk = ((range + n - 1) / n + RT_YROWS - 1) / RT_YROWS * RT_YROWS;
@@ -544,7 +546,12 @@ cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s) {
     p1.xmap = p.kmap_x;  // X = K blocks
     p1.ymap = p.qmap_y;  // Y = Q chunks
     const int nkb = (p.nv + RT_XROWS - 1) / RT_XROWS;
-    if (p.NQP == RT_YROWS && !getenv("SVL_RT_NO_QRES")) {  // Q tile resident, CTAs walk key blocks
+#ifndef SVL_RT_NO_QRES
+    constexpr bool qres = true;
+#else
+    constexpr bool qres = false;  // A/B builds only
+#endif
+    if (p.NQP == RT_YROWS && qres) {  // Q tile resident, CTAs walk key blocks
         const int per_unit = std::max(1, std::min(nkb, (2 * sms + units - 1) / units));
         const dim3 g2(per_unit, units, 1);
         static bool attr_done[64][2] = {};

@@ -447,7 +447,11 @@ static cudaError_t launch_fast(Kern kern, const SelectParams& p, int n_units, cu
 
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
     const int slice = (p.nv + p.CS - 1) / p.CS;
-    const bool fast = !getenv("SVL_OLD_SELECT");
+#ifndef SVL_OLD_SELECT
+    const bool fast = true;  // the generic cluster kernels below stay for slices past the fast-path capacity
+#else
+    const bool fast = false;  // A/B builds only
+#endif
     if (fast && p.mode == 2 && slice <= FsLayout<256>::kFsSliceMax)
         return launch_fast<256>(select_fast_kernel<2, 1, 256>, p, n_units, s, *attr_flag(6));
     if (fast && p.mode == 0 && slice <= FsLayout<64>::kFsSliceMax) {

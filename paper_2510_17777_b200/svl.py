@@ -22,6 +22,14 @@ SVL_NORM_VISUAL_ONLY = 1
 SVL_SELECT_SHARED = 2
 SVL_RETRIEVE_SCORE_ONLY = 0x100
 SVL_RETRIEVE_SELECT_ONLY = 0x200
+SVL_FRESH_UNFUSED = 0x400
+WORKSPACE_HEADER_BYTES = 1024  # SVL_WORKSPACE_HEADER_BYTES
+SVL_PIN_SPLITS_MASK = 0xff000000
+
+
+def SVL_PIN_SPLITS(n: int) -> int:
+    """flags bits 24..31: pin the per-unit split count (include/sparsevila.h)."""
+    return (int(n) & 0xff) << 24
 SVL_SAL_SUMMARY, SVL_SAL_MULTI_SUMMARY, SVL_SAL_INTRA_VISUAL = 0, 1, 2
 SVL_DEVFLAG_INDEX, SVL_DEVFLAG_NONFINITE, SVL_DEVFLAG_SPAN, SVL_DEVFLAG_WAIT_TIMEOUT = 1, 2, 4, 8
 
@@ -162,7 +170,7 @@ class Workspace:
         self.device = device
 
     def get(self, nbytes: int, stream=None) -> torch.Tensor:
-        nbytes = max(int(nbytes), 256)
+        nbytes = max(int(nbytes), WORKSPACE_HEADER_BYTES)
         if self.buf is None or self.buf.numel() < nbytes:
             self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device or "cuda")
         return self.buf
@@ -244,7 +252,7 @@ def rope_remap(K_pre: torch.Tensor, V: Optional[torch.Tensor], seq_len: torch.Te
     if V is not None and V_out is None:
         V_out = torch.zeros(B, Hkv, ocap, d, dtype=V.dtype, device=V.device)
     null_kv = svl_kv(None, 0, 0, 0, 0)
-    w = _ws(ws, K_pre.device).get(256)
+    w = _ws(ws, K_pre.device).get(WORKSPACE_HEADER_BYTES)
     _check(lib().svl_rope_remap(kv_view(K_pre, "K_pre"), kv_view(V, "V") if V is not None else null_kv, B, Hkv, d,
                                 span(visual_begin, visual_len, seq_len), _cuda(kept, "kept", torch.int32), k,
                                 float(rope_base), kv_view(K_out, "K_out"),
@@ -265,7 +273,7 @@ def pack_kv(K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor, visual_begi
         Kp = torch.empty(B, Hkv, pcap, d, dtype=K.dtype, device=K.device)
     if Vp is None:
         Vp = torch.empty(B, Hkv, pcap, d, dtype=V.dtype, device=V.device)
-    w = _ws(ws, K.device).get(256)
+    w = _ws(ws, K.device).get(WORKSPACE_HEADER_BYTES)
     _check(lib().svl_pack_kv(kv_view(K, "K"), kv_view(V, "V"), B, Hkv, d,
                              span(visual_begin, visual_len, seq_len),
                              _cuda(vis_idx, "vis_idx", torch.int32), k, flags, kv_view(Kp, "Kp"),
@@ -340,7 +348,7 @@ def sparse_decode_attn_push(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, s
 
 def wait_flags(flags: torch.Tensor, epoch: int, ws: Optional[Workspace] = None, stream=None):
     """svl_wait_flags: stream-ordered wait until flags[s] >= epoch for all s (int32 [P] tensor)."""
-    w = _ws(ws, flags.device).get(256)
+    w = _ws(ws, flags.device).get(WORKSPACE_HEADER_BYTES)
     _check(lib().svl_wait_flags(_cuda(flags, "flags", torch.int32), flags.numel(), epoch,
                                 w.data_ptr(), _stream(stream)))
 

@@ -1,0 +1,97 @@
+"""svl_sparse_decode_attn's split-K decomposition (SURVEY.md 8(a) a4 + a5): the
+attended rows of each (b, KV group) unit are cut into S splits, one CTA each,
+merged after a grid-wide barrier.  The result must match the fp64 oracle for
+any S (pinned with SVL_PIN_SPLITS), including more splits than rows (empty
+partials), one split (no merge), and every split count reruns bitwise; the
+barrier's self-resetting counters must survive back-to-back calls with
+different split counts on one workspace, inside a CUDA graph too."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2510_17777_b200 import inputs as gen
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+NTH = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def svl():
+    from paper_2510_17777_b200 import build, svl as mod
+    build.build()
+    mod.lib()
+    return mod
+
+
+def _case(orc, name, seed):
+    wl = gen.CONFIGS[name]
+    cpu = gen.make_decode_inputs(wl, seed=seed)
+    oi, _, _ = orc.retrieve(cpu["q"], cpu["K"], cpu["seq_len"], wl.vb, wl.nv, wl.k, nthreads=NTH)
+    oo, ol = orc.sparse_decode(cpu["q_dec"], cpu["K"], cpu["V"], cpu["seq_len"], wl.vb, wl.nv, oi,
+                               nthreads=NTH)
+    dev = {kk: v.cuda() for kk, v in cpu.items()}
+    return wl, dev, torch.as_tensor(oi).cuda(), oo, ol
+
+
+@pytest.mark.parametrize("name,splits", [("toy", [1, 2, 7, 74]),
+                                         ("long-video", [1, 3, 16, 37])])
+def test_decode_any_split_count_matches_oracle(svl, orc, name, splits):
+    wl, dev, idx, oo, ol = _case(orc, name, seed=81)
+    ws = svl.Workspace()
+    for S in splits:
+        lse = torch.empty(wl.B, wl.H, device="cuda")
+        a, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                      flags=svl.SVL_PIN_SPLITS(S), lse_out=lse, ws=ws)
+        a, lse_a = a.clone(), lse.clone()
+        b, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                      flags=svl.SVL_PIN_SPLITS(S), lse_out=lse, ws=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b) and torch.equal(lse_a, lse), f"S={S} not bitwise repeatable"
+        mx, rel = parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)
+        print(f"{name} S={S}: max-abs {mx:.2e} rel {rel:.2e}")
+    assert ws.flags() == 0
+    # the header counters are back to zero after every call
+    assert int(ws.buf[12:16].view(torch.int32).abs().sum()) == 0  # the push counter (header word 3)
+
+
+def test_decode_planner_default_and_graph_replay(svl, orc):
+    """The planner's split count, inside a CUDA graph replayed many times (the bench's
+    arrangement: PDL between consecutive layers) -- results equal the eager call."""
+    wl, dev, idx, oo, ol = _case(orc, "long-video", seed=82)
+    ws = svl.Workspace()
+    ref, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx, ws=ws)
+    ref = ref.clone()
+    parity.check_attention(ref.cpu().numpy(), None, oo, ol)
+    outs = [torch.empty_like(ref) for _ in range(6)]
+
+    def body():
+        for o in outs:
+            svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                   out=o, ws=ws)
+    body()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            body()
+    for _ in range(50):
+        g.replay()
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
+    assert ws.flags() == 0
+
+
+def test_decode_pin_too_many_splits_rejected(svl):
+    wl = gen.CONFIGS["multi-turn"]  # 32 units: 32 * 255 CTAs cannot be co-resident
+    x = gen.make_decode_inputs(gen.DecodeWorkload(**{**wl.__dict__, "nv": 2048, "k": 200}), seed=83,
+                               device="cuda")
+    idx = torch.arange(200, dtype=torch.int32, device="cuda").expand(wl.B, wl.Hkv, 200).contiguous()
+    with pytest.raises(svl.SvlError) as e:
+        svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, 2048, idx,
+                               flags=svl.SVL_PIN_SPLITS(255))
+    assert e.value.status == 5  # SVL_ERR_UNSUPPORTED

@@ -22,14 +22,15 @@ def svl():
     return mod
 
 
-def _run(svl, orc, wl, seed, flags=0, k=None, big=True):
+def _run(svl, orc, wl, seed, flags=0, k=None, big=True, xflags=0):
+    """fresh step vs the oracle; xflags = library-only flags (SVL_PIN_SPLITS, SVL_FRESH_UNFUSED)"""
     k = wl.k if k is None else k
     x = gen.make_decode_inputs(wl, seed=seed, device="cuda" if big else "cpu")
     cpu = {kk: v.cpu() for kk, v in x.items()}
     dev = {kk: v.cuda() for kk, v in x.items()}
     lse = torch.empty(wl.B, wl.H, device="cuda")
     out, idx = svl.fresh_decode_step(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb,
-                                     wl.nv, k, flags=flags, lse_out=lse)
+                                     wl.nv, k, flags=flags | xflags, lse_out=lse)
     torch.cuda.synchronize()
     idx = idx.cpu().numpy()
     oi, osc, gap = orc.retrieve(cpu["q"], cpu["K"], cpu["seq_len"], wl.vb, wl.nv, k, flags=flags,
@@ -108,22 +109,22 @@ def test_fresh_step_sweep_fallback_sampled(svl, orc):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_fresh_step_simulated_shards_bitwise(svl, P, monkeypatch):
+def test_fresh_step_simulated_shards_bitwise(svl, P):
     """SURVEY.md 4 'simulated-shard test': each rank's (batch x KV-head) slice
     run separately on one GPU and assembled == the unsharded run, bitwise, with
     the per-unit split count pinned -- the planner may pick
     a different cluster size for a different number of units."""
     from paper_2510_17777_b200 import sharding
-    monkeypatch.setenv("SVL_FRESH_CS", "8")
+    pin = svl.SVL_PIN_SPLITS(8)
     wl = gen.DecodeWorkload("shd", 4, 28, 4, 128, 32, 8192, 300, 819, 1, 256)
     x = gen.make_decode_inputs(wl, seed=38, device="cuda")
-    ref, _ = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k)
+    ref, _ = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k, flags=pin)
     ref = ref.clone()
     parts, plans = [], []
     for r in range(P):
         sp = sharding.plan(wl.B, wl.H, wl.Hkv, P, r)
         ql, Kl, Vl, sl = sharding.local_inputs(sp, x["q_dec"], x["K"], x["V"], x["seq_len"])
-        o, _ = svl.fresh_decode_step(ql, Kl, Vl, sl, wl.vb, wl.nv, wl.k)
+        o, _ = svl.fresh_decode_step(ql, Kl, Vl, sl, wl.vb, wl.nv, wl.k, flags=pin)
         parts.append(o.clone())
         plans.append(sp)
     full = sharding.assemble(parts, plans, wl.B, wl.H)
@@ -141,17 +142,17 @@ def test_fresh_step_deterministic(svl):
 
 @pytest.mark.parametrize("pin", [None, "16"])
 @pytest.mark.parametrize("B,nv", [(2, 32768), (8, 32768), (8, 24576)])
-def test_fresh_step_many_units(svl, orc, B, nv, pin, monkeypatch):
+def test_fresh_step_many_units(svl, orc, B, nv, pin):
     """More clusters than fit at once (later clusters start on SMs vacated by earlier
     ones): this exposed the text-row / ring-slot parity race fixed in fused.cu (the
     text rows now have their own buffer and barrier); run twice back to back."""
-    if pin:  # force the fused kernel into a multi-wave launch (the planner would take two calls)
-        monkeypatch.setenv("SVL_FRESH_CS", pin)
+    # pin: force the fused kernel into a multi-wave launch (the planner would take two calls)
+    xf = svl.SVL_PIN_SPLITS(int(pin)) if pin else 0
     base = gen.CONFIGS["long-video"]
     wl = gen.DecodeWorkload(**{**base.__dict__, "name": f"mu{B}", "B": B, "nv": nv, "k": nv // 10,
                                "seq_lens": None})
-    _run(svl, orc, wl, seed=40 + B)
-    _run(svl, orc, wl, seed=41 + B)
+    _run(svl, orc, wl, seed=40 + B, xflags=xf)
+    _run(svl, orc, wl, seed=41 + B, xflags=xf)
 
 
 def test_multi_turn_eviction_is_a_seq_len_rollback(svl):

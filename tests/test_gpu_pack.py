@@ -50,7 +50,7 @@ def test_pack_bad_indices_flagged(svl):
     idx = torch.arange(wl.k, dtype=torch.int32, device="cuda").expand(wl.B, wl.Hkv, wl.k).contiguous().clone()
     idx[0, 0, 3] = idx[0, 0, 2]  # not strictly ascending
     ws = svl.Workspace()
-    ws.get(256)
+    ws.get(1024)
     ws.reset_flags()
     svl.pack_kv(x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx, ws=ws)
     assert ws.flags() & svl.SVL_DEVFLAG_INDEX

@@ -53,7 +53,7 @@ def test_rope_remap_bad_kept_flagged(svl):
     K, V, kept, seq = _case(1, 1, 64, 4, 64, 8, 16, seed=3)
     kept[0, 5] = kept[0, 4]
     ws = svl.Workspace()
-    ws.get(256)
+    ws.get(1024)
     ws.reset_flags()
     svl.rope_remap(K.cuda(), None, seq.cuda(), 4, 64, kept.cuda(), 10000.0, ws=ws)
     assert ws.flags() & svl.SVL_DEVFLAG_INDEX

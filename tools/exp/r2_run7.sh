@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm --format=csv
+(timeout 200 python tools/trace_decode.py long-video
+ timeout 200 python tools/trace_decode.py multi-turn
+ timeout 300 python tools/exp/decode_bench.py base) > gpurun_out/r2_trace7.txt 2>&1
+cat gpurun_out/r2_trace7.txt

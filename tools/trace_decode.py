@@ -1,33 +1,59 @@
-"""Phase timeline of the split decode kernel (SVL_TRACE=1 stamps), cold L2 (28 rotating layers).
-usage: python tools/trace_decode.py [config]"""
-import os, sys
-os.environ["SVL_TRACE"] = "1"
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-from paper_2510_17777_b200 import inputs as gen, svl
+"""Phase timeline of the steady decode kernel (svl_sparse_decode_attn), from
+globaltimer stamps of a SVL_TRACE_BUILD library (built here as build/trace/),
+cold L2 (28 rotating layers, the last one traced).
+usage: python tools/trace_decode.py [config] [pin]"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+if "SVL_LIB" not in os.environ:
+    env = dict(os.environ, SVL_VARIANT="trace", SVL_DEFS="-DSVL_TRACE_BUILD=1")
+    subprocess.run([sys.executable, "-m", "paper_2510_17777_b200.build"], cwd=ROOT, env=env, check=True,
+                   stdout=subprocess.DEVNULL)
+    os.environ["SVL_LIB"] = os.path.join(ROOT, "build", "trace", "libsparsevila.so")
+import torch  # noqa: E402
+
+from paper_2510_17777_b200 import inputs as gen, svl  # noqa: E402
+
 name = sys.argv[1] if len(sys.argv) > 1 else "long-video"
+pin = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+flags = svl.SVL_PIN_SPLITS(pin) if pin else 0
 wl = gen.CONFIGS[name]
-NL = 28
+NL = 28 if wl.B * wl.nv <= 65536 else 3
 xs = [gen.make_decode_inputs(wl, seed=s, device="cuda") for s in range(NL)]
 idx = [svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k).clone() for x in xs]
+base = svl.sparse_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity, flags)
 ws = svl.Workspace()
-ws.get(svl.sparse_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
-for rep in range(2):
+ws.get(base + (1 << 20))
+tr_view = ws.buf[ws.buf.numel() - (1 << 20):]
+# ~1 s of back-to-back copies first: the SM clock ramps up from idle under load
+# (a copy, not a GEMM: a power-capped GEMM leaves the clock low)
+a = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+b = torch.empty_like(a)
+for _ in range(2000):
+    b.copy_(a)
+for rep in range(3):
     for i in range(NL):
         x = xs[i]
-        if i == NL - 1:
-            ws.buf[256:256 + (1 << 20)].zero_()
-        svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx[i], ws=ws)
+        if rep == 2 and i == NL - 1:
+            tr_view.zero_()
+        svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx[i], flags=flags, ws=ws)
 torch.cuda.synchronize()
-tr = ws.buf[256:256 + (1 << 20)].view(torch.int64)[: 4096 * 16].view(-1, 16).cpu()
+tr = tr_view.view(torch.int64)[: 4096 * 16].view(-1, 16).cpu()
 tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
-names = {0: "start", 1: "batch0 ready", 2: "batch1 ready", 3: "batch2 ready", 10: "compute done", 11: "partial",
-         12: "cl.sync", 13: "merge", 14: "end"}
-print(f"{name} decode: {tr.shape[0]} CTAs (us from first start: min / median / max)")
+clk = (tr[:, 15] - tr[:, 14]).double() / (tr[:, 7] - tr[:, 0]).double() * 1e3
+print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {clk.median():.0f} MHz")
+names = {0: "start", 1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 10: "b0 scores+max",
+         11: "b0 P table", 4: "compute done", 5: "partial stored", 8: "merge loads (polled)",
+         9: "merge weights", 7: "merged"}
+print(f"{name} decode pin={pin}: {tr.shape[0]} CTAs (us from first start: min / median / max)")
 for ph, nm in names.items():
     col = tr[:, ph]
-    if (col == 0).any():
+    col = col[col > 0]
+    if col.numel() == 0:
         continue
     v = (col - t0).double() / 1e3
-    print(f"  {ph:2d} {nm:14s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
+    print(f"  {ph:2d} {nm:20s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")

@@ -15,10 +15,10 @@ for rep in range(2):
     for it in range(NL):
         x = xs[it]
         if it == NL - 1:
-            ws.buf[256:256 + (1 << 20)].zero_()
+            ws.buf[1024:1024 + (1 << 20)].zero_()
         svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k, ws=ws)
 torch.cuda.synchronize()
-tr = ws.buf[256:256 + (1 << 20)].view(torch.int64)[: 2048 * 64].view(-1, 64).cpu()
+tr = ws.buf[1024:1024 + (1 << 20)].view(torch.int64)[: 2048 * 64].view(-1, 64).cpu()
 tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
 names = {0: "start", 1: "stream+textV", 2: "lse", 3: "hist+thr", 4: "select", 5: "Ptab+Vwait", 6: "PV", 7: "O+l",
