@@ -475,6 +475,9 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     p.shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
     p.capacity = K.capacity;
     p.S = S;
+    // rows of one split <= ceil(vb / S) + ceil(k / S) + ceil(T_max / S) (three segments)
+    p.single_batch = ((span.visual_begin + S - 1) / S + (k + S - 1) / S +
+                      (std::max(0, K.capacity - span.visual_begin - span.visual_len) + S - 1) / S) <= kDecodeRowsMax;
     p.scale2 = scale * kLog2e;
     p.out = out;
     p.lse_out = lse_out;

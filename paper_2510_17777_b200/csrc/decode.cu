@@ -42,23 +42,20 @@ constexpr int NTH = kDecodeThreads;  // 256: 8 warps
 constexpr int NW = NTH / 32;
 constexpr int RB = kDecodeRowsMax;   // 128 rows per batch = 8 warps x one 16-row tile
 static_assert(RB == 16 * NW, "one 16-row tile per warp and batch");
-#ifndef SVL_DECODE_NBUF
-#define SVL_DECODE_NBUF 3
-#endif
-constexpr int NBUF = SVL_DECODE_NBUF;  // gather buffers: NBUF - 1 batches in flight while one is computed
-static_assert(NBUF >= 2 && (NBUF - 1) * RB <= NTH, "prologue: one row id per thread");
-
-template <int D>
+// NB = gather buffers: NB - 1 batches in flight while one is computed.  NB = 1 when every
+// CTA has a single batch (B = 1 shapes): 66 KB of shared memory, so the next launch's CTAs
+// (programmatic dependent launch) are resident while this grid runs; NB = 3 otherwise.
+template <int D, int NB>
 struct DecodeSmem {
+    static_assert(NB >= 1 && (NB - 1) * RB <= NTH, "prologue: one row id per thread");
     static constexpr int ROW_BYTES = D * 2;
-    static constexpr int BUF_BYTES = 2 * RB * ROW_BYTES;        // K + V of one batch
-    static constexpr int ROWS_OFF = NBUF * BUF_BYTES;            // row ids [NBUF][RB]
-    static constexpr int TRED_OFF = ROWS_OFF + NBUF * RB * 4;    // tile max / sum [2][NW][16] fp32
-    static constexpr int PT_OFF = TRED_OFF + 2 * NW * 16 * 4;    // P hi + lo [RB][16] bf16
-    static constexpr int RUN_OFF = PT_OFF + 2 * RB * 16 * 2;     // running M[16], l[16]
-    static constexpr int BYTES = RUN_OFF + 32 * 4;
-    // merge staging (the gather buffers are free by then)
-    static constexpr int MRG_FLOATS = BUF_BYTES / 4;
+    static constexpr int BUF_BYTES = 2 * RB * ROW_BYTES;           // K + V of one batch
+    static_assert(NB * BUF_BYTES >= NW * 16 * D * 4, "cross-warp merge staging fits the gather buffers");
+    static constexpr int ROWS_OFF = NB * BUF_BYTES;                 // row ids [NB][RB]
+    static constexpr int WML_OFF = ROWS_OFF + NB * RB * 4;          // per-warp m, l [2][NW][16] fp32
+    static constexpr int RUN_OFF = WML_OFF + 2 * NW * 16 * 4;       // CTA M[16], l[16]
+    static constexpr int SC_OFF = RUN_OFF + 32 * 4;                 // warp scales [NW][16]
+    static constexpr int BYTES = SC_OFF + NW * 16 * 4;
 };
 
 // swizzles (physical 16-byte chunk within a row)
@@ -95,36 +92,33 @@ SVL_DEV uint32_t ld_relaxed_u32(const uint32_t* p) {
     return v;
 }
 
-template <int D>
+template <int D, int NBUF>
 __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
-    using SM = DecodeSmem<D>;
+    using SM = DecodeSmem<D, NBUF>;
     constexpr int CH = D / 8;    // 16-byte chunks per row
     constexpr int NCH = D / 32;  // chunks per thread per row in the permuted-k layout
     extern __shared__ __align__(128) uint8_t smem[];
     const int S = (int)gridDim.x, split = (int)blockIdx.x, u = (int)blockIdx.y;
     int* rows_s = reinterpret_cast<int*>(smem + SM::ROWS_OFF);  // [NBUF][RB]
-    float* tred = reinterpret_cast<float*>(smem + SM::TRED_OFF);
-    uint16_t* pth = reinterpret_cast<uint16_t*>(smem + SM::PT_OFF);  // [RB][16] P hi
-    uint16_t* ptl = pth + RB * 16;                                    // [RB][16] P lo
     float* run = reinterpret_cast<float*>(smem + SM::RUN_OFF);       // M[16], l[16]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gid = lane >> 2, t = lane & 3;
 #if SVL_TRACE_BUILD
     uint64_t* trace = p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
-    auto stamp = [&](int i) {
-        if (trace && tid == 0) {
-            uint64_t tnow;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-            trace[i] = tnow;
-        }
+    auto stamp = [&](int i) {  // SM cycles (clock64: exact within a CTA)
+        if (trace && tid == 0) trace[i] = clock64();
     };
 #else
     auto stamp = [](int) {};
 #endif
     stamp(0);
 #if SVL_TRACE_BUILD
-    if (trace && tid == 0) trace[14] = clock64();
+    if (trace && tid == 0) {
+        uint64_t tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        trace[14] = tnow;
+    }
 #endif
     // programmatic dependent launch: nothing an upstream kernel may write (seq_len,
     // idx, q, the appended K/V row) is read before the wait
@@ -211,11 +205,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     // ---- prologue: row ids of batches [0, NBUF - 1) (one per thread), their gathers, and
     // the idx loads of batch NBUF - 1 (consumed at the top of iteration 0)
     if (tid < (NBUF - 1) * RB) rows_s[tid] = resolve(tid, pre);
-    Pending pend = tid < RB ? fetch((NBUF - 1) * RB + tid) : Pending{0, -1};
-    if (tid < 16) {
-        run[tid] = -INFINITY;
-        run[16 + tid] = 0.f;
-    }
+    Pending pend = tid < RB ? (NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid)) : Pending{0, -1};
     cta_sync();
     stamp(2);
     for (int j = 0; j < NBUF - 1; ++j) issue(j);
@@ -238,8 +228,16 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         }
     }
 
-    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    static_assert(D / 16 <= NW, "one warp per 16 output columns");
+    // FlashAttention-2 style per warp: warp w owns rows [16 w, 16 w + 16) of every batch,
+    // scores them, keeps a running max per head, and multiplies P (still in registers: the
+    // two n-tiles of the score accumulator ARE the A fragment of a k16 MMA) into its own
+    // O[16 heads][D] -- no per-batch CTA barrier beyond the buffer hand-over.
+    constexpr int NTO = D / 8;  // output n-tiles
+    float o[NTO][4];
+#pragma unroll
+    for (int i = 0; i < NTO; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_a = -INFINITY, m_b = -INFINITY;  // running max of heads gid, gid + 8 (quad-uniform)
+    float l_a = 0.f, l_b = 0.f;              // this thread's share of the running sums
 
     for (int j = 0; j < nb; ++j) {
         // row ids of batch j + NBUF - 1 (loads issued one iteration ago), then the loads of
@@ -258,142 +256,146 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         const uint32_t sK = smem_u32(smem + (j % NBUF) * SM::BUF_BYTES);
         const uint32_t sV = sK + RB * SM::ROW_BYTES;
         const int nj = min(RB, n - j * RB);
-        const int nr = (nj + 15) & ~15;  // rows padded to whole 16-row tiles
         const int tb = warp * 16;
-        const int ntl = nr >> 4;
+        if (tb >= nj) continue;  // (warp-uniform) no rows of this warp in the batch
         float s[2][4];  // n-tile nt: c0, c1 -> head gid, rows tb + 8nt + 2t, +1; c2, c3 -> head gid + 8
-        if (tb < nr) {
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-                const int r = tb + nt * 8 + gid;
+        for (int nt = 0; nt < 2; ++nt) {
+            s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+            const int r = tb + nt * 8 + gid;
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) {
-                    const uint4 kc = lds128(sK + r * SM::ROW_BYTES + swz_k(r, t + 4 * i) * 16);
-                    {
-                        const uint32_t a[4] = {qa[i].x, qb[i].x, qa[i].y, qb[i].y};
-                        mma_bf16_16816(s[nt], a, kc.x, kc.y);
-                    }
-                    {
-                        const uint32_t a[4] = {qa[i].z, qb[i].z, qa[i].w, qb[i].w};
-                        mma_bf16_16816(s[nt], a, kc.z, kc.w);
-                    }
+            for (int i = 0; i < NCH; ++i) {
+                const uint4 kc = lds128(sK + r * SM::ROW_BYTES + swz_k(r, t + 4 * i) * 16);
+                {
+                    const uint32_t a[4] = {qa[i].x, qb[i].x, qa[i].y, qb[i].y};
+                    mma_bf16_16816(s[nt], a, kc.x, kc.y);
+                }
+                {
+                    const uint32_t a[4] = {qa[i].z, qb[i].z, qa[i].w, qb[i].w};
+                    mma_bf16_16816(s[nt], a, kc.z, kc.w);
                 }
             }
-            float mx_a = -INFINITY, mx_b = -INFINITY;
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int rr = tb + nt * 8 + 2 * t + (e & 1);
-                    const int h = gid + 8 * (e >> 1);
-                    s[nt][e] = (rr < nj && rows[rr] >= 0 && h < p.g) ? s[nt][e] * p.scale2 : -INFINITY;
-                    if (e < 2) mx_a = fmaxf(mx_a, s[nt][e]);
-                    else mx_b = fmaxf(mx_b, s[nt][e]);
-                }
-            mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
-            mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
-            mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
-            mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
-            if (t == 0) {
-                tred[warp * 16 + gid] = mx_a;
-                tred[warp * 16 + gid + 8] = mx_b;
-            }
         }
-        cta_sync();
-        if (j == 0) stamp(10);
-        // batch max of heads gid, gid + 8 (every thread, same fixed order) -> new running max
-        float bm_a = -INFINITY, bm_b = -INFINITY;
-        for (int w = 0; w < ntl; ++w) {
-            bm_a = fmaxf(bm_a, tred[w * 16 + gid]);
-            bm_b = fmaxf(bm_b, tred[w * 16 + gid + 8]);
-        }
-        const float mo_a = run[gid], mo_b = run[gid + 8];
-        const float mn_a = fmaxf(mo_a, bm_a), mn_b = fmaxf(mo_b, bm_b);
-        if (tb < nr) {
-            // P = exp2(s - M) into the split bf16 table; tile sums of the weights the PV uses
-            float ls_a = 0.f, ls_b = 0.f;
+        float mx_a = -INFINITY, mx_b = -INFINITY;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float mn = (e < 2) ? mn_a : mn_b;
-                    const float pv = (s[nt][e] == -INFINITY) ? 0.f : fast_exp2(s[nt][e] - mn);
-                    const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
-                    const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
-                    const int rr = tb + nt * 8 + 2 * t + (e & 1), h = gid + 8 * (e >> 1);
-                    pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
-                    ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
-                    const float w = __bfloat162float(hi) + __bfloat162float(lo);
-                    if (e < 2) ls_a += w;
-                    else ls_b += w;
-                }
-            ls_a += __shfl_xor_sync(0xffffffffu, ls_a, 1);
-            ls_a += __shfl_xor_sync(0xffffffffu, ls_a, 2);
-            ls_b += __shfl_xor_sync(0xffffffffu, ls_b, 1);
-            ls_b += __shfl_xor_sync(0xffffffffu, ls_b, 2);
-            if (t == 0) {
-                tred[NW * 16 + warp * 16 + gid] = ls_a;
-                tred[NW * 16 + warp * 16 + gid + 8] = ls_b;
+            for (int e = 0; e < 4; ++e) {
+                const int rr = tb + nt * 8 + 2 * t + (e & 1);
+                const int h = gid + 8 * (e >> 1);
+                s[nt][e] = (rr < nj && rows[rr] >= 0 && h < p.g) ? s[nt][e] * p.scale2 : -INFINITY;
+                if (e < 2) mx_a = fmaxf(mx_a, s[nt][e]);
+                else mx_b = fmaxf(mx_b, s[nt][e]);
             }
-        }
-        cta_sync();
-        if (j == 0) stamp(11);
-        if (tid < 16) {  // running (M, l) of head tid; fixed tile order
-            const float mo = run[tid];
-            float mn = mo, ls = 0.f;
-            for (int w = 0; w < ntl; ++w) {
-                mn = fmaxf(mn, tred[w * 16 + tid]);
-                ls += tred[NW * 16 + w * 16 + tid];
+        mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
+        mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
+        mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
+        mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
+        const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
+        const float al_a = (mn_a == -INFINITY) ? 1.f : fast_exp2(m_a - mn_a);
+        const float al_b = (mn_b == -INFINITY) ? 1.f : fast_exp2(m_b - mn_b);
+        m_a = mn_a;
+        m_b = mn_b;
+        // P = exp2(s - M) split into bf16 hi + lo, packed straight into A fragments:
+        // a0 = (head gid, rows 2t, 2t+1), a1 = (gid + 8, ...), a2 / a3 = the same for rows + 8
+        uint32_t ph[4], plo[4];
+        float ls_a = 0.f, ls_b = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int hb = 0; hb < 2; ++hb) {
+                const float mn = hb ? mn_b : mn_a;
+                const float p0 = (s[nt][2 * hb] == -INFINITY) ? 0.f : fast_exp2(s[nt][2 * hb] - mn);
+                const float p1 = (s[nt][2 * hb + 1] == -INFINITY) ? 0.f : fast_exp2(s[nt][2 * hb + 1] - mn);
+                const uint32_t hw = pack_bf16(p0, p1);
+                const uint32_t lw = pack_bf16(p0 - bf16lo(hw), p1 - bf16hi(hw));
+                ph[2 * nt + hb] = hw;
+                plo[2 * nt + hb] = lw;
+                const float w = bf16lo(hw) + bf16lo(lw) + bf16hi(hw) + bf16hi(lw);
+                if (hb) ls_b += w;
+                else ls_a += w;
             }
-            const float al = (mn == -INFINITY) ? 1.f : fast_exp2(mo - mn);
-            run[16 + tid] = run[16 + tid] * al + ls;
-            run[tid] = mn;
-        }
-        const float al_a = (mn_a == -INFINITY) ? 1.f : fast_exp2(mo_a - mn_a);
-        const float al_b = (mn_b == -INFINITY) ? 1.f : fast_exp2(mo_b - mn_b);
-        if (warp < D / 16) {
-            // rescale this warp's accumulator rows (heads gid, gid + 8), then O += P V
+        l_a = l_a * al_a + ls_a;
+        l_b = l_b * al_b + ls_b;
+        // O = O * al + P V over the warp's 16 rows: V B-fragments by ldmatrix.trans, two
+        // output n-tiles per load; all 2 x NTO MMAs independent
+        const int mi = lane >> 3, rin = lane & 7;
+        const int vrow = tb + (mi & 1) * 8 + rin;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                o[nt][0] *= al_a; o[nt][1] *= al_a;
-                o[nt][2] *= al_b; o[nt][3] *= al_b;
+        for (int cp = 0; cp < NTO / 2; ++cp) {
+            uint32_t v0, v1, v2, v3;
+            ldsm_x4_trans(sV + vrow * SM::ROW_BYTES + swz_v(vrow, 2 * cp + (mi >> 1)) * 16, v0, v1, v2, v3);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                float* oo = o[2 * cp + h2];
+                oo[0] *= al_a; oo[1] *= al_a;
+                oo[2] *= al_b; oo[3] *= al_b;
+                const uint32_t b0 = h2 ? v2 : v0, b1 = h2 ? v3 : v1;
+                mma_bf16_16816(o[2 * cp + h2], ph, b0, b1);
+                mma_bf16_16816(o[2 * cp + h2], plo, b0, b1);
             }
-            const int mi = lane >> 3, rin = lane & 7;
-            const uint32_t aph = smem_u32(pth), apl = smem_u32(ptl);
-            // k-steps of 16 rows; the hi and lo products go to separate accumulators (two
-            // independent MMA chains per n-tile), summed once after the batch
-            float ol[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-            for (int tt = 0; tt < RB; tt += 16) {
-                if (tt < nr) {
-                    // P fragment (m = heads, k = rows): matrices (h0-7,k0-7) (h8-15,k0-7) (h0-7,k8-15) (h8-15,k8-15)
-                    const int prow = tt + (mi >> 1) * 8 + rin;
-                    uint32_t ph[4], pl4[4];
-                    ldsm_x4_trans(aph + prow * 32 + (mi & 1) * 16, ph[0], ph[1], ph[2], ph[3]);
-                    ldsm_x4_trans(apl + prow * 32 + (mi & 1) * 16, pl4[0], pl4[1], pl4[2], pl4[3]);
-                    const int vrow = tt + (mi & 1) * 8 + rin;
-                    const int c = 2 * warp + (mi >> 1);
-                    uint32_t v0, v1, v2, v3;
-                    ldsm_x4_trans(sV + vrow * SM::ROW_BYTES + swz_v(vrow, c) * 16, v0, v1, v2, v3);
-                    mma_bf16_16816(o[0], ph, v0, v1);
-                    mma_bf16_16816(ol[0], pl4, v0, v1);
-                    mma_bf16_16816(o[1], ph, v2, v3);
-                    mma_bf16_16816(ol[1], pl4, v2, v3);
-                }
-            }
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) o[nt][e] += ol[nt][e];
         }
     }
     cp_async_wait<0>();
-    cta_sync();  // run[] final (also when this CTA had no rows); the gather buffers are free
+    cta_sync();  // every warp's batches done; the gather buffers are free
     stamp(4);
+
+    // ---- cross-warp merge inside the CTA (shared memory, the gather buffers): each warp's
+    // (m, l, O) rescaled to the CTA max; the result is the CTA's partial (o, M, l)
+    float* wml = reinterpret_cast<float*>(smem + SM::WML_OFF);   // [2][NW][16] m, l
+    float* wsc = reinterpret_cast<float*>(smem + SM::SC_OFF);    // [NW][16] exp2(m_w - M)
+    float* wo = reinterpret_cast<float*>(smem);                   // [NW][16][D]
+    {
+        l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+        l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+        l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+        l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+        if (t == 0) {
+            wml[warp * 16 + gid] = m_a;
+            wml[warp * 16 + gid + 8] = m_b;
+            wml[NW * 16 + warp * 16 + gid] = l_a;
+            wml[NW * 16 + warp * 16 + gid + 8] = l_b;
+        }
+        // column swizzle c ^ 8 (h & 3): the 8 heads a warp's quarter-groups store land in
+        // distinct banks (row stride D is a multiple of 32 words: 8-way conflicts otherwise)
+#pragma unroll
+        for (int i = 0; i < NTO; ++i) {
+            const int col = (i * 8 + 2 * t) ^ ((gid & 3) << 3);
+            if (gid < p.g) *reinterpret_cast<float2*>(wo + (warp * 16 + gid) * D + col) = make_float2(o[i][0], o[i][1]);
+            if (gid + 8 < p.g)
+                *reinterpret_cast<float2*>(wo + (warp * 16 + gid + 8) * D + col) = make_float2(o[i][2], o[i][3]);
+        }
+    }
+    cta_sync();
+    if (tid < 16) {  // CTA max, warp scales and sum of head tid (fixed warp order)
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, wml[w * 16 + tid]);
+        float l = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float mw = wml[w * 16 + tid];
+            const float sc = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
+            wsc[w * 16 + tid] = sc;
+            l += sc * wml[NW * 16 + w * 16 + tid];
+        }
+        run[tid] = M;
+        run[16 + tid] = l;
+    }
+    cta_sync();
+    // item (h, c) of the CTA partial: the warps' O rescaled to the CTA max, summed in warp order
+    auto cta_o = [&](int h, int c) -> float {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc += wsc[w * 16 + h] * wo[(w * 16 + h) * D + (c ^ ((h & 3) << 3))];
+        return acc;
+    };
 
     constexpr int PSTRIDE = kDecodePartStride<D>;
     auto finalize = [&](int h, int dd, float ov, float M, float den) {
+#if SVL_EXP_NOFINAL  // timing experiment: no output stores
+        if (ov != 12345.f) return;
+#endif
         const int hh = G * p.g + h;
         if (p.out) p.out[((int64_t)b * p.H + hh) * D + dd] = ov;
         if (dd == 0 && p.lse_out)
@@ -404,30 +406,19 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         }
     };
     if (S == 1) {
-        if (warp < D / 16) {
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int h = gid + 8 * (e >> 1), dd = warp * 16 + nt * 8 + 2 * t + (e & 1);
-                    if (h < p.g) {
-                        const float den = run[16 + h];
-                        finalize(h, dd, den > 0.f ? o[nt][e] / den : 0.f, run[h], den);
-                    }
-                }
+        for (int i = tid; i < p.g * D; i += NTH) {
+            const int h = i / D, c = i % D;
+            const float den = run[16 + h];
+            finalize(h, c, den > 0.f ? cta_o(h, c) / den : 0.f, run[h], den);
         }
     } else {
         // Partial (o, M, l) of this split -> workspace slot (u, split), every value stored as a
         // 64-bit (bits, tag) pair with one single-copy-atomic store; tag = the unit's call
         // epoch.  A reader that sees the tag sees the value: no barrier, no flag round trip.
         uint64_t* mine = p.part + (int64_t)(u * S + split) * PSTRIDE;
-        if (warp < D / 16) {
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int col = warp * 16 + nt * 8 + 2 * t;
-                if (gid < p.g) st_tagged2(mine + gid * D + col, o[nt][0], o[nt][1], tag);
-                if (gid + 8 < p.g) st_tagged2(mine + (gid + 8) * D + col, o[nt][2], o[nt][3], tag);
-            }
+        for (int i = 2 * tid; i < p.g * D; i += 2 * NTH) {
+            const int h = i / D, c = i % D;
+            st_tagged2(mine + i, cta_o(h, c), cta_o(h, c + 1), tag);
         }
         if (tid < 32) st_tagged(mine + 16 * D + tid, run[tid], tag);  // M[16], l[16]
         stamp(5);
@@ -441,7 +432,6 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             float* ob = reinterpret_cast<float*>(smem);  // [S][ni]
             float* mb = ob + S * ni;                     // [S][nh] m, then the weights
             float* lb = mb + S * nh;                     // [S][nh]
-            float* hM = lb + S * nh;                     // [nh] M, den
             const uint64_t* up = p.part + (int64_t)u * S * PSTRIDE;
             constexpr int MAXL = (16 * D + kDecodeMaxSplits + NTH - 1) / NTH;  // S * ni <= g D + S
             uint64_t v[MAXL], vm[2], vl[2];  // S * nh <= max(2 S, S + 16) <= 2 NTH
@@ -494,44 +484,35 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             }
             cta_sync();
             stamp(8);
-            for (int hh = warp; hh < nh; hh += NW) {  // per head: M, weights, den (lanes over splits)
-                float M = -INFINITY;
-                for (int q = lane; q < S; q += 32) M = fmaxf(M, mb[q * nh + hh]);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-                float den = 0.f;
-                for (int q = lane; q < S; q += 32) {
-                    const float w = (M == -INFINITY) ? 0.f : fast_exp2(mb[q * nh + hh] - M);
-                    mb[q * nh + hh] = w;
-                    den += w * lb[q * nh + hh];
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-                if (lane == 0) {
-                    hM[2 * hh] = M;
-                    hM[2 * hh + 1] = den;
-                }
-            }
-            cta_sync();
-            stamp(9);
-            // per item: T threads (a power of two <= 32) stride over the splits, then a
-            // fixed xor tree inside the T-lane group; every lane takes part in the shuffles
+            // per item: T threads (a power of two <= 32) stride over the splits -- max, then the
+            // weighted sums of o and l -- with fixed xor trees inside the T-lane group
             int T = 32;
             while (T > 1 && T * ni > 2 * NTH) T >>= 1;
             for (int jb = 0; jb < ni; jb += NTH / T) {
                 const int j = jb + tid / T, sub = tid & (T - 1);
                 const int hh = (j < ni) ? (i0 + j) / D - h0 : 0;
-                float num = 0.f;
+                float M = -INFINITY;
                 if (j < ni) {
 #pragma unroll 4
-                    for (int q = sub; q < S; q += T) num += mb[q * nh + hh] * ob[q * ni + j];
+                    for (int q = sub; q < S; q += T) M = fmaxf(M, mb[q * nh + hh]);
                 }
-                for (int off = T >> 1; off > 0; off >>= 1) num += __shfl_xor_sync(0xffffffffu, num, off);
-                if (sub == 0 && j < ni) {
-                    const float den = hM[2 * hh + 1];
-                    finalize(h0 + hh, (i0 + j) % D, (den > 0.f) ? num / den : 0.f, hM[2 * hh], den);
+                for (int off = T >> 1; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+                float num = 0.f, den = 0.f;
+                if (j < ni && M != -INFINITY) {
+#pragma unroll 4
+                    for (int q = sub; q < S; q += T) {
+                        const float w = fast_exp2(mb[q * nh + hh] - M);
+                        num += w * ob[q * ni + j];
+                        den += w * lb[q * nh + hh];
+                    }
                 }
+                for (int off = T >> 1; off > 0; off >>= 1) {
+                    num += __shfl_xor_sync(0xffffffffu, num, off);
+                    den += __shfl_xor_sync(0xffffffffu, den, off);
+                }
+                if (sub == 0 && j < ni) finalize(h0 + hh, (i0 + j) % D, (den > 0.f) ? num / den : 0.f, M, den);
             }
+            stamp(9);
         }
         // split 0 advances the unit's epoch once its own merge has seen every split's
         // partial -- so every CTA of the unit has read the current epoch already
@@ -539,7 +520,11 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     }
     stamp(7);
 #if SVL_TRACE_BUILD
-    if (trace && tid == 0) trace[15] = clock64();
+    if (trace && tid == 0) {
+        uint64_t tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        trace[15] = tnow;
+    }
 #endif
     // push variant: the grid's last CTA publishes the epoch flags once every CTA's peer
     // stores are fenced at system scope (self-resetting counter, header word 3)
@@ -578,23 +563,23 @@ __global__ void wait_flags_kernel(const uint32_t* flags, int P, uint32_t epoch, 
     }
 }
 
-template <int D>
+template <int D, int NB>
 cudaError_t prepare_decode_t() {
-    using SM = DecodeSmem<D>;
+    using SM = DecodeSmem<D, NB>;
     static bool attr_done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && attr_done[dev]) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
-    if (e == cudaSuccess) e = set_max_carveout(decode_kernel<D>);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+    if (e == cudaSuccess) e = set_max_carveout(decode_kernel<D, NB>);
     if (e == cudaSuccess && dev < 64) attr_done[dev] = true;
     return e;
 }
 
-template <int D>
+template <int D, int NB>
 cudaError_t launch_decode_t(const DecodeParams& p, cudaStream_t s) {
-    using SM = DecodeSmem<D>;
-    cudaError_t e = prepare_decode_t<D>();
+    using SM = DecodeSmem<D, NB>;
+    cudaError_t e = prepare_decode_t<D, NB>();
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.S, p.B * p.Hkv);
@@ -604,29 +589,21 @@ cudaError_t launch_decode_t(const DecodeParams& p, cudaStream_t s) {
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see griddepcontrol in the kernel
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    // the grid barrier needs every CTA resident: the grid is sized to the co-resident count,
-    // and a cooperative launch makes the runtime guarantee it
+    // the merge polls other CTAs' partials: every CTA must be resident -- the grid is sized
+    // to the co-resident count, and a cooperative launch makes the runtime guarantee it
     attr[1].id = cudaLaunchAttributeCooperative;
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-#if SVL_DECODE_NO_COOP  // A/B builds: co-residency by grid sizing alone
-    cfg.numAttrs = 1;
-#else
     cfg.numAttrs = p.S > 1 ? 2 : 1;
-#endif
-#if SVL_DECODE_NO_PDL  // A/B builds
-    attr[0] = attr[1];
-    cfg.numAttrs -= 1;
-#endif
-    return cudaLaunchKernelEx(&cfg, decode_kernel<D>, p);
+    return cudaLaunchKernelEx(&cfg, decode_kernel<D, NB>, p);
 }
 
 template <int D>
 int decode_ctas_per_sm_t() {
-    if (prepare_decode_t<D>() != cudaSuccess) return 0;
+    using SM = DecodeSmem<D, 3>;
+    if (prepare_decode_t<D, 3>() != cudaSuccess) return 0;
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<D>, NTH, DecodeSmem<D>::BYTES) !=
-        cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel<D, 3>, NTH, SM::BYTES) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -641,9 +618,8 @@ cudaError_t launch_wait_flags(const uint32_t* flags, int P, uint32_t epoch, uint
 }
 
 cudaError_t launch_decode(const DecodeParams& p, int d, cudaStream_t s) {
-    if (d == 128) return launch_decode_t<128>(p, s);
-    if (d == 64) return launch_decode_t<64>(p, s);
-    return cudaErrorInvalidValue;
+    if (p.single_batch) return d == 128 ? launch_decode_t<128, 1>(p, s) : launch_decode_t<64, 1>(p, s);
+    return d == 128 ? launch_decode_t<128, 3>(p, s) : launch_decode_t<64, 3>(p, s);
 }
 
 int decode_ctas_per_sm(int d) {

@@ -63,7 +63,8 @@ struct DecodeParams {
     const int32_t* seq_len;
     const int32_t* idx;  // [B][U][k]
     int B, H, Hkv, g, vb, nv, k, shared, capacity;
-    int S;         // splits (CTAs) per unit; the grid (S x units) is co-resident
+    int S;             // splits (CTAs) per unit; the grid (S x units) is co-resident
+    int single_batch;  // every split has <= kDecodeRowsMax rows (host bound): one gather buffer
     float scale2;  // scale * log2(e)
     float* out;    // [B][H][d]
     float* lse_out;

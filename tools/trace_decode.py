@@ -43,17 +43,17 @@ for rep in range(3):
 torch.cuda.synchronize()
 tr = tr_view.view(torch.int64)[: 4096 * 16].view(-1, 16).cpu()
 tr = tr[tr[:, 0] > 0]
-t0 = tr[:, 0].min()
-clk = (tr[:, 15] - tr[:, 14]).double() / (tr[:, 7] - tr[:, 0]).double() * 1e3
-print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {clk.median():.0f} MHz")
-names = {0: "start", 1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 10: "b0 scores+max",
+# stamps 0..13: SM cycles (clock64) of the CTA; 14 / 15: globaltimer at start / end
+f_ghz = ((tr[:, 7] - tr[:, 0]).double() / (tr[:, 15] - tr[:, 14]).double())
+print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {f_ghz.median() * 1e3:.0f} MHz")
+names = {1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 10: "b0 scores+max",
          11: "b0 P table", 4: "compute done", 5: "partial stored", 8: "merge loads (polled)",
          9: "merge weights", 7: "merged"}
-print(f"{name} decode pin={pin}: {tr.shape[0]} CTAs (us from first start: min / median / max)")
+print(f"{name} decode pin={pin}: {tr.shape[0]} CTAs; per-CTA cycles from its start -> us at its clock "
+      f"(min / median / max); kernel span {((tr[:, 15].max() - tr[:, 14].min()) / 1e3).item():.2f} us")
 for ph, nm in names.items():
-    col = tr[:, ph]
-    col = col[col > 0]
-    if col.numel() == 0:
+    ok = tr[:, ph] > 0
+    if not ok.any():
         continue
-    v = (col - t0).double() / 1e3
-    print(f"  {ph:2d} {nm:20s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
+    v = (tr[ok, ph] - tr[ok, 0]).double() / f_ghz[ok] / 1e3
+    print(f"  {ph:2d} {nm:22s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
