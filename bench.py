@@ -3,17 +3,27 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {svl,reference}]
 
-Step = one fresh-retrieval decode step of a 28-layer stack (NVILA-8B /
-Qwen2-7B depth) on the long-video workload (BASELINE.json configs[2]: 32768
-retained visual tokens, 512 + 256 text rows at the last of 256 generated
-tokens, k = keep_budget(32768, 0.90) = 3277, batch 1, 28 q / 4 KV heads,
-d = 128): per layer svl_retrieve (a1-a3) then svl_sparse_decode_attn (a4-a5)
-through the C ABI, replayed as one CUDA graph.  28 distinct layer KV caches
-(1.9 GB) rotate, so the working set is > L2 every step.
+N = 1 (default): the headline.  Step = one fresh-retrieval decode step of a
+28-layer stack (NVILA-8B / Qwen2-7B depth) on the long-video workload
+(BASELINE.json configs[2]: 32768 retained visual tokens, 512 + 256 text rows at
+the last of 256 generated tokens, k = keep_budget(32768, 0.90) = 3277, batch
+1, 28 q / 4 KV heads, d = 128): per layer ONE svl_fresh_decode_step (retrieve
+a1-a3 + sparse decode a4-a5 fused; fresh_kernel) through the C ABI, replayed
+as one CUDA graph.  28 distinct layer KV caches (1.9 GB) rotate, so the
+working set is > L2 every step.
+
+N > 1: `python bench.py --gpus N` re-launches itself under torch.distributed.run
+(one rank per GPU, NCCL).  Default there: the throughput-sweep config
+(BASELINE.json configs[4]: B 16, 65536 visual, k 6554) sharded over (batch x KV
+head) (sharding.plan), one svl_fresh_decode_step per layer per rank and one
+NCCL all-gather of the fp32 head outputs per layer, captured in the same CUDA
+graph: strong scaling; rank 0 also times the unsharded step on its GPU alone,
+so the line carries E(P) = T(1) / (P T(P)) with and without the gather.
+--mode replicas: every rank serves its own long-video request (weak scaling).
 
 value  = algorithmic HBM bytes of the step (scored visual
          K + selected K/V + text K/V once + q + out + idx) / step time, summed
-         over ranks (weak scaling: every rank serves its own request).
+         over ranks.
 e2e    = the same through the public API with host buffers: per step the
          new token's q and K/V rows go H2D from pinned memory, the graph
          replays, and the attention outputs come back D2H.
@@ -127,6 +137,45 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def quantile(xs, q):
+    ys = sorted(xs)
+    if not ys:
+        return None
+    pos = q * (len(ys) - 1)
+    lo = int(pos)
+    hi = min(lo + 1, len(ys) - 1)
+    return ys[lo] + (ys[hi] - ys[lo]) * (pos - lo)
+
+
+def replay_times(g, n):
+    """ms of each of n graph replays (CUDA events around every replay)."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for a, b in ev:
+        a.record()
+        g.replay()
+        b.record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def cold_layer_us(fn, n=30):
+    """Median us of one launch of fn() after a 2 x L2 write (cold L2, nothing in flight)."""
+    import torch
+    flush = torch.empty(2 * 126 * 2 ** 20, dtype=torch.uint8, device="cuda")
+    ts = []
+    for _ in range(n):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    del flush
+    return statistics.median(ts)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -159,43 +208,123 @@ def cpu_oracle_sample(wl, budget_s=12.0, nthreads=None):
     return nb * layers / t_total, layers, nthreads, t_total
 
 
+def kernel_src_sha(names=("fused.cu", "select_fast.cuh", "select_push.cuh", "common.cuh", "kernels.h")):
+    import hashlib
+    h = hashlib.sha256()
+    for n in names:
+        h.update(open(os.path.join(ROOT, "paper_2510_17777_b200", "csrc", n), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def fresh_traffic():
+    """dram bytes per fresh_kernel launch from the committed ncu capture, only while that
+    capture's kernel source hash matches the current source (else null)."""
+    tp = os.path.join(ROOT, "profiles", "ncu_fresh_traffic.json")
+    try:
+        d = json.load(open(tp))
+    except (OSError, ValueError):
+        return None, None
+    if d.get("src_sha") != kernel_src_sha():
+        return None, "stale: profiles/ncu_fresh_traffic.json was captured from another fresh_kernel source"
+    return d.get("dram_bytes_per_launch"), d.get("source")
+
+
+def config_rows(graph_of, timed):
+    """SURVEY.md 8(d) d2 rows beside the headline: per config the fresh step and the steady
+    decode per layer (CUDA graphs over rotating layer caches larger than L2) and the
+    per-round amortised step."""
+    import torch
+
+    from paper_2510_17777_b200 import inputs as gen
+    from paper_2510_17777_b200 import svl
+    out = {}
+    for name, nrot, round_len in (("nvila-4k", 77, ROUND_STEPS), ("multi-turn", LAYERS, 250)):
+        wl = gen.CONFIGS[name]
+        xs = [gen.make_decode_inputs(wl, seed=3000 + l, device="cuda") for l in range(nrot)]
+        idx = [torch.empty(wl.B, wl.Hkv, wl.k, dtype=torch.int32, device="cuda") for _ in range(nrot)]
+        outs = [torch.empty(wl.B, wl.H, wl.d, device="cuda") for _ in range(nrot)]
+        wsf, wsd = svl.Workspace(), svl.Workspace()
+        wsf.get(svl.fresh_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
+        wsd.get(svl.sparse_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
+        g_f = graph_of(lambda: [svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k,
+                                                      idx_out=i, out=o, ws=wsf) for x, i, o in zip(xs, idx, outs)])
+        g_d = graph_of(lambda: [svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, i,
+                                                       out=o, ws=wsd) for x, i, o in zip(xs, idx, outs)])
+        f_us = timed(g_f, 100, 10) * 1e3 / nrot
+        d_us = timed(g_d, 100, 10) * 1e3 / nrot
+        b = step_bytes(wl)
+        am = (f_us + (round_len - 1) * d_us) / round_len
+        out[name] = {"B": wl.B, "visual_tokens": wl.nv, "k": wl.k,
+                     "fresh_us_per_layer": f_us, "fresh_GB_s": b["total"] / (f_us * 1e-6) / 1e9,
+                     "fresh_path": "fused" if svl.fresh_uses_fused(wl.B, wl.H, wl.Hkv, wl.d, wl.nv, wl.capacity)
+                     else "two calls",
+                     "steady_us_per_layer": d_us, "steady_GB_s": b["decode"] / (d_us * 1e-6) / 1e9,
+                     "amortized_us_per_layer": am,
+                     "amortized_what": f"(1 fresh + {round_len - 1} steady) / {round_len} per round",
+                     "tokens_per_s_28_layers": wl.B / (am * 1e-6 * LAYERS),
+                     "rotating_layers": nrot}
+        del xs, g_f, g_d
+    return out
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args):
+    """The reference arm of this tier: the fp64 CPU oracle, as it stands, on the
+    box's host cores.  One step = `sample` whole layers of the long-video step
+    (retrieve + sparse decode), sized after timing one layer so that the whole
+    --steps K --warmup W run ends within ~2 minutes; ms_per_step is the measured
+    time of that step (no extrapolation) and config.layers says how many layers
+    a step holds."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2510_17777_b200 import inputs as gen
     wl = gen.CONFIGS[WORKLOAD]
     per_layer = step_bytes(wl)["total"]
-    # each step = a bounded sample (2 layers) of the 28-layer step
     import oracle
     x = gen.make_decode_inputs(wl, seed=0)
     nth = os.cpu_count() or 1
-    sample_layers = 2
 
-    def one():
-        for _ in range(sample_layers):
-            idx, _, _ = oracle.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k,
-                                        nthreads=nth)
-            oracle.sparse_decode(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx,
-                                 nthreads=nth)
+    def layer():
+        idx, _, _ = oracle.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k, nthreads=nth)
+        oracle.sparse_decode(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx, nthreads=nth)
 
+    t0 = time.perf_counter()
+    layer()
+    t_layer = time.perf_counter() - t0
+    sample = int(max(1, min(LAYERS, 120.0 / max(1, args.steps + args.warmup) / max(t_layer, 1e-6))))
     for _ in range(args.warmup):
-        one()
+        for _ in range(sample):
+            layer()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        one()
+        for _ in range(sample):
+            layer()
     dt = time.perf_counter() - t0
-    sec_per_layer = dt / (args.steps * sample_layers)
-    value = per_layer / sec_per_layer / 1e9
+    ms_step = dt * 1e3 / args.steps
+    value = per_layer * sample / (ms_step * 1e-3) / 1e9
+    cfg = config_dict(wl)
+    cfg["layers"] = sample
+    cfg["workload"] = f"{WORKLOAD}: {sample}-layer sample of the {LAYERS}-layer fresh-retrieval decode step"
     line = {
         "impl": "reference", "metric": "decode step HBM GB/s (retrieve+sparse attn) @32k visual tok",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": sec_per_layer * LAYERS * 1e3,
+        "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(wl),
+        "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nth, "kind": "oracle",
-                         "sample": f"{sample_layers} of {LAYERS} layers per step (fp64 C oracle, "
-                                   f"OpenMP over units), ms_per_step extrapolated to {LAYERS} layers"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{sample} of {LAYERS} layers per step, measured (fp64 C oracle, "
+                                   f"OpenMP over the (b, KV group) units)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -212,11 +341,83 @@ def config_dict(wl):
 # ---------------------------------------------------------------- GPU arm
 
 
-def run_heads(args):
-    """the multi-turn batch (B=8, 16k visual) sharded over
-    (batch x KV head), one fused fresh step per layer per rank, then the NCCL
-    all-gather of head outputs (captured in the same CUDA graph).  Strong
-    scaling: the total work is fixed."""
+def fused_gather_timing(wl, sp, loc, world, rank, dev, steps):
+    """Per layer: svl_retrieve on the rank's slice, then svl_sparse_decode_attn_push into
+    every rank's gathered [B][H][d] buffer (symmetric memory across processes), then
+    svl_wait_flags for every producer's epoch.  Returns ms per 28-layer step (max over
+    ranks) or the reason it could not run."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_17777_b200 import svl
+    try:
+        if world > 1:
+            import torch.distributed._symmetric_memory as symm_mem
+            bufs, flags = [], []
+            for _ in range(SHARD_ROT):
+                t = symm_mem.empty(wl.B * wl.H * wl.d, dtype=torch.float32, device=dev)
+                h = symm_mem.rendezvous(t, dist.group.WORLD.group_name)
+                bufs.append([h.get_buffer(r, (wl.B, wl.H, wl.d), torch.float32) for r in range(world)])
+            tf = symm_mem.empty(world, dtype=torch.int32, device=dev)
+            tf.zero_()
+            hf = symm_mem.rendezvous(tf, dist.group.WORLD.group_name)
+            flags = [hf.get_buffer(r, (world,), torch.int32) for r in range(world)]
+            dist.barrier()
+        else:
+            bufs = [[torch.empty(wl.B, wl.H, wl.d, device=dev)] for _ in range(SHARD_ROT)]
+            tf = torch.zeros(1, dtype=torch.int32, device=dev)
+            flags = [tf]
+    except Exception as e:  # noqa: BLE001 -- report, do not fail the bench line
+        return {"unavailable": f"symmetric memory: {type(e).__name__}: {str(e)[:120]}"}
+    Hkvl = sp.kv1 - sp.kv0
+    ws = svl.Workspace(dev)
+    wsw = svl.Workspace(dev)
+    idx = torch.empty(sp.B_local, Hkvl, wl.k, dtype=torch.int32, device=dev)
+    epoch = [0]
+
+    def step():
+        for l in range(LAYERS):
+            r = l % SHARD_ROT
+            ql, Kl, Vl, sl = loc[r]
+            epoch[0] += 1
+            svl.retrieve(ql.unsqueeze(1), Kl, sl, wl.vb, wl.nv, wl.k, idx_out=idx, ws=ws)
+            svl.sparse_decode_attn_push(ql, Kl, Vl, sl, wl.vb, wl.nv, idx, bufs[r], flags, rank, epoch[0],
+                                        sp.b0, sp.kv0 * sp.g, ws=ws)
+            svl.wait_flags(tf, epoch[0], ws=wsw)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    timeouts = bool(wsw.flags() & svl.SVL_DEVFLAG_WAIT_TIMEOUT)
+    return {"ms_per_step": ms, "steps": steps, "wait_timeouts": timeouts,
+            "how": "eager: svl_retrieve + svl_sparse_decode_attn_push (peer stores into symmetric memory) + "
+                   "svl_wait_flags per layer"}
+
+
+SHARD_ROT = 4  # rotating layer caches of the sharded runs (the 28-layer step cycles through them)
+
+
+def run_sharded(args, cfg_name):
+    """one batch (the throughput sweep by default) sharded over
+    (batch x KV head) (sharding.plan: P_h = gcd(P, Hkv), P_b = P / P_h), one
+    svl_fresh_decode_step per layer per rank on its slice of every layer's cache,
+    then one NCCL all_gather_into_tensor of the fp32 head outputs per layer (the
+    harness's exchange, north star), permuted into [B][H][d] -- all captured in
+    one CUDA graph per 28-layer step.  Strong scaling: the total work is fixed.
+    Rank 0 also times the same 28-layer step unsharded on its GPU alone (T(1)), so
+    the line carries E(P) = T(1) / (P T(P)) with and without the gather."""
     import torch
     import torch.distributed as dist
 
@@ -228,68 +429,198 @@ def run_heads(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    wl = gen.CONFIGS["multi-turn"]
+    svl.lib()
+    wl = gen.CONFIGS[cfg_name]
     sp = sharding.plan(wl.B, wl.H, wl.Hkv, world, rank)
-    lwl = gen.DecodeWorkload(**{**wl.__dict__, "B": sp.B_local, "Hkv": sp.kv1 - sp.kv0,
-                                "H": sp.H_local})
-    layers = []
-    for layer in range(LAYERS):
-        x = gen.make_decode_inputs(lwl, seed=7000 + 100 * rank + layer, device=dev)
-        layers.append(x)
+    # every rank generates the same global layers and keeps views of its slice (the
+    # sharded outputs can then be checked against the unsharded run); ~1.3 GB per sweep layer
+    xs = [gen.make_decode_inputs(wl, seed=7000 + l, device=dev) for l in range(SHARD_ROT)]
+    loc = [sharding.local_inputs(sp, x["q_dec"], x["K"], x["V"], x["seq_len"]) for x in xs]
+    Bl, Hl, Hkvl = sp.B_local, sp.H_local, sp.kv1 - sp.kv0
     ws = svl.Workspace(dev)
-    ws.get(svl.fresh_decode_workspace_size(lwl.B, lwl.H, lwl.Hkv, lwl.d, lwl.k, lwl.nv, lwl.capacity))
-    outs = [torch.empty(lwl.B, lwl.H, lwl.d, device=dev) for _ in range(LAYERS)]
-    idxs = [torch.empty(lwl.B, lwl.Hkv, lwl.k, dtype=torch.int32, device=dev) for _ in range(LAYERS)]
-    full = [torch.empty(wl.B, wl.H, wl.d, device=dev) for _ in range(LAYERS)]
+    ws.get(svl.fresh_decode_workspace_size(Bl, Hl, Hkvl, wl.d, wl.k, wl.nv, wl.capacity))
+    outs = [torch.empty(Bl, Hl, wl.d, device=dev) for _ in range(SHARD_ROT)]
+    idxs = [torch.empty(Bl, Hkvl, wl.k, dtype=torch.int32, device=dev) for _ in range(SHARD_ROT)]
+    gbuf = [torch.empty(world * Bl * Hl * wl.d, device=dev) for _ in range(SHARD_ROT)]
+    full = [torch.empty(wl.B, wl.H, wl.d, device=dev) for _ in range(SHARD_ROT)]
+    plans = [sharding.plan(wl.B, wl.H, wl.Hkv, world, r) for r in range(world)]
+    # permutation of the gathered rank blocks into [B][H][d] (a gather by index: graph-safe)
+    perm = torch.empty(wl.B, wl.H, dtype=torch.int64)
+    for r, pr in enumerate(plans):
+        bb, hh = torch.meshgrid(torch.arange(pr.B_local), torch.arange(pr.H_local), indexing="ij")
+        perm[pr.b0:pr.b1, pr.kv0 * pr.g:pr.kv1 * pr.g] = r * pr.B_local * pr.H_local + bb * pr.H_local + hh
+    perm = perm.view(-1).to(dev)
 
-    def step():
-        for l, x in enumerate(layers):
-            svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], lwl.vb, lwl.nv, lwl.k,
-                                  idx_out=idxs[l], out=outs[l], ws=ws)
+    def layer(l, gather):
+        r = l % SHARD_ROT
+        ql, Kl, Vl, sl = loc[r]
+        svl.fresh_decode_step(ql, Kl, Vl, sl, wl.vb, wl.nv, wl.k, idx_out=idxs[r], out=outs[r], ws=ws)
+        if gather:
             if world > 1:
-                full[l].copy_(sharding.all_gather_heads(outs[l], sp, wl.H))
+                dist.all_gather_into_tensor(gbuf[r], outs[r].view(-1))
             else:
-                full[l].copy_(outs[l])
+                gbuf[r].copy_(outs[r].view(-1))
+            torch.index_select(gbuf[r].view(-1, wl.d), 0, perm, out=full[r].view(-1, wl.d))
 
-    step()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    s = torch.cuda.Stream(device=dev)
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(g, stream=s):
-            step()
-    for _ in range(args.warmup):
-        g.replay()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    def graph_of(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                fn()
+        torch.cuda.synchronize()
+        return g
+
+    def timed(g, steps, warmup):
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             g.replay()
         e1.record()
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-    total = step_bytes(wl)["total"] * LAYERS
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms
+
+    steps = max(5, min(args.steps, 200))
+    warm = max(3, min(args.warmup, 20))
+    # ---- T(1): rank 0 alone, the unsharded step (same layers, same 28-layer structure)
+    t1 = None
+    ref_out = None
     if rank == 0:
-        print(json.dumps({
-            "metric": "decode step HBM GB/s (retrieve+sparse attn), multi-turn batch head-sharded",
-            "value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "multi-turn: B=8, 16384 visual, k=1638, 28 layers, (batch x KV-head) "
-                                   "shards + NCCL all-gather of head outputs per layer",
-                       "P_b": sp.P_b, "P_h": sp.P_h},
-            "tokens_per_s": wl.B / (ms * 1e-3), "clocks": clk.summary(),
-            "gpu_launches": LAYERS * args.steps}))
+        ws1 = svl.Workspace(dev)
+        ws1.get(svl.fresh_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
+        o1 = [torch.empty(wl.B, wl.H, wl.d, device=dev) for _ in range(SHARD_ROT)]
+        i1 = [torch.empty(wl.B, wl.Hkv, wl.k, dtype=torch.int32, device=dev) for _ in range(SHARD_ROT)]
+
+        def one_gpu():
+            for l in range(LAYERS):
+                r = l % SHARD_ROT
+                svl.fresh_decode_step(xs[r]["q_dec"], xs[r]["K"], xs[r]["V"], xs[r]["seq_len"], wl.vb, wl.nv,
+                                      wl.k, idx_out=i1[r], out=o1[r], ws=ws1)
+        g1 = graph_of(one_gpu)
+        for _ in range(warm):
+            g1.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            g1.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        t1 = e0.elapsed_time(e1) / steps
+        ref_out = o1[(LAYERS - 1) % SHARD_ROT].clone()
+        del g1, o1, i1, ws1
+    if world > 1:
+        dist.barrier()
+    # ---- T(P): the sharded step with and without the gather
+    g_full = graph_of(lambda: [layer(l, True) for l in range(LAYERS)])
+    g_comp = graph_of(lambda: [layer(l, False) for l in range(LAYERS)])
+    with ClockSampler(local) as clk:
+        ms = timed(g_full, steps, warm)
+    ms_c = timed(g_comp, steps, warm)
+    # the gathered output equals the unsharded one (per-unit split counts differ between a
+    # shard and the whole batch, so within the attention tolerance, not bitwise)
+    check = None
+    if rank == 0:
+        g_full.replay()
+        torch.cuda.synchronize()
+        got = full[(LAYERS - 1) % SHARD_ROT]
+        check = {"max_abs_vs_unsharded": float((got - ref_out).abs().max().item())}
+    # ---- --fused-gather: the exchange folded into the decode kernel (svl_sparse_decode_attn_push
+    # stores every output element into each rank's symmetric-memory buffer, then raises the
+    # rank's epoch flag; svl_wait_flags is the consumer).  Eager launches (the epoch is a
+    # call argument, so a replayed graph would reuse it).
+    fused = None
+    if args.fused_gather:
+        fused = fused_gather_timing(wl, sp, loc, world, rank, dev, steps=max(3, steps // 10))
+    # ---- e2e through the public API: per step the ranks' q slices H2D (pinned), the graph,
+    # the gathered outputs D2H
+    q_host = [loc[r][0].cpu().pin_memory() for r in range(SHARD_ROT)]
+    out_host = torch.empty(SHARD_ROT, wl.B, wl.H, wl.d).pin_memory()
+
+    def e2e_once():
+        for r in range(SHARD_ROT):
+            loc[r][0].copy_(q_host[r], non_blocking=True)
+        g_full.replay()
+        for r in range(SHARD_ROT):
+            out_host[r].copy_(full[r], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(3):
+        e2e_once()
+    if world > 1:
+        dist.barrier()
+    n_e2e = max(5, steps // 4)
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        e2e_once()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    total = step_bytes(wl)["total"] * LAYERS
+    nccl = {"backend": dist.get_backend() if world > 1 else None, "nranks": world,
+            "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if world > 1 else None,
+            "gather_bytes_per_layer_per_rank": Bl * Hl * wl.d * 4}
+    if rank == 0:
+        line = {
+            "metric": f"decode step HBM GB/s (retrieve+sparse attn), {cfg_name} batch head-sharded",
+            "value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded generator)",
+            "config": {"workload": f"{cfg_name}: B {wl.B}, {wl.nv} visual, k {wl.k}, {LAYERS} layers "
+                                   f"({SHARD_ROT} rotating caches), (batch x KV-head) shards + NCCL "
+                                   f"all-gather of head outputs per layer",
+                       "P_b": sp.P_b, "P_h": sp.P_h, "B_local": Bl, "kv_heads_local": Hkvl,
+                       "l2": "inputs > L2 (rotating layer caches)"},
+            "us_per_layer": ms * 1e3 / LAYERS,
+            "compute_only": {"ms_per_step": ms_c, "GB_s": total / (ms_c * 1e-3) / 1e9},
+            "one_gpu": {"ms_per_step": t1, "GB_s": total / (t1 * 1e-3) / 1e9} if t1 else None,
+            "E_strong": (t1 / (world * ms)) if t1 else None,
+            "E_strong_compute_only": (t1 / (world * ms_c)) if t1 else None,
+            "E_definition": "T(1) / (P T(P)), T(1) = the unsharded step on rank 0's GPU in this run (SURVEY 8(e) e5)",
+            "correctness": check,
+            "fused_gather": fused,
+            "collective": nccl,
+            "e2e": {"value": total / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": sum(int(q.numel()) * 2 for q in q_host),
+                    "d2h_bytes_per_step": int(out_host.numel()) * 4},
+            "gpu_launches": LAYERS * steps * (1 if svl.fresh_uses_fused(Bl, Hl, Hkvl, wl.d, wl.nv, wl.capacity)
+                                               else 3),
+            "clocks": clk.summary()}
+        print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def free_port():
+    import socket
+    sck = socket.socket()
+    sck.bind(("127.0.0.1", 0))
+    port = sck.getsockname()[1]
+    sck.close()
+    return port
+
+
+def relaunch(args):
+    """--gpus N > 1 without a torch.distributed launcher: re-run this script under
+    torch.distributed.run with N ranks (one per GPU), the driver's own launch line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -300,16 +631,37 @@ def main():
     ap.add_argument("--impl", default="svl", choices=["svl", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON checks)")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "heads"],
-                    help="replicas: every rank serves its own long-video request (weak); heads: "
-                         "one multi-turn batch sharded over (batch x KV head) with a per-layer "
-                         "NCCL all-gather of the head outputs (strong)")
+    ap.add_argument("--mode", default="auto", choices=["auto", "headline", "replicas", "sweep-heads", "heads"],
+                    help="auto: headline at N = 1, sweep-heads at N > 1; replicas: every rank serves its "
+                         "own long-video request (weak); sweep-heads: the B 16 / 64k sweep sharded over "
+                         "(batch x KV head) with a per-layer NCCL all-gather of the head outputs (strong); "
+                         "heads: the same for the multi-turn batch")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="sweep-heads: replace the NCCL all-gather by svl_sparse_decode_attn_push into "
+                         "symmetric-memory peer buffers (eager launches: the epoch is a call argument)")
+    ap.add_argument("--launch-check", action="store_true", help="print rank / world and exit (launcher test)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and args.gpus not in (1, world):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.launch_check:
+        print(json.dumps({"launch_check": True, "rank": rank, "world": world, "local_rank": local}), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
-    if args.mode == "heads":
-        return run_heads(args)
+    mode = args.mode if args.mode != "auto" else ("headline" if world == 1 else "sweep-heads")
+    if mode == "sweep-heads":
+        return run_sharded(args, "sweep")
+    if mode == "heads":
+        return run_sharded(args, "multi-turn")
+    return run_headline(args)
 
+
+def run_headline(args):
+    """N = 1: the headline long-video line (+ companions); N > 1 (--mode replicas):
+    every rank serves its own long-video request, weak scaling."""
     import torch
     import torch.distributed as dist
 
@@ -416,6 +768,14 @@ def main():
         ms_step = t.item()
     total_bytes = nbytes["total"] * LAYERS * world
     value = total_bytes / (ms_step * 1e-3) / 1e9
+    # per-replay distribution (events around each replay): median / p10 / p90 per step
+    dist_ms = replay_times(g_step, min(200, args.steps))
+    pct = {"median": statistics.median(dist_ms), "p10": quantile(dist_ms, 0.10),
+           "p90": quantile(dist_ms, 0.90), "n": len(dist_ms)}
+    # cold single layer: a 2 x L2 write before each launch, events
+    # around the one launch only -- no overlap with a neighbouring layer
+    cold_fresh_us = cold_layer_us(lambda: layer_fresh(0))
+    cold_decode_us = cold_layer_us(lambda: layer_decode(0))
 
     # ---- breakdown (same stream, CUDA events): score / select / decode graphs
     sub = max(200, args.steps // 4)
@@ -442,18 +802,15 @@ def main():
     del packed
 
     # ---- e2e through the public API with host buffers (pinned)
-    q_host = torch.stack(qs).cpu().pin_memory()
     qd_host = torch.stack(qds).cpu().pin_memory()
     newkv_host = torch.zeros(LAYERS, 2, wl.B, wl.Hkv, wl.d, dtype=torch.bfloat16).pin_memory()
     out_host = torch.empty(LAYERS, wl.B, wl.H, wl.d, dtype=torch.float32).pin_memory()
-    q_dev = torch.stack(qs)
     qd_dev = torch.stack(qds)
     newkv_dev = torch.empty(LAYERS, 2, wl.B, wl.Hkv, wl.d, dtype=torch.bfloat16, device=dev)
     last = wl.seq_len - 1
     for l in range(LAYERS):
         newkv_host[l, 0] = Ks[l][:, :, last].cpu()
         newkv_host[l, 1] = Vs[l][:, :, last].cpu()
-    qs_e = [q_dev[l] for l in range(LAYERS)]
     qds_e = [qd_dev[l] for l in range(LAYERS)]
 
     def e2e_step():
@@ -465,12 +822,11 @@ def main():
 
     g_e2e = graph_of(e2e_step)
     out_stack = torch.stack(outs)  # placeholder to size
-    h2d = q_host.numel() * 2 + qd_host.numel() * 2 + newkv_host.numel() * 2
+    h2d = qd_host.numel() * 2 + newkv_host.numel() * 2
     d2h = out_host.numel() * 4
     e2e_steps = max(50, args.steps // 10)
 
     def e2e_once():
-        q_dev.copy_(q_host, non_blocking=True)
         qd_dev.copy_(qd_host, non_blocking=True)
         newkv_dev.copy_(newkv_host, non_blocking=True)
         g_e2e.replay()
@@ -512,19 +868,25 @@ def main():
         g_sal, g_prune = graph_of(sal_step), graph_of(prune_step)
         ms_sal = timed(g_sal, 20, 3)
         ms_prune = timed(g_prune, 200, 10)
-        flops = 2 * 2 * pw.Nf * pw.Nf * pw.de * pw.He * pw.F  # 2 passes x 2 N_f^2 d_e per head and frame
+        flops_exec = 2 * pw.Nf * pw.Nf * pw.de * pw.He * pw.F  # S = Q K^T once per head and frame (tcgen05)
+        flops_survey = 2 * flops_exec  # SURVEY.md 8(d) d5 counts two QK^T passes
         bf16_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops") \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
         n_exp = pw.Nf * pw.Nf * pw.He * pw.F
+        tf_exec = flops_exec / (ms_sal * 1e-3) / 1e12
         prefill = {"config": f"prune: {pw.F} frames x {pw.Nf} tokens, H_e {pw.He}, d_e {pw.de}, "
                              f"INTRA_VISUAL, s_p {pw.sparsity}",
-                   "salience_ms": ms_sal, "salience_tflops": flops / (ms_sal * 1e-3) / 1e12,
-                   "salience_flops_accounting": "SURVEY.md 8(d) d5: 2 passes x 2 N_f^2 d_e per head and "
-                                                "frame; the tcgen05 kernel computes S once (half of it)",
+                   "salience_ms": ms_sal,
+                   "salience_tflops": tf_exec,
+                   "salience_flops_accounting": "executed: 2 N_f^2 d_e per head and frame (the tcgen05 kernel "
+                                                "computes S = Q K^T once; row LSE and column sums come from the "
+                                                "same tile); SURVEY.md 8(d) d5's 2-pass count is "
+                                                "salience_tflops_survey_count",
+                   "salience_tflops_survey_count": flops_survey / (ms_sal * 1e-3) / 1e12,
                    "salience_exp2_per_s": n_exp / (ms_sal * 1e-3),
-                   "salience_bound": "tensor (per SURVEY); measured: exp2 + issue bound at d_e = 72",
+                   "salience_bound": "measured: exp2 + issue bound at d_e = 72 (one exponential per 2 d_e flop)",
                    "bf16_peak_tflops": bf16_peak,
-                   "salience_frac": (flops / (ms_sal * 1e-3) / 1e12 / bf16_peak) if bf16_peak else None,
+                   "salience_frac": (tf_exec / bf16_peak) if bf16_peak else None,
                    "prune_us": ms_prune * 1e3, "kept": int(kept.numel())}
         # f4(i): unified RoPE remap of the kept tokens (pre-RoPE K rotated to their new
         # contiguous positions, V compacted) on the LLM cache the prune feeds: 4 KV heads, d 128
@@ -613,21 +975,23 @@ def main():
     score_us = ms_score * 1e3 / LAYERS
     fused_us = ms_step * 1e3 / LAYERS
     achieved = nbytes["fused"] / (fused_us * 1e-6) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_fresh_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = fresh_traffic()
+    # ---- the other BASELINE configs as rows: nvila-4k and the multi-turn
+    # round (8 rounds of 1 fresh retrieval + 249 steady steps, batch 8)
+    rows = None
+    if rank == 0 and world == 1 and not args.profile:
+        rows = config_rows(graph_of, timed)
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): the oracle on all host cores, and on one thread
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, layers, th, secs = cpu_oracle_sample(wl)
-        cpu = {"value": v / 1e9, "unit": "GB/s", "cores": th, "kind": "oracle",
+        v1, layers1, _, secs1 = cpu_oracle_sample(wl, budget_s=4.0, nthreads=1)
+        cpu = {"value": v / 1e9, "unit": "GB/s", "cores": th, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{layers} whole layers of the long-video step (retrieve + sparse decode),"
-                         f" {secs:.1f} s of fp64 oracle work, OpenMP over (b, KV-group) units"}
+                         f" {secs:.1f} s of fp64 oracle work, OpenMP over (b, KV-group) units",
+               "one_thread": {"value": v1 / 1e9, "unit": "GB/s", "cores": 1,
+                              "sample": f"{layers1} whole layers, {secs1:.1f} s"}}
 
     launches = LAYERS * args.steps  # one fused fresh_kernel launch per layer
     if rank == 0:
@@ -639,6 +1003,10 @@ def main():
             "data": "synthetic (seeded generator, paper_2510_17777_b200/inputs.py)",
             "config": config_dict(wl),
             "us_per_layer": ms_step * 1e3 / LAYERS,
+            "ms_per_step_distribution": pct,
+            "cold_single_layer_us": {"fresh_step": cold_fresh_us, "steady_decode": cold_decode_us,
+                                     "how": "one launch after a 2 x L2 write, events around the launch only "
+                                            "(no overlap with a neighbouring layer; SURVEY.md 8(d) d6)"},
             "tokens_per_s": wl.B * world / (ms_step * 1e-3),
             "hbm_frac_of_measured": value / world / peak,
             "unfused_us_per_layer": {"retrieve+decode (2 calls)": ms_unfused * 1e3 / LAYERS,
@@ -658,11 +1026,13 @@ def main():
                           "amortized_packed_us_per_layer": amort_packed_us},
             "roofline": {"bound": "hbm", "kernel": "fresh_kernel (svl_fresh_decode_step)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": nbytes["fused"]},
             "prefill": prefill,
             "question_retrieve": qret,
             "throughput_sweep": sweep,
+            "configs": rows,
             "cpu_baseline": cpu,
             "e2e": {"value": nbytes["total"] * LAYERS * world / (e2e_ms * 1e-3) / 1e9,
                     "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,

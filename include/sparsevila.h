@@ -304,6 +304,13 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
                                  uint32_t flags, int32_t* idx_out, float* out, float* lse_out,
                                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* 1 if svl_fresh_decode_step runs the fused kernel for this shape and flags on the
+ * current device (one launch per call), 0 if it runs the two separate calls
+ * (host-only query; a K view that cannot be encoded as a TMA tensor map also
+ * takes the two calls at run time). */
+int32_t svl_fresh_decode_plan(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t visual_len,
+                              int32_t capacity, uint32_t flags);
+
 size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                        int32_t visual_len, int32_t capacity, uint32_t flags);
 

@@ -672,6 +672,13 @@ static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int
     return true;
 }
 
+int32_t svl_fresh_decode_plan(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t visual_len, int32_t capacity,
+                              uint32_t flags) {
+    if (B < 1 || Hkv < 1 || H < 1 || H % Hkv || visual_len < 1 || (d != 64 && d != 128)) return 0;
+    int CS, slice;
+    return fresh_plan(B, Hkv, H / Hkv, visual_len, capacity, CS, slice, d, flags) ? 1 : 0;
+}
+
 size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                        int32_t visual_len, int32_t capacity, uint32_t flags) {
     if (B < 1 || Hkv < 1 || H % Hkv || visual_len < 1) return 0;

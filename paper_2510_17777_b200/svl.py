@@ -42,7 +42,7 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
            "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
-           "svl_wait_flags", "svl_pack_kv", "svl_rope_remap"]
+           "svl_wait_flags", "svl_pack_kv", "svl_rope_remap", "svl_fresh_decode_plan"]
 
 
 class SvlError(RuntimeError):
@@ -96,6 +96,8 @@ def lib():
         L.svl_fresh_decode_step.restype = ctypes.c_int
         L.svl_fresh_decode_step.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, I32,
                                             F, U32, P, P, P, P, SZ, P]
+        L.svl_fresh_decode_plan.restype = ctypes.c_int
+        L.svl_fresh_decode_plan.argtypes = [I32, I32, I32, I32, I32, I32, U32]
         L.svl_fresh_decode_workspace_size.restype = SZ
         L.svl_fresh_decode_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, I32, U32]
         L.svl_prefill_prune.restype = ctypes.c_int
@@ -351,6 +353,11 @@ def wait_flags(flags: torch.Tensor, epoch: int, ws: Optional[Workspace] = None, 
     w = _ws(ws, flags.device).get(WORKSPACE_HEADER_BYTES)
     _check(lib().svl_wait_flags(_cuda(flags, "flags", torch.int32), flags.numel(), epoch,
                                 w.data_ptr(), _stream(stream)))
+
+
+def fresh_uses_fused(B, H, Hkv, d, visual_len, capacity, flags=0) -> bool:
+    """Whether svl_fresh_decode_step runs the fused kernel (one launch per call) for a shape."""
+    return bool(lib().svl_fresh_decode_plan(B, H, Hkv, d, visual_len, capacity, flags))
 
 
 def fresh_decode_workspace_size(B, H, Hkv, d, k, visual_len, capacity, flags=0) -> int:
