@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
                 if (rw[k] == -2) continue;
                 const bool valid = rw[k] >= 0;
                 const int rr = valid ? rw[k] : 0;
+#if SVL_DEBUG_TRAP  // debug builds: every gathered row lies inside the cache
+                if (rr >= p.capacity) __trap();
+#endif
                 cp_async16(sK + r * SM::ROW_BYTES + swz_k(r, c) * 16, Kb + (int64_t)rr * p.kst + c * 8, valid);
                 cp_async16(sV + r * SM::ROW_BYTES + swz_v(r, c) * 16, Vb + (int64_t)rr * p.vst + c * 8, valid);
             }
@@ -469,6 +472,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
                     if ((uint32_t)(vl[r] >> 32) != tag) vl[r] = ld_relaxed_u64(addr_m(tid + r * NTH) + 16);
                 }
             }
+            cta_sync();  // every thread's cta_o reads of the staging region are done
 #pragma unroll
             for (int r = 0; r < MAXL; ++r) {
                 const int e = tid + r * NTH;

@@ -191,6 +191,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     auto gather_rows = [&](int s0, int s1, int base) {
         for (int e = tid; e < (s1 - s0) * CH; e += FT) {
             const int sl = s0 + e / CH, c = e % CH;
+#if SVL_DEBUG_TRAP  // debug builds: a V slot must name a row of this CTA's work list
+            if (att[sl] < 0 || att[sl] >= nvis + ntext || work_row(att[sl]) < 0 || work_row(att[sl]) >= L) __trap();
+#endif
             cp_async16(vst + (sl - base) * GM::VROWB + c * 16, Vb + (int64_t)work_row(att[sl]) * p.vst + c * 8, true);
         }
         cp_async_commit();
@@ -614,7 +617,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         if (lane == 0) lse2[warp] = x.x + log2f(x.y);
     }
     // text rows' V: V slots [0, ntext); the gather overlaps everything up to the decode
-    // (issued after the LSE barrier: a cluster arrive.release waits for in-flight copies)
+    // (issued after the LSE barrier: a cluster arrive.release waits for in-flight copies;
+    // the CTA barrier publishes att[0, ntext) to every gathering thread -- compute-sanitizer
+    // racecheck)
+    cta_sync();
     gather_rows(0, ntext, 0);
     cta_sync();
     SVL_TRACE(2);
@@ -689,6 +695,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         gather_rows(ntext, min(nslots, VCAP), 0);
         v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
 #else
+        cta_sync();  // every thread's V-slot assignments (att) visible to the gathering threads
         gather_rows(ntext, min(nslots, VCAP), 0);
         v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
         SVL_TRACE(12);

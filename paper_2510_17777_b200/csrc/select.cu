@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kSmallFrame) prune_small_kernel(const SelectPa
 
 int select_cluster_size(int n) {
     int cs = (n + 2047) / 2048;
-    if (cs < 1) cs = 1;
+    if (cs < 2) cs = 2;  // >= 2: st.async / DSMEM exchanges need a real cluster (compute-sanitizer)
     if (cs > 16) cs = 16;
     int c = 1;  // power of two: the 4096 / 1024 digit bins split evenly between owners
     while (c < cs) c <<= 1;
