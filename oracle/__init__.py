@@ -63,6 +63,10 @@ def lib():
         L.o_prune.restype = I
         L.o_prune.argtypes = [P, I, I, P, I, D, P, I, P]
         L.o_rope_remap.argtypes = [P, I, I, I, I, P, I, I, P, I, D, P, I, P]
+        L.o_page_summary.restype = I
+        L.o_page_summary.argtypes = [P, I, I, I, I64, I64, I64, I, I, I, P, P]
+        L.o_retrieve_pages.restype = I
+        L.o_retrieve_pages.argtypes = [P, I, I, I, I, I, P, P, I, I, D, P, P, P]
         _lib = L
     return _lib
 
@@ -212,3 +216,43 @@ def rope_remap(K_pre, seq_len, vb: int, nv: int, kept, base: float, cap_out: int
                             cap_out, _ptr(rows))
     _check(rc, "o_rope_remap")
     return out, rows
+
+
+def page_summary(K, vb: int, nv: int, page: int):
+    """Per-page elementwise max / min of the visual keys.
+    K bf16 [B][Hkv][cap][d].  Returns (kmax, kmin) float64 [B][Hkv][nv/page][d]."""
+    B, Hkv, _, d = K.shape
+    ka, koff, sb, sh, st = _kv(K)
+    npg = nv // page
+    kmax = np.zeros((B, Hkv, npg, d), np.float64)
+    kmin = np.zeros((B, Hkv, npg, d), np.float64)
+    rc = lib().o_page_summary(_ptr(ka, koff), B, Hkv, d, sb, sh, st, vb, nv, page, _ptr(kmax), _ptr(kmin))
+    _check(rc, "o_page_summary")
+    return kmax, kmin
+
+
+def retrieve_pages(q, kmax, kmin, k_pages: int, scale: float | None = None):
+    """Quest-style page retrieval (reading A22).  q bf16 [B][n_q][H][d]; kmax / kmin
+    float64 [B][Hkv][np][d].  Returns (page_idx [B][Hkv][k_pages] int32, scores
+    [B][Hkv][np] f64, rel_gap [B][Hkv])."""
+    B, n_q, H, d = q.shape
+    _, Hkv, npg, _ = kmax.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    qa = _u16(q.contiguous())
+    mx = np.ascontiguousarray(kmax, dtype=np.float64)
+    mn = np.ascontiguousarray(kmin, dtype=np.float64)
+    idx = np.zeros((B, Hkv, k_pages), np.int32)
+    sc = np.zeros((B, Hkv, npg), np.float64)
+    gap = np.zeros((B, Hkv), np.float64)
+    rc = lib().o_retrieve_pages(_ptr(qa), B, n_q, H, Hkv, d, _ptr(mx), _ptr(mn), npg, k_pages, scale,
+                                _ptr(idx), _ptr(sc), _ptr(gap))
+    _check(rc, "o_retrieve_pages")
+    return idx, sc, gap
+
+
+def pages_to_rows(page_idx, page: int):
+    """Ascending page indices -> the ascending visual rows they cover (relative to vb)."""
+    pi = np.asarray(page_idx, dtype=np.int64)
+    rows = pi[..., :, None] * page + np.arange(page)[None, :]
+    return rows.reshape(*pi.shape[:-1], pi.shape[-1] * page).astype(np.int32)

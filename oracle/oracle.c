@@ -475,3 +475,99 @@ int o_rope_remap(const uint16_t* Kpre, int B, int Hkv, int d, int cap, const int
     }
     return 0;
 }
+
+/*
+ * o_page_summary -- per-page elementwise key bounds (
+ * PAPER.md:527 "Quest estimates upper-bound attention scores for each page").
+ * For each unit (b, G) and page p of `page` consecutive visual rows
+ * [vb + p*page, vb + (p+1)*page):
+ *   kmax[b][G][p][c] = max_j K[b,G,j,c],  kmin[b][G][p][c] = min_j K[b,G,j,c]
+ * (exact: the max / min of bf16 values is a bf16 value; returned as double).
+ * nv % page == 0 (reading A22).
+ */
+int o_page_summary(const uint16_t* K, int B, int Hkv, int d, int64_t ksb, int64_t ksh, int64_t kst,
+                   int vb, int nv, int page, double* kmax, double* kmin) {
+    if (B < 0 || Hkv < 1 || d < 1 || vb < 0 || nv < 1 || page < 1 || nv % page) return O_ERR_SHAPE;
+    const int np = nv / page;
+    for (int b = 0; b < B; ++b)
+        for (int G = 0; G < Hkv; ++G) {
+            const uint16_t* Kb = K + (int64_t)b * ksb + (int64_t)G * ksh;
+            for (int p = 0; p < np; ++p)
+                for (int c = 0; c < d; ++c) {
+                    double mx = -INFINITY, mn = INFINITY;
+                    for (int j = vb + p * page; j < vb + (p + 1) * page; ++j) {
+                        const double v = bf(Kb[(int64_t)j * kst + c]);
+                        if (v > mx) mx = v;
+                        if (v < mn) mn = v;
+                    }
+                    const int64_t o = (((int64_t)b * Hkv + G) * np + p) * d + c;
+                    kmax[o] = mx;
+                    kmin[o] = mn;
+                }
+        }
+    return 0;
+}
+
+/*
+ * o_retrieve_pages -- query-aware retrieval on page summaries (SURVEY.md 8(f)
+ * f2(ii); PAPER.md:527 Quest; reading A22).  For each unit (b, G):
+ *  1. ub[r,h,p] = scale * sum_c max(q[b,r,h,c] * kmax[p][c], q[b,r,h,c] * kmin[p][c])
+ *     -- an upper bound of scale * q . K_j over every row j of page p (Quest);
+ *  2. LSEp[r,h] = log sum_p exp(ub[r,h,p])   (softmax over the unit's pages);
+ *  3. score[p] = sum_r sum_h exp(ub[r,h,p] - LSEp[r,h]), r asc, h asc  (the
+ *     page analogue of the visual-only relevance, readings A2, A3);
+ *  4. top-k_p pages by (score desc, p asc); page indices ascending.
+ * With page = 1 this is o_retrieve with O_VISUAL_ONLY.
+ * kmax, kmin: double [B][Hkv][np][d] (o_page_summary); q bf16 [B][n_q][H][d].
+ */
+int o_retrieve_pages(const uint16_t* q, int B, int n_q, int H, int Hkv, int d, const double* kmax,
+                     const double* kmin, int np, int kp, double scale, int32_t* pidx_out,
+                     double* scores_out, double* rel_gap_out) {
+    if (B < 0 || n_q < 1 || H < 1 || Hkv < 1 || H % Hkv || d < 1 || np < 1) return O_ERR_SHAPE;
+    if (kp < 0 || kp > np) return O_ERR_ARG;
+    const int g = H / Hkv;
+    double* ub = (double*)malloc(sizeof(double) * (size_t)np);
+    double* score = (double*)malloc(sizeof(double) * (size_t)np);
+    if (!ub || !score) {
+        free(ub);
+        free(score);
+        return O_ERR_NOMEM;
+    }
+    int err = 0;
+    for (int b = 0; b < B; ++b)
+        for (int G = 0; G < Hkv; ++G) {
+            for (int p = 0; p < np; ++p) score[p] = 0.0;
+            const double* mx = kmax + ((int64_t)b * Hkv + G) * np * d;
+            const double* mn = kmin + ((int64_t)b * Hkv + G) * np * d;
+            for (int r = 0; r < n_q; ++r)
+                for (int h = G * g; h < G * g + g; ++h) {
+                    const uint16_t* qv = q + (((int64_t)b * n_q + r) * H + h) * d;
+                    for (int p = 0; p < np; ++p) {
+                        double acc = 0.0;
+                        for (int c = 0; c < d; ++c) {
+                            const double a = bf(qv[c]) * mx[(int64_t)p * d + c];
+                            const double e = bf(qv[c]) * mn[(int64_t)p * d + c];
+                            acc += (a > e) ? a : e;
+                        }
+                        ub[p] = scale * acc;
+                    }
+                    double m = -INFINITY;
+                    for (int p = 0; p < np; ++p)
+                        if (ub[p] > m) m = ub[p];
+                    double sum = 0.0;
+                    for (int p = 0; p < np; ++p) sum += exp(ub[p] - m);
+                    const double lse = m + log(sum);
+                    for (int p = 0; p < np; ++p) score[p] += exp(ub[p] - lse);
+                }
+            const int unit = b * Hkv + G;
+            for (int p = 0; p < np; ++p)
+                if (!isfinite(score[p])) err = O_ERR_NONFINITE;
+            if (scores_out) memcpy(scores_out + (int64_t)unit * np, score, sizeof(double) * (size_t)np);
+            const int e = topk_select(score, np, kp, pidx_out + (int64_t)unit * kp,
+                                      rel_gap_out ? rel_gap_out + unit : NULL);
+            if (e) err = e;
+        }
+    free(ub);
+    free(score);
+    return err;
+}

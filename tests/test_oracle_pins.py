@@ -477,3 +477,84 @@ def test_rope_remap_relative_position_and_norm(orc):
         assert abs(np.linalg.norm(out[0, 0, w]) - np.linalg.norm(x[w])) < 1e-9 * np.linalg.norm(x[w])
     assert abs(out[0, 0, 1] @ out[0, 0, 2] - out[0, 0, 5] @ out[0, 0, 6]) < 1e-9
     assert abs(out[0, 0, 2] @ out[0, 0, 3] - out[0, 0, 9] @ out[0, 0, 10]) < 1e-9
+
+
+# ---------------------------------------------------------------- page summaries (f2(ii))
+
+def _pages_case(B=2, H=6, Hkv=2, d=16, vb=3, nv=48, n_q=1, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    cap = vb + nv + 5
+    q = (torch.randn(B, n_q, H, d, generator=g) * 2).to(torch.bfloat16)
+    K = torch.randn(B, Hkv, cap, d, generator=g).to(torch.bfloat16)
+    return q, K, vb, nv
+
+
+def test_p14_page_retrieval_worked_example(orc):
+    """PAPER.md:527 (Quest) / reading A22: the hand-worked two-page case."""
+    ex = GOLD["P14_page_retrieval"]
+    K = torch.tensor(ex["K_visual"], dtype=torch.float32).view(1, 1, 4, 1).to(torch.bfloat16)
+    kmax, kmin = orc.page_summary(K, 0, 4, ex["page"])
+    assert kmax.ravel().tolist() == [2.0, 3.0] and kmin.ravel().tolist() == [0.0, -1.0]
+    for case in ex["cases"]:
+        q = torch.tensor(case["q"], dtype=torch.float32).view(1, 1, 1, 1).to(torch.bfloat16)
+        idx, sc, _ = orc.retrieve_pages(q, kmax, kmin, case["k_pages"], scale=ex["scale"])
+        assert np.allclose(sc.ravel(), case["scores"], rtol=1e-14, atol=0)
+        assert idx.ravel().tolist() == case["page_idx"]
+
+
+def test_page_summary_is_elementwise_max_min(orc):
+    """The summary is the per-page elementwise max / min (a library reduction)."""
+    q, K, vb, nv = _pages_case()
+    for page in (1, 4, 16):
+        kmax, kmin = orc.page_summary(K, vb, nv, page)
+        vis = K[:, :, vb:vb + nv].float().numpy().astype(np.float64)
+        B, Hkv, _, d = vis.shape
+        r = vis.reshape(B, Hkv, nv // page, page, d)
+        assert np.array_equal(kmax, r.max(axis=3)) and np.array_equal(kmin, r.min(axis=3))
+
+
+@pytest.mark.parametrize("n_q,H,Hkv", [(1, 6, 2), (2, 3, 3), (1, 4, 1)])
+def test_page_one_equals_visual_only_retrieve(orc, n_q, H, Hkv):
+    """page = 1: the bound is the logit itself and the softmax over pages is the softmax
+    over the visual rows -> o_retrieve with VISUAL_ONLY, scores and indices."""
+    q, K, vb, nv = _pages_case(H=H, Hkv=Hkv, n_q=n_q, seed=3 + n_q)
+    seq = torch.full((q.shape[0],), vb + nv + 5, dtype=torch.int32)
+    kmax, kmin = orc.page_summary(K, vb, nv, 1)
+    pi, ps, _ = orc.retrieve_pages(q, kmax, kmin, 7)
+    ri, rs, _ = orc.retrieve(q, K, seq, vb, nv, 7, flags=orc.VISUAL_ONLY)
+    assert np.allclose(ps, rs, rtol=1e-12, atol=0)
+    assert np.array_equal(pi, ri)
+
+
+def test_page_bound_dominates_every_row_logit(orc):
+    """Quest's bound: scale*sum_c max(q kmax, q kmin) >= scale * q.K_j for every row j of
+    the page, with equality when the page's rows are identical (exact logits by torch)."""
+    q, K, vb, nv = _pages_case(B=1, H=2, Hkv=1, d=32, nv=64, seed=9)
+    page = 8
+    K[0, 0, vb + 16:vb + 24] = K[0, 0, vb + 16]  # page 2: identical rows
+    kmax, kmin = orc.page_summary(K, vb, nv, page)
+    scale = 0.25
+    # one head at a time, single page kept per call: the score of a 1-page set is 1, so
+    # read the bound from two pages: score_p / score_0 = exp(ub_p - ub_0)
+    vis = K[0, 0, vb:vb + nv].double()
+    for h in range(2):
+        qh = q[:, :, h:h + 1]
+        _, sc, _ = orc.retrieve_pages(qh, kmax[:, :1], kmin[:, :1], 1, scale=scale)
+        ub_rel = np.log(sc[0, 0]) - np.log(sc[0, 0, 0])  # ub_p - ub_0
+        logits = scale * (vis @ q[0, 0, h].double()).numpy()
+        mx = logits.reshape(nv // page, page).max(axis=1)
+        # ub_p - ub_0 >= ... : compare both sides against page 2 (tight) to remove ub_0
+        tight = mx[2]
+        ub_p = ub_rel - ub_rel[2] + tight
+        assert np.all(ub_p >= mx - 1e-9)
+        assert abs(ub_p[2] - mx[2]) < 1e-9
+
+
+def test_page_retrieval_permutation_equivariant(orc):
+    q, K, vb, nv = _pages_case(B=1, seed=11)
+    page = 4
+    kmax, kmin = orc.page_summary(K, vb, nv, page)
+    perm = np.random.default_rng(1).permutation(nv // page)
+    _, s0, _ = orc.retrieve_pages(q, kmax, kmin, 3)
+    _, s1, _ = orc.retrieve_pages(q, kmax[:, :, perm], kmin[:, :, perm], 3)
+    assert np.allclose(s1, s0[:, :, perm], rtol=1e-12, atol=0)
