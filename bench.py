@@ -267,6 +267,67 @@ def config_rows(graph_of, timed):
     return out
 
 
+def page_row(graph_of, timed, page=16):
+    """retrieval on page summaries (Quest-style, reading A22) on the
+    long-video cache: the summaries are built once per retained cache; per decode step the
+    page scores + top-k pages + the decode over the kept pages' rows.  Recall = the share of
+    the exact fresh step's kept rows that the kept pages contain; err = max |out - exact out|."""
+    import torch
+
+    from paper_2510_17777_b200 import inputs as gen
+    from paper_2510_17777_b200 import svl
+    wl = gen.CONFIGS[WORKLOAD]
+    nl = LAYERS
+    xs = [gen.make_decode_inputs(wl, seed=5000 + l, device="cuda") for l in range(nl)]
+    kp = wl.k // page
+    summ = [svl.page_summary(x["K"], wl.vb, wl.nv, page) for x in xs]
+    pidx = [torch.empty(wl.B, wl.Hkv, kp, dtype=torch.int32, device="cuda") for _ in range(nl)]
+    rows = [torch.empty(wl.B, wl.Hkv, kp * page, dtype=torch.int32, device="cuda") for _ in range(nl)]
+    outs = [torch.empty(wl.B, wl.H, wl.d, device="cuda") for _ in range(nl)]
+    wsr, wsd, wss = svl.Workspace(), svl.Workspace(), svl.Workspace()
+    wsd.get(svl.sparse_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, kp * page, wl.nv, wl.capacity))
+
+    def retr(l):
+        svl.retrieve_pages(xs[l]["q"], summ[l][0], summ[l][1], page, kp, page_idx_out=pidx[l], row_idx_out=rows[l],
+                           ws=wsr)
+
+    def dec(l):
+        svl.sparse_decode_attn(xs[l]["q_dec"], xs[l]["K"], xs[l]["V"], xs[l]["seq_len"], wl.vb, wl.nv, rows[l],
+                               out=outs[l], ws=wsd)
+
+    g_step = graph_of(lambda: [(retr(l), dec(l)) for l in range(nl)])
+    g_retr = graph_of(lambda: [retr(l) for l in range(nl)])
+    g_sum = graph_of(lambda: [svl.page_summary(xs[l]["K"], wl.vb, wl.nv, page, kmax=summ[l][0], kmin=summ[l][1],
+                                               ws=wss) for l in range(nl)])
+    step_us = timed(g_step, 200, 10) * 1e3 / nl
+    retr_us = timed(g_retr, 200, 10) * 1e3 / nl
+    sum_us = timed(g_sum, 50, 5) * 1e3 / nl
+    # quality vs the exact fresh step (same layer 0 inputs)
+    ex_out, ex_idx = svl.fresh_decode_step(xs[0]["q_dec"], xs[0]["K"], xs[0]["V"], xs[0]["seq_len"], wl.vb, wl.nv,
+                                           wl.k)
+    g_step.replay()
+    torch.cuda.synchronize()
+    recall = []
+    for G in range(wl.Hkv):
+        kept = set(rows[0][0, G].tolist())
+        ex = ex_idx[0, G].tolist()
+        recall.append(sum(1 for j in ex if j in kept) / len(ex))
+    err = (outs[0] - ex_out).abs().max().item()
+    b = step_bytes(wl)
+    row = wl.d * 2
+    scored = wl.B * wl.Hkv * (wl.nv // page) * 2 * row
+    dec_bytes = b["decode"] - wl.B * wl.Hkv * wl.k * 2 * row + wl.B * wl.Hkv * kp * page * 2 * row
+    return {"what": "svl_retrieve_pages (page bounds, softmax over pages, top-k pages) + svl_sparse_decode_attn over "
+                    "the kept pages' rows, long-video, 28-layer graph (SURVEY.md 8(f) f2(ii), reading A22)",
+            "page": page, "k_pages": kp, "rows_kept": kp * page,
+            "us_per_layer": step_us, "retrieve_us_per_layer": retr_us,
+            "summary_build_us_per_layer": sum_us, "summary_build_when": "once per retained cache (prefill / round)",
+            "scored_bytes_per_layer": scored, "exact_scored_bytes_per_layer": wl.B * wl.Hkv * wl.nv * row,
+            "step_bytes_per_layer": scored + dec_bytes,
+            "GB_s": (scored + dec_bytes) / (step_us * 1e-6) / 1e9,
+            "recall_vs_exact_topk": recall, "max_abs_out_vs_exact_fresh_step": err}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -979,8 +1040,10 @@ def run_headline(args):
     # ---- the other BASELINE configs as rows: nvila-4k and the multi-turn
     # round (8 rounds of 1 fresh retrieval + 249 steady steps, batch 8)
     rows = None
+    pages = None
     if rank == 0 and world == 1 and not args.profile:
         rows = config_rows(graph_of, timed)
+        pages = page_row(graph_of, timed)
 
     # ---- CPU baseline (rank 0, N=1 only): the oracle on all host cores, and on one thread
     cpu = None
@@ -1033,6 +1096,7 @@ def run_headline(args):
             "question_retrieve": qret,
             "throughput_sweep": sweep,
             "configs": rows,
+            "page_retrieval": pages,
             "cpu_baseline": cpu,
             "e2e": {"value": nbytes["total"] * LAYERS * world / (e2e_ms * 1e-3) / 1e9,
                     "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,

@@ -314,6 +314,45 @@ int32_t svl_fresh_decode_plan(int32_t B, int32_t H, int32_t Hkv, int32_t d, int3
 size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                        int32_t visual_len, int32_t capacity, uint32_t flags);
 
+/* ------------------------------------ page-summary retrieval (Quest-style) */
+/*
+ * svl_page_summary -- per-page key bounds for retrieval on page summaries
+ * (north star "optionally on a page/chunk summary";
+ * PAPER.md:527 Quest "estimates upper-bound attention scores for each page").
+ * For each (b, G) and page p of `page` consecutive visual rows
+ * [vb + p*page, vb + (p+1)*page):
+ *   kmax[b][G][p][c] = max_j K[b,G,j,c],   kmin[b][G][p][c] = min_j K[b,G,j,c]
+ * (bf16, exact).  visual_len % page == 0.  Built once per retained cache.
+ * kmax, kmin  device bf16 [B][Hkv][visual_len/page][d] contiguous, caller-owned.
+ * Workspace: SVL_WORKSPACE_HEADER_BYTES.
+ */
+svl_status svl_page_summary(svl_kv K, int32_t B, int32_t Hkv, int32_t d, svl_span span, int32_t page,
+                            void* kmax, void* kmin, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * svl_retrieve_pages -- query-aware retrieval of whole pages from the page
+ * summaries (reading A22).  For each unit (b, G):
+ *   ub[r,h,p]  = scale * sum_c max(q[b,r,h,c] kmax[p][c], q[b,r,h,c] kmin[p][c])
+ *                (an upper bound of every row logit of page p),
+ *   score[p]   = sum_r sum_h softmax_p(ub[r,h,.])[p]   (softmax over the pages),
+ *   the k_pages pages of largest score (ties -> lower page), ascending.
+ * page = 1 reproduces svl_retrieve with SVL_NORM_VISUAL_ONLY.
+ * q            device bf16 [B][n_q][H][d], n_q * H/Hkv <= 32.
+ * kmax, kmin   svl_page_summary's output, n_pages = visual_len / page.
+ * page_idx_out device int32 [B][Hkv][k_pages] ascending.
+ * row_idx_out  nullable device int32 [B][Hkv][k_pages * page]: the kept pages' visual
+ *              rows ascending, relative to vb -- svl_sparse_decode_attn's vis_idx
+ *              with k = k_pages * page.
+ * scores_out   nullable device fp32 [B][Hkv][n_pages].
+ * flags        0.  Workspace: svl_retrieve_pages_workspace_size.
+ */
+svl_status svl_retrieve_pages(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                              const void* kmax, const void* kmin, int32_t n_pages, int32_t page, int32_t k_pages,
+                              float scale, uint32_t flags, int32_t* page_idx_out, int32_t* row_idx_out,
+                              float* scores_out, void* workspace, size_t workspace_bytes, void* stream);
+
+size_t svl_retrieve_pages_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t n_pages);
+
 /* ----------------------------------------------------- prefill companion */
 /*
  * svl_prefill_prune -- query-agnostic per-frame pruning (PAPER.md:113,

@@ -757,6 +757,104 @@ svl_status svl_fresh_decode_step(const void* q, int32_t B, int32_t H, int32_t Hk
     return SVL_OK;
 }
 
+// ------------------------------------------------- page summaries (f2(ii))
+svl_status svl_page_summary(svl_kv K, int32_t B, int32_t Hkv, int32_t d, svl_span span, int32_t page,
+                            void* kmax, void* kmin, void* ws, size_t ws_bytes, void* stream) {
+    if (!kmax || !kmin) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (B < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, Hkv must be >= 1%s");
+    if (page < 1) return fail(SVL_ERR_INVALID_ARGUMENT, "page must be >= 1%s");
+    if (span.visual_len < 1 || span.visual_len % page)
+        return fail(SVL_ERR_SHAPE, "visual_len must be a positive multiple of page%s");
+    if (span.visual_begin < 0 || (int64_t)span.visual_begin + span.visual_len > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span outside the KV capacity%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    if (!aligned16(kmax) || !aligned16(kmin)) return fail(SVL_ERR_ALIGNMENT, "kmax / kmin not 16-byte aligned%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws) || ws_bytes < kWsHeader) return fail(SVL_ERR_WORKSPACE, "workspace NULL, misaligned or too small%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+    PageSumParams p;
+    p.K = static_cast<const uint16_t*>(K.data);
+    p.ksb = K.stride_b; p.ksh = K.stride_h; p.kst = K.stride_t;
+    p.units = B * Hkv; p.Hkv = Hkv; p.d = d; p.vb = span.visual_begin; p.page = page;
+    p.np = span.visual_len / page;
+    p.kmax = static_cast<uint16_t*>(kmax);
+    p.kmin = static_cast<uint16_t*>(kmin);
+    cudaError_t e = launch_page_summary(p, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_page_summary");
+    return SVL_OK;
+}
+
+struct PagesLayout {
+    size_t ub2, scores, total;
+};
+static PagesLayout pages_layout(int units, int NC, int n_pages) {
+    PagesLayout l;
+    l.ub2 = kWsHeader;
+    l.scores = round_up(l.ub2 + (size_t)units * NC * n_pages * sizeof(float), 256);
+    l.total = round_up(l.scores + (size_t)units * n_pages * sizeof(float), 256);
+    return l;
+}
+
+size_t svl_retrieve_pages_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t n_pages) {
+    if (B < 1 || n_q < 1 || Hkv < 1 || H % Hkv || n_pages < 1) return 0;
+    return pages_layout(B * Hkv, n_q * (H / Hkv), n_pages).total;
+}
+
+svl_status svl_retrieve_pages(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                              const void* kmax, const void* kmin, int32_t n_pages, int32_t page, int32_t k_pages,
+                              float scale, uint32_t flags, int32_t* page_idx_out, int32_t* row_idx_out,
+                              float* scores_out, void* ws, size_t ws_bytes, void* stream) {
+    if (!q || !kmax || !kmin || (!page_idx_out && k_pages > 0))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (B < 1 || n_q < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, n_q, H, Hkv must be >= 1%s");
+    if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
+    if (n_pages < 1 || page < 1) return fail(SVL_ERR_SHAPE, "n_pages and page must be >= 1%s");
+    if (k_pages < 0 || k_pages > n_pages) return fail(SVL_ERR_INVALID_ARGUMENT, "k_pages outside [0, n_pages]%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    const int g = H / Hkv;
+    if (n_q * g > 32) return fail(SVL_ERR_UNSUPPORTED, "page retrieval needs n_q * g <= 32%s");
+    if (n_pages > 16 * kSelectThreads * kSelectMaxPerThread) return fail(SVL_ERR_UNSUPPORTED, "n_pages > 131072%s");
+    if (!aligned16(q) || !aligned16(kmax) || !aligned16(kmin)) return fail(SVL_ERR_ALIGNMENT, "q / kmax / kmin not 16-byte aligned%s");
+    const int units = B * Hkv;
+    PagesLayout lay = pages_layout(units, n_q * g, n_pages);
+    if (!ws || !aligned16(ws) || ws_bytes < lay.total) return fail(SVL_ERR_WORKSPACE, "workspace NULL, misaligned or too small%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    cudaStream_t s = (cudaStream_t)stream;
+    PageRetrParams p;
+    p.q = static_cast<const uint16_t*>(q);
+    p.kmax = static_cast<const uint16_t*>(kmax);
+    p.kmin = static_cast<const uint16_t*>(kmin);
+    p.units = units; p.n_q = n_q; p.H = H; p.Hkv = Hkv; p.g = g; p.NC = n_q * g; p.d = d; p.np = n_pages;
+    p.scale2 = scale * kLog2e;
+    p.ub2 = reinterpret_cast<float*>(w + lay.ub2);
+    p.scores = scores_out ? scores_out : reinterpret_cast<float*>(w + lay.scores);
+    cudaError_t e = launch_page_scores(p, s);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve_pages/scores");
+    if (k_pages == 0) return SVL_OK;
+    SelectParams se = {};
+    se.mode = 2;
+    se.scores_in = p.scores;
+    se.Hkv = Hkv;
+    se.shared = 0;
+    se.nv = n_pages; se.k = k_pages;
+    se.idx_out = page_idx_out;
+    se.flags = reinterpret_cast<uint32_t*>(w);
+    se.CS = select_cluster_size(n_pages);
+    e = launch_select(se, units, s);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve_pages/select");
+    if (row_idx_out) {
+        e = launch_page_expand(page_idx_out, units, k_pages, page, row_idx_out, s);
+        if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve_pages/expand");
+    }
+    return SVL_OK;
+}
+
 // ---------------------------------------------------------------- prune
 size_t svl_prune_workspace_size(int32_t B, int32_t N, int32_t n_frames) {
     (void)B;

@@ -163,6 +163,26 @@ struct PackParams {
     uint32_t* flags;
 };
 cudaError_t launch_pack(const PackParams& p, int d, int max_rows, cudaStream_t s);
+// ------------------------------------- page summaries
+struct PageSumParams {
+    const uint16_t* K;
+    int64_t ksb, ksh, kst;
+    int units, Hkv, d, vb, page, np;
+    uint16_t* kmax;  // [units][np][d]
+    uint16_t* kmin;
+};
+struct PageRetrParams {
+    const uint16_t* q;  // [B][n_q][H][d]
+    const uint16_t* kmax;
+    const uint16_t* kmin;
+    int units, n_q, H, Hkv, g, NC, d, np;
+    float scale2;
+    float* ub2;     // [units][NC][np] base-2 page bounds (workspace)
+    float* scores;  // [units][np]
+};
+cudaError_t launch_page_summary(const PageSumParams& p, cudaStream_t s);
+cudaError_t launch_page_scores(const PageRetrParams& p, cudaStream_t s);
+cudaError_t launch_page_expand(const int32_t* pidx, int units, int kp, int page, int32_t* rows, cudaStream_t s);
 // -------------------------------------------- RoPE remap
 struct RopeParams {
     const uint16_t* K;  // pre-RoPE keys

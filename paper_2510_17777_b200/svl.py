@@ -42,7 +42,8 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_salience", "svl_salience_workspace_size", "svl_keep_budget", "svl_workspace_init",
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
            "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
-           "svl_wait_flags", "svl_pack_kv", "svl_rope_remap", "svl_fresh_decode_plan"]
+           "svl_wait_flags", "svl_pack_kv", "svl_rope_remap", "svl_fresh_decode_plan",
+           "svl_page_summary", "svl_retrieve_pages", "svl_retrieve_pages_workspace_size"]
 
 
 class SvlError(RuntimeError):
@@ -96,6 +97,13 @@ def lib():
         L.svl_fresh_decode_step.restype = ctypes.c_int
         L.svl_fresh_decode_step.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, I32,
                                             F, U32, P, P, P, P, SZ, P]
+        L.svl_page_summary.restype = ctypes.c_int
+        L.svl_page_summary.argtypes = [svl_kv, I32, I32, I32, svl_span, I32, P, P, P, SZ, P]
+        L.svl_retrieve_pages.restype = ctypes.c_int
+        L.svl_retrieve_pages.argtypes = [P, I32, I32, I32, I32, I32, P, P, I32, I32, I32, ctypes.c_float, U32,
+                                         P, P, P, P, SZ, P]
+        L.svl_retrieve_pages_workspace_size.restype = SZ
+        L.svl_retrieve_pages_workspace_size.argtypes = [I32, I32, I32, I32, I32]
         L.svl_fresh_decode_plan.restype = ctypes.c_int
         L.svl_fresh_decode_plan.argtypes = [I32, I32, I32, I32, I32, I32, U32]
         L.svl_fresh_decode_workspace_size.restype = SZ
@@ -443,3 +451,48 @@ def salience(Qe: torch.Tensor, Ke: torch.Tensor, S: int, mode: int,
 
 def version() -> str:
     return lib().svl_version().decode()
+
+
+def page_summary(K: torch.Tensor, visual_begin: int, visual_len: int, page: int,
+                 kmax: Optional[torch.Tensor] = None, kmin: Optional[torch.Tensor] = None,
+                 ws: Optional[Workspace] = None, stream=None):
+    """svl_page_summary.  K bf16 [B][Hkv][cap][d] -> (kmax, kmin) bf16 [B][Hkv][visual_len/page][d]."""
+    B, Hkv, _, d = K.shape
+    npg = visual_len // page
+    if kmax is None:
+        kmax = torch.empty(B, Hkv, npg, d, dtype=torch.bfloat16, device=K.device)
+    if kmin is None:
+        kmin = torch.empty(B, Hkv, npg, d, dtype=torch.bfloat16, device=K.device)
+    w = _ws(ws, K.device).get(WORKSPACE_HEADER_BYTES)
+    seq = torch.full((B,), visual_begin + visual_len, dtype=torch.int32, device=K.device)
+    _check(lib().svl_page_summary(kv_view(K, "K"), B, Hkv, d, span(visual_begin, visual_len, seq), page,
+                                  _cuda(kmax, "kmax", torch.bfloat16), _cuda(kmin, "kmin", torch.bfloat16),
+                                  w.data_ptr(), w.numel(), _stream(stream)))
+    return kmax, kmin
+
+
+def retrieve_pages(q: torch.Tensor, kmax: torch.Tensor, kmin: torch.Tensor, page: int, k_pages: int,
+                   scale: Optional[float] = None, page_idx_out: Optional[torch.Tensor] = None,
+                   row_idx_out: Optional[torch.Tensor] = None, scores_out: Optional[torch.Tensor] = None,
+                   want_rows: bool = True, ws: Optional[Workspace] = None, stream=None):
+    """svl_retrieve_pages.  q bf16 [B][n_q][H][d].  Returns (page_idx [B][Hkv][k_pages],
+    rows [B][Hkv][k_pages * page] or None)."""
+    B, n_q, H, d = q.shape
+    _, Hkv, npg, _ = kmax.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if not (q.is_contiguous() and kmax.is_contiguous() and kmin.is_contiguous()):
+        raise ValueError("q, kmax, kmin must be contiguous")
+    if page_idx_out is None:
+        page_idx_out = torch.empty(B, Hkv, k_pages, dtype=torch.int32, device=q.device)
+    if row_idx_out is None and want_rows:
+        row_idx_out = torch.empty(B, Hkv, k_pages * page, dtype=torch.int32, device=q.device)
+    w = _ws(ws, q.device).get(lib().svl_retrieve_pages_workspace_size(B, n_q, H, Hkv, npg))
+    _check(lib().svl_retrieve_pages(
+        q.data_ptr(), B, n_q, H, Hkv, d, _cuda(kmax, "kmax", torch.bfloat16), _cuda(kmin, "kmin", torch.bfloat16),
+        npg, page, k_pages, scale, 0, _cuda(page_idx_out, "page_idx_out", torch.int32),
+        _cuda(row_idx_out, "row_idx_out", torch.int32) if row_idx_out is not None else None,
+        _cuda(scores_out, "scores_out", torch.float32) if scores_out is not None else None,
+        w.data_ptr(), w.numel(), _stream(stream)))
+    return page_idx_out, row_idx_out
