@@ -63,6 +63,10 @@ def lib():
         L.o_prune.restype = I
         L.o_prune.argtypes = [P, I, I, P, I, D, P, I, P]
         L.o_rope_remap.argtypes = [P, I, I, I, I, P, I, I, P, I, D, P, I, P]
+        L.o_mrope_plan.restype = I
+        L.o_mrope_plan.argtypes = [P, I, I, I, P, I, P, P]
+        L.o_mrope_remap.restype = I
+        L.o_mrope_remap.argtypes = [P, I, I, I, I, P, I, I, P, I, P, P, P, D, P, I, P]
         L.o_page_summary.restype = I
         L.o_page_summary.argtypes = [P, I, I, I, I64, I64, I64, I, I, I, P, P]
         L.o_retrieve_pages.restype = I
@@ -256,3 +260,37 @@ def pages_to_rows(page_idx, page: int):
     pi = np.asarray(page_idx, dtype=np.int64)
     rows = pi[..., :, None] * page + np.arange(page)[None, :]
     return rows.reshape(*pi.shape[:-1], pi.shape[-1] * page).astype(np.int32)
+
+
+def mrope_plan(coords, vb: int, kept):
+    """mRoPE remap plan (SURVEY.md 8(f) f4(i), reading A23).  coords int [B][nv][3] (t, h, w);
+    kept int [B][k] ascending.  Returns (new_coords int32 [B][k][3], text_start int32 [B])."""
+    c = np.ascontiguousarray(np.asarray(coords, dtype=np.int32))
+    kp = np.ascontiguousarray(np.asarray(kept, dtype=np.int32))
+    B, nv, _ = c.shape
+    k = kp.shape[-1]
+    nc = np.zeros((B, k, 3), np.int32)
+    ts = np.zeros((B,), np.int32)
+    rc = lib().o_mrope_plan(_ptr(c), B, nv, vb, _ptr(kp), k, _ptr(nc), _ptr(ts))
+    _check(rc, "o_mrope_plan")
+    return nc, ts
+
+
+def mrope_remap(K_pre, seq_len, vb: int, nv: int, kept, new_coords, text_start, sections, base: float,
+                cap_out: int | None = None):
+    """Apply the mRoPE plan (reading A23).  Returns (K_post float64 [B][Hkv][cap_out][d], rows)."""
+    Kc = K_pre.contiguous()
+    B, Hkv, cap, d = Kc.shape
+    kp = np.ascontiguousarray(np.asarray(kept, dtype=np.int32))
+    k = kp.shape[-1]
+    sl = np.ascontiguousarray(np.asarray(seq_len, dtype=np.int32))
+    nc = np.ascontiguousarray(np.asarray(new_coords, dtype=np.int32))
+    ts = np.ascontiguousarray(np.asarray(text_start, dtype=np.int32))
+    sec = np.ascontiguousarray(np.asarray(sections, dtype=np.int32))
+    cap_out = cap - nv + k if cap_out is None else cap_out
+    out = np.zeros((B, Hkv, cap_out, d), np.float64)
+    rows = np.zeros((B, cap_out), np.int32)
+    rc = lib().o_mrope_remap(_ptr(_u16(Kc)), B, Hkv, d, cap, _ptr(sl), vb, nv, _ptr(kp), k, _ptr(nc), _ptr(ts),
+                             _ptr(sec), base, _ptr(out), cap_out, _ptr(rows))
+    _check(rc, "o_mrope_remap")
+    return out, rows

@@ -571,3 +571,111 @@ int o_retrieve_pages(const uint16_t* q, int B, int n_q, int H, int Hkv, int d, c
     free(score);
     return err;
 }
+
+/*
+ * o_mrope_plan -- multimodal-RoPE remap plan after pruning (SURVEY.md 8(f)
+ * f4(i); "reconstruct the minimal contiguous positional grid along
+ * temporal, height, and width dimensions and then shift subsequent text
+ * positions to maintain global continuity"; SPEC.md:428-433 remap_mrope;
+ * reading A23).  Per batch row b, for each dimension x in (t, h, w)
+ * independently: the distinct values of the kept tokens' coordinates, ranked
+ * in increasing order (coordinate compression): x' = #{distinct kept values < x}.
+ * Positions are offset by the text before the visual span: the kept token's
+ * position in dimension x is vb + x'; the first later text token takes the
+ * scalar position text_start = vb + 1 + max over kept tokens of max(t', h', w')
+ * (Qwen-style continuation; 0-kept: vb).
+ * coords: [B][nv][3] (t, h, w) of the original visual rows, each >= 0.
+ * kept: [B][k] ascending in [0, nv).  Outputs new_coords [B][k][3] (t', h', w')
+ * and text_start [B].  Duplicate kept triples -> O_ERR_ARG.
+ */
+int o_mrope_plan(const int32_t* coords, int B, int nv, int vb, const int32_t* kept, int k, int32_t* new_coords,
+                 int32_t* text_start) {
+    if (B < 1 || nv < 0 || vb < 0 || k < 0 || k > nv) return O_ERR_ARG;
+    for (int b = 0; b < B; ++b) {
+        const int32_t* kb = kept + (int64_t)b * k;
+        for (int i = 0; i < k; ++i)
+            if (kb[i] < 0 || kb[i] >= nv || (i > 0 && kb[i - 1] >= kb[i])) return O_ERR_ORDER;
+        /* duplicate triples (brute force) */
+        for (int i = 0; i < k; ++i)
+            for (int j = i + 1; j < k; ++j) {
+                const int32_t* a = coords + ((int64_t)b * nv + kb[i]) * 3;
+                const int32_t* c = coords + ((int64_t)b * nv + kb[j]) * 3;
+                if (a[0] == c[0] && a[1] == c[1] && a[2] == c[2]) return O_ERR_ARG;
+            }
+        int32_t mx = -1;
+        for (int x = 0; x < 3; ++x)
+            for (int i = 0; i < k; ++i) {
+                const int32_t v = coords[((int64_t)b * nv + kb[i]) * 3 + x];
+                if (v < 0) return O_ERR_ARG;
+                /* rank = number of distinct kept values in this dimension below v */
+                int32_t r = 0;
+                for (int j = 0; j < k; ++j) {
+                    const int32_t u = coords[((int64_t)b * nv + kb[j]) * 3 + x];
+                    if (u >= v) continue;
+                    int first = 1; /* count u once: only at its first occurrence */
+                    for (int jj = 0; jj < j; ++jj)
+                        if (coords[((int64_t)b * nv + kb[jj]) * 3 + x] == u) first = 0;
+                    r += first;
+                }
+                new_coords[((int64_t)b * k + i) * 3 + x] = r;
+                if (r > mx) mx = r;
+            }
+        text_start[b] = (k > 0) ? vb + 1 + mx : vb;
+    }
+    return 0;
+}
+
+/*
+ * o_mrope_remap -- apply the plan to the cache (post-RoPE keys are
+ * recomputed from the stored pre-RoPE keys; reading A23).  Output rows as in
+ * o_rope_remap: [0, vb) system text, [vb, vb + k) kept visual, then the later
+ * text rows.  Rotate-half pairs (c, c + d/2); pair c takes the position of its
+ * section: c < sec[0] -> t, c < sec[0] + sec[1] -> h, else w; text rows use
+ * their scalar position on every section (system row w: w; later text row i:
+ * text_start + i).  theta_c = pos * base^(-2c/d), all in double.
+ */
+int o_mrope_remap(const uint16_t* Kpre, int B, int Hkv, int d, int cap, const int32_t* seq_len, int vb, int nv,
+                  const int32_t* kept, int k, const int32_t* new_coords, const int32_t* text_start,
+                  const int32_t* sec, double base, double* Kout, int cap_out, int32_t* rows_out) {
+    if (B < 1 || Hkv < 1 || d < 2 || (d & 1) || vb < 0 || nv < 0 || k < 0 || k > nv || !(base > 1.0))
+        return O_ERR_ARG;
+    if (sec[0] < 0 || sec[1] < 0 || sec[2] < 0 || sec[0] + sec[1] + sec[2] != d / 2) return O_ERR_ARG;
+    for (int b = 0; b < B; ++b) {
+        const int L = seq_len[b];
+        if (L < vb + nv || L > cap) return O_ERR_SHAPE;
+        const int n_out = vb + k + (L - vb - nv);
+        if (n_out > cap_out) return O_ERR_SHAPE;
+        for (int w = 0; w < cap_out; ++w) {
+            int old = -1;
+            double pos[3] = {0.0, 0.0, 0.0};
+            if (w < vb) {
+                old = w;
+                pos[0] = pos[1] = pos[2] = (double)w;
+            } else if (w < vb + k) {
+                const int i = w - vb;
+                old = vb + kept[(int64_t)b * k + i];
+                for (int x = 0; x < 3; ++x) pos[x] = (double)(vb + new_coords[((int64_t)b * k + i) * 3 + x]);
+            } else if (w < n_out) {
+                old = w - k + nv;
+                pos[0] = pos[1] = pos[2] = (double)(text_start[b] + (w - vb - k));
+            }
+            rows_out[(int64_t)b * cap_out + w] = old;
+            for (int G = 0; G < Hkv; ++G) {
+                double* o = Kout + (((int64_t)b * Hkv + G) * cap_out + w) * d;
+                if (old < 0) {
+                    for (int c = 0; c < d; ++c) o[c] = 0.0;
+                    continue;
+                }
+                const uint16_t* xk = Kpre + (((int64_t)b * Hkv + G) * cap + old) * d;
+                for (int c = 0; c < d / 2; ++c) {
+                    const int x = (c < sec[0]) ? 0 : (c < sec[0] + sec[1]) ? 1 : 2;
+                    const double theta = pos[x] * pow(base, -2.0 * (double)c / (double)d);
+                    const double x1 = bf(xk[c]), x2 = bf(xk[c + d / 2]);
+                    o[c] = x1 * cos(theta) - x2 * sin(theta);
+                    o[c + d / 2] = x2 * cos(theta) + x1 * sin(theta);
+                }
+            }
+        }
+    }
+    return 0;
+}

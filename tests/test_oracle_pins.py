@@ -558,3 +558,87 @@ def test_page_retrieval_permutation_equivariant(orc):
     _, s0, _ = orc.retrieve_pages(q, kmax, kmin, 3)
     _, s1, _ = orc.retrieve_pages(q, kmax[:, :, perm], kmin[:, :, perm], 3)
     assert np.allclose(s1, s0[:, :, perm], rtol=1e-12, atol=0)
+
+
+# ---------------------------------------------------------------- mRoPE remap (f4(i))
+
+def _grid_coords(T, Hh, Ww):
+    t, h, w = np.meshgrid(np.arange(T), np.arange(Hh), np.arange(Ww), indexing="ij")
+    return np.stack([t.ravel(), h.ravel(), w.ravel()], axis=-1).astype(np.int32)
+
+
+def test_p15_mrope_plan_spec_example(orc):
+    ex = GOLD["P15_mrope_plan"]
+    coords = np.array(ex["kept_coords"], np.int32)[None]
+    nc, ts = orc.mrope_plan(coords, ex["vb"], np.arange(4, dtype=np.int32)[None])
+    assert nc[0].tolist() == ex["new_coords"] and int(ts[0]) == ex["text_start"]
+
+
+def test_mrope_plan_full_grid_is_identity(orc):
+    coords = _grid_coords(3, 4, 5)[None]
+    n = coords.shape[1]
+    nc, ts = orc.mrope_plan(coords, 7, np.arange(n, dtype=np.int32)[None])
+    assert np.array_equal(nc, coords) and int(ts[0]) == 7 + 1 + 4
+
+
+def test_mrope_plan_rank_compression_injective_idempotent(orc):
+    """Per dimension the plan is numpy's unique-inverse (coordinate compression); distinct
+    triples stay distinct over random prunings (SPEC.md:433); re-planning is the identity;
+    the text start exceeds every remapped position."""
+    rng = np.random.default_rng(0)
+    coords = _grid_coords(6, 5, 7)[None]
+    n = coords.shape[1]
+    for _ in range(200):
+        k = int(rng.integers(1, n))
+        kept = np.sort(rng.choice(n, k, replace=False)).astype(np.int32)[None]
+        nc, ts = orc.mrope_plan(coords, 3, kept)
+        kc = coords[0, kept[0]]
+        for x in range(3):
+            _, inv = np.unique(kc[:, x], return_inverse=True)
+            assert np.array_equal(nc[0, :, x], inv)
+        assert len({tuple(r) for r in nc[0]}) == k
+        nc2, ts2 = orc.mrope_plan(nc, 3, np.arange(k, dtype=np.int32)[None])
+        assert np.array_equal(nc2, nc) and ts2[0] == ts[0]
+        assert ts[0] > 3 + nc.max()
+
+
+def test_mrope_plan_rejects_duplicate_triples(orc):
+    coords = np.array([[[0, 0, 0], [0, 0, 0], [1, 0, 0]]], np.int32)
+    with pytest.raises(orc.OracleError):
+        orc.mrope_plan(coords, 0, np.array([[0, 1]], np.int32))
+
+
+def test_mrope_diagonal_coords_equal_unified_rope(orc):
+    """Kept tokens on the diagonal (i, i, i): every section sees position vb + rank, the
+    text start is vb + k -- exactly the unified remap (o_rope_remap), bitwise in fp64."""
+    g = torch.Generator().manual_seed(4)
+    B, Hkv, d, vb, nv, ta = 1, 2, 16, 3, 20, 4
+    cap = vb + nv + ta
+    K = torch.randn(B, Hkv, cap, d, generator=g).to(torch.bfloat16)
+    seq = np.array([cap], np.int32)
+    coords = np.stack([np.arange(nv)] * 3, axis=-1).astype(np.int32)[None]
+    kept = np.array([[1, 4, 5, 9, 15, 19]], np.int32)
+    nc, ts = orc.mrope_plan(coords, vb, kept)
+    a, ra = orc.mrope_remap(K, seq, vb, nv, kept, nc, ts, [2, 3, 3], 10000.0)
+    b, rb = orc.rope_remap(K, seq, vb, nv, kept, 10000.0)
+    assert np.array_equal(ra, rb) and np.array_equal(a, b)
+
+
+def test_mrope_relative_position_property(orc):
+    """Shifting every position by a common constant (here: 4 more system rows) leaves the
+    dot products between re-rotated kept visual keys unchanged (RoPE's relative-position
+    property per section, 1e-9)."""
+    g = torch.Generator().manual_seed(6)
+    Hkv, d, nv, ta = 1, 24, 30, 2
+    coords = _grid_coords(2, 3, 5)[None]
+    kept = np.array([[0, 3, 7, 8, 14, 22, 29]], np.int32)
+    outs = []
+    for vb in (2, 6):
+        cap = vb + nv + ta
+        Kfull = torch.randn(1, Hkv, 6 + nv + ta, d, generator=torch.Generator().manual_seed(6)).to(torch.bfloat16)
+        K = torch.cat([Kfull[:, :, :vb], Kfull[:, :, 6:]], dim=2)  # same visual / text keys, vb system rows
+        nc, ts = orc.mrope_plan(coords, vb, kept)
+        o, _ = orc.mrope_remap(K, np.array([cap], np.int32), vb, nv, kept, nc, ts, [4, 4, 4], 10000.0)
+        vis = o[0, 0, vb:vb + kept.shape[1]]
+        outs.append(vis @ vis.T)
+    assert np.allclose(outs[0], outs[1], rtol=0, atol=1e-9)
