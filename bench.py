@@ -966,7 +966,20 @@ def run_headline(args):
         prefill.update({"rope_remap_us": ms_rope * 1e3, "rope_remap_GB_s": rope_bytes / (ms_rope * 1e-3) / 1e9,
                         "rope_remap_what": f"svl_rope_remap: {nvp} visual -> {kp_} kept + {rw.vb + rw.t_after} "
                                            f"text rows, {rw.Hkv} KV heads, d {rw.d}, base 1e6 (SURVEY 8(f) f4(i))"})
-        del Kpre, Vpre, Kro, Vro
+        # f4(i), multimodal RoPE: the same kept set on a 256-frame x 16 x 32 grid, Qwen2-VL sections
+        tt, hh, ww = torch.meshgrid(torch.arange(pw.F), torch.arange(16), torch.arange(pw.Nf // 16), indexing="ij")
+        coords = torch.stack([tt.reshape(-1), hh.reshape(-1), ww.reshape(-1)], -1).to(torch.int32).view(1, -1, 3).to(dev)
+        ws_m = svl.Workspace(dev)
+        Kmo, Vmo, _, _ = svl.mrope_remap(Kpre, Vpre, seqr, rw.vb, nvp, coords, kept_rel, 1000000.0, (16, 24, 24),
+                                         ws=ws_m)
+        g_mrope = graph_of(lambda: svl.mrope_remap(Kpre, Vpre, seqr, rw.vb, nvp, coords, kept_rel, 1000000.0,
+                                                   (16, 24, 24), K_out=Kmo, V_out=Vmo, ws=ws_m))
+        ms_mrope = timed(g_mrope, 50, 5)
+        prefill.update({"mrope_remap_us": ms_mrope * 1e3, "mrope_remap_GB_s": rope_bytes / (ms_mrope * 1e-3) / 1e9,
+                        "mrope_remap_what": "svl_mrope_remap: plan (per-dimension rank compression of the kept "
+                                            "(t,h,w)) + sectioned re-rotation, 256 x 16 x 32 grid, sections "
+                                            "(16, 24, 24) (SURVEY 8(f) f4(i), reading A23)"})
+        del Kpre, Vpre, Kro, Vro, Kmo, Vmo
 
     # ---- question-chunk retrieval on tcgen05: svl_retrieve
     # with n_q question rows on the long-video cache, FULL_PREFIX normalisation computed in-kernel

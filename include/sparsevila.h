@@ -212,6 +212,38 @@ svl_status svl_rope_remap(svl_kv K_pre, svl_kv V, int32_t B, int32_t Hkv, int32_
                           void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * svl_mrope_remap -- multimodal-RoPE remap after prefill pruning (SURVEY.md 8(f)
+ * f4(i); "reconstruct the minimal contiguous positional grid along
+ * temporal, height, and width dimensions and then shift subsequent text
+ * positions to maintain global continuity"; reading A23).
+ * Plan, per batch row b and dimension x in (t, h, w) independently: the kept
+ * tokens' coordinate x is replaced by its rank among the distinct kept values
+ * (coordinate compression, order-preserving).  Positions: kept visual token
+ * (t', h', w') -> (vb + t', vb + h', vb + w'); system rows keep w; the later
+ * text rows continue at text_start = vb + 1 + max over kept of max(t', h', w').
+ * Output rows as svl_rope_remap: [0, vb) system, [vb, vb + k) kept visual, then
+ * the later text rows.  Rotate-half pairs (c, c + d/2); pair c uses the t
+ * position for c < sections[0], h for c < sections[0] + sections[1], else w;
+ * theta = pos * rope_base^(-2c/d) in double; bf16 RNE output; V compacted.
+ *
+ * coords   device int32 [B][visual_len][3] (t, h, w) of the original visual rows,
+ *          each in [0, 65536); out-of-range values / a kept list that is not
+ *          strictly ascending raise SVL_DEVFLAG_INDEX (clamped).  Duplicate kept
+ *          triples are a precondition violation (not detected on the device).
+ * kept     device int32 [B][k] ascending in [0, visual_len).
+ * sections HOST int32 [3]: rotary pairs per section, sum d/2, first two even
+ *          (Qwen2-VL at d = 128: {16, 24, 24}).
+ * new_coords_out nullable device int32 [B][k][3]; text_start_out nullable device int32 [B].
+ * Workspace: svl_mrope_remap_workspace_size(B, k).
+ */
+svl_status svl_mrope_remap(svl_kv K_pre, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
+                           const int32_t* coords, const int32_t* kept, int32_t k, double rope_base,
+                           const int32_t* sections, svl_kv K_out, svl_kv V_out, int32_t* new_coords_out,
+                           int32_t* text_start_out, void* workspace, size_t workspace_bytes, void* stream);
+
+size_t svl_mrope_remap_workspace_size(int32_t B, int32_t k);
+
+/*
  * svl_pack_kv -- pack-once of the retained KV cache (
  * PAPER.md:124 "compactly packed into a contiguous memory region";
  * SPEC.md:315-323).  For every unit (b, G) writes into the packed views Kp, Vp:

@@ -603,23 +603,31 @@ int o_mrope_plan(const int32_t* coords, int B, int nv, int vb, const int32_t* ke
                 if (a[0] == c[0] && a[1] == c[1] && a[2] == c[2]) return O_ERR_ARG;
             }
         int32_t mx = -1;
-        for (int x = 0; x < 3; ++x)
+        int32_t* vals = (int32_t*)malloc(sizeof(int32_t) * (size_t)(k > 0 ? k : 1));
+        if (!vals) return O_ERR_NOMEM;
+        for (int x = 0; x < 3; ++x) {
+            /* the distinct kept values of this dimension, ascending (sort + unique) */
+            for (int i = 0; i < k; ++i) {
+                vals[i] = coords[((int64_t)b * nv + kb[i]) * 3 + x];
+                if (vals[i] < 0) {
+                    free(vals);
+                    return O_ERR_ARG;
+                }
+            }
+            qsort(vals, (size_t)k, sizeof(int32_t), cmp_i32);
+            int nd = 0;
+            for (int i = 0; i < k; ++i)
+                if (i == 0 || vals[i] != vals[i - 1]) vals[nd++] = vals[i];
+            /* rank = number of distinct kept values below v = its position in vals */
             for (int i = 0; i < k; ++i) {
                 const int32_t v = coords[((int64_t)b * nv + kb[i]) * 3 + x];
-                if (v < 0) return O_ERR_ARG;
-                /* rank = number of distinct kept values in this dimension below v */
                 int32_t r = 0;
-                for (int j = 0; j < k; ++j) {
-                    const int32_t u = coords[((int64_t)b * nv + kb[j]) * 3 + x];
-                    if (u >= v) continue;
-                    int first = 1; /* count u once: only at its first occurrence */
-                    for (int jj = 0; jj < j; ++jj)
-                        if (coords[((int64_t)b * nv + kb[jj]) * 3 + x] == u) first = 0;
-                    r += first;
-                }
+                while (r < nd && vals[r] < v) ++r;
                 new_coords[((int64_t)b * k + i) * 3 + x] = r;
                 if (r > mx) mx = r;
             }
+        }
+        free(vals);
         text_start[b] = (k > 0) ? vb + 1 + mx : vb;
     }
     return 0;

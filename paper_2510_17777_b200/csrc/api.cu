@@ -550,6 +550,67 @@ svl_status svl_rope_remap(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d,
     return SVL_OK;
 }
 
+size_t svl_mrope_remap_workspace_size(int32_t B, int32_t k) {
+    if (B < 1 || k < 0) return 0;
+    return round_up(kWsHeader + (size_t)B * 3 * sizeof(int32_t), 256) + round_up((size_t)B * k * 3 * sizeof(int32_t), 256);
+}
+
+svl_status svl_mrope_remap(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
+                           const int32_t* coords, const int32_t* kept, int32_t k, double rope_base,
+                           const int32_t* sections, svl_kv Ko, svl_kv Vo, int32_t* new_coords_out,
+                           int32_t* text_start_out, void* ws, size_t ws_bytes, void* stream) {
+    if (!span.seq_len || (k > 0 && (!kept || !coords)) || !K.data || !Ko.data || (V.data && !Vo.data) || !sections)
+        return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (B < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, Hkv must be >= 1%s");
+    if (!(rope_base > 1.0) || !isfinite(rope_base)) return fail(SVL_ERR_INVALID_ARGUMENT, "rope_base must be finite > 1%s");
+    if (span.visual_begin < 0 || span.visual_len < 0 ||
+        (int64_t)span.visual_begin + span.visual_len > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span outside the KV capacity%s");
+    if (k < 0 || k > span.visual_len) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, visual_len]%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    if (sections[0] < 0 || sections[1] < 0 || sections[2] < 0 || sections[0] + sections[1] + sections[2] != d / 2 ||
+        (sections[0] & 1) || (sections[1] & 1))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "sections must be >= 0, sum to d/2, the first two even%s");
+    const int64_t need = (int64_t)span.visual_begin + k + (K.capacity - span.visual_begin - span.visual_len);
+    if (Ko.capacity < need || (V.data && Vo.capacity < need))
+        return fail(SVL_ERR_SHAPE, "output capacity < vb + k + (capacity - vb - N_v)%s");
+    if (V.data && V.capacity != K.capacity) return fail(SVL_ERR_SHAPE, "K and V capacities differ%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K_pre");
+    if (st == SVL_OK) st = check_kv(Ko, B, Hkv, d, "K_out");
+    if (st == SVL_OK && V.data) st = check_kv(V, B, Hkv, d, "V");
+    if (st == SVL_OK && V.data) st = check_kv(Vo, B, Hkv, d, "V_out");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws) || ws_bytes < svl_mrope_remap_workspace_size(B, k))
+        return fail(SVL_ERR_WORKSPACE, "workspace NULL, misaligned or too small%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    MropeParams p;
+    p.K = static_cast<const uint16_t*>(K.data);
+    p.ksb = K.stride_b; p.ksh = K.stride_h; p.kst = K.stride_t;
+    p.V = static_cast<const uint16_t*>(V.data);
+    p.vsb = V.stride_b; p.vsh = V.stride_h; p.vst = V.stride_t;
+    p.Ko = static_cast<uint16_t*>(const_cast<void*>(Ko.data));
+    p.osb = Ko.stride_b; p.osh = Ko.stride_h; p.ost = Ko.stride_t;
+    p.Vo = static_cast<uint16_t*>(const_cast<void*>(Vo.data));
+    p.vosb = Vo.stride_b; p.vosh = Vo.stride_h; p.vost = Vo.stride_t;
+    p.seq_len = span.seq_len;
+    p.kept = kept;
+    p.coords = coords;
+    p.B = B; p.Hkv = Hkv; p.d = d; p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k;
+    p.capacity = K.capacity;
+    p.sec0 = sections[0]; p.sec1 = sections[1];
+    p.log2_base = log2(rope_base);
+    p.dim_max = reinterpret_cast<int32_t*>(w + kWsHeader);
+    p.new_coords = new_coords_out ? new_coords_out
+                                  : reinterpret_cast<int32_t*>(w + round_up(kWsHeader + (size_t)B * 3 * sizeof(int32_t), 256));
+    p.text_start_out = text_start_out;
+    p.flags = static_cast<uint32_t*>(ws);
+    cudaError_t e = launch_mrope_remap(p, (int)need, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_mrope_remap");
+    return SVL_OK;
+}
+
 svl_status svl_pack_kv(svl_kv K, svl_kv V, int32_t B, int32_t Hkv, int32_t d, svl_span span,
                        const int32_t* vis_idx, int32_t k, uint32_t flags, svl_kv Kp, svl_kv Vp, void* ws,
                        size_t ws_bytes, void* stream) {

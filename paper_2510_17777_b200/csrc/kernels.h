@@ -200,6 +200,27 @@ struct RopeParams {
     uint32_t* flags;
 };
 cudaError_t launch_rope_remap(const RopeParams& p, int max_rows, cudaStream_t s);
+struct MropeParams {
+    const uint16_t* K;  // pre-RoPE keys
+    int64_t ksb, ksh, kst;
+    const uint16_t* V;  // nullable
+    int64_t vsb, vsh, vst;
+    uint16_t* Ko;
+    int64_t osb, osh, ost;
+    uint16_t* Vo;
+    int64_t vosb, vosh, vost;
+    const int32_t* seq_len;
+    const int32_t* kept;    // [B][k]
+    const int32_t* coords;  // [B][nv][3] (t, h, w) of the original visual rows
+    int B, Hkv, d, vb, nv, k, capacity;
+    int sec0, sec1;         // rotary pairs of the t and h sections (w: the rest of d/2)
+    double log2_base;
+    int32_t* new_coords;    // [B][k][3]
+    int32_t* dim_max;       // [B][3] workspace
+    int32_t* text_start_out;  // nullable [B]
+    uint32_t* flags;
+};
+cudaError_t launch_mrope_remap(const MropeParams& p, int max_rows, cudaStream_t s);
 constexpr int kScoreThreads = 512;
 constexpr int kSelectThreads = 512;
 constexpr int kSelectMaxPerThread = 16;  // => <= 8192 keys per CTA

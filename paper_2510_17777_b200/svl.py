@@ -43,7 +43,8 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_status_string", "svl_last_error_message", "svl_read_device_flags",
            "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
            "svl_wait_flags", "svl_pack_kv", "svl_rope_remap", "svl_fresh_decode_plan",
-           "svl_page_summary", "svl_retrieve_pages", "svl_retrieve_pages_workspace_size"]
+           "svl_page_summary", "svl_retrieve_pages", "svl_retrieve_pages_workspace_size",
+           "svl_mrope_remap", "svl_mrope_remap_workspace_size"]
 
 
 class SvlError(RuntimeError):
@@ -97,6 +98,11 @@ def lib():
         L.svl_fresh_decode_step.restype = ctypes.c_int
         L.svl_fresh_decode_step.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, I32,
                                             F, U32, P, P, P, P, SZ, P]
+        L.svl_mrope_remap.restype = ctypes.c_int
+        L.svl_mrope_remap.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, P, I32, ctypes.c_double, P,
+                                      svl_kv, svl_kv, P, P, P, SZ, P]
+        L.svl_mrope_remap_workspace_size.restype = SZ
+        L.svl_mrope_remap_workspace_size.argtypes = [I32, I32]
         L.svl_page_summary.restype = ctypes.c_int
         L.svl_page_summary.argtypes = [svl_kv, I32, I32, I32, svl_span, I32, P, P, P, SZ, P]
         L.svl_retrieve_pages.restype = ctypes.c_int
@@ -496,3 +502,30 @@ def retrieve_pages(q: torch.Tensor, kmax: torch.Tensor, kmin: torch.Tensor, page
         _cuda(scores_out, "scores_out", torch.float32) if scores_out is not None else None,
         w.data_ptr(), w.numel(), _stream(stream)))
     return page_idx_out, row_idx_out
+
+
+def mrope_remap(K_pre: torch.Tensor, V: Optional[torch.Tensor], seq_len: torch.Tensor, visual_begin: int,
+                visual_len: int, coords: torch.Tensor, kept: torch.Tensor, rope_base: float, sections,
+                K_out: Optional[torch.Tensor] = None, V_out: Optional[torch.Tensor] = None,
+                ws: Optional[Workspace] = None, stream=None):
+    """svl_mrope_remap.  coords int32 [B][visual_len][3]; kept int32 [B][k]; sections 3 ints.
+    Returns (K_out, V_out, new_coords int32 [B][k][3], text_start int32 [B])."""
+    B, Hkv, cap, d = K_pre.shape
+    k = kept.shape[-1]
+    cap_out = cap - visual_len + k
+    if K_out is None:
+        K_out = torch.empty(B, Hkv, cap_out, d, dtype=torch.bfloat16, device=K_pre.device)
+    if V is not None and V_out is None:
+        V_out = torch.empty(B, Hkv, cap_out, d, dtype=torch.bfloat16, device=K_pre.device)
+    nc = torch.empty(B, k, 3, dtype=torch.int32, device=K_pre.device)
+    ts = torch.empty(B, dtype=torch.int32, device=K_pre.device)
+    sec = (ctypes.c_int32 * 3)(*[int(x) for x in sections])
+    w = _ws(ws, K_pre.device).get(lib().svl_mrope_remap_workspace_size(B, k))
+    empty = svl_kv(None, 0, 0, 0, 0)
+    _check(lib().svl_mrope_remap(
+        kv_view(K_pre, "K_pre"), kv_view(V, "V") if V is not None else empty, B, Hkv, d,
+        span(visual_begin, visual_len, seq_len), _cuda(coords.contiguous(), "coords", torch.int32),
+        _cuda(kept.contiguous(), "kept", torch.int32), k, float(rope_base), ctypes.cast(sec, ctypes.c_void_p),
+        kv_view(K_out, "K_out"), kv_view(V_out, "V_out") if V_out is not None else empty,
+        nc.data_ptr(), ts.data_ptr(), w.data_ptr(), w.numel(), _stream(stream)))
+    return K_out, V_out, nc, ts
