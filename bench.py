@@ -667,6 +667,127 @@ def run_sharded(args, cfg_name):
     return 0
 
 
+def run_seq_split(args):
+    """ONE long-video request (B = 1) over P GPUs: P_h =
+    gcd(P, Hkv) KV-head groups x P_s = P / P_h sequence shards (8 GPUs: 4 x 2).  Per layer
+    every rank runs the sequence-split fresh step on its shard view (seqpar.py: partial LSE,
+    LSE exchange, scores exchange + global top-k, padded decode, partial exchange + merge;
+    NCCL all-gathers inside the sequence group) and the head outputs are all-gathered over
+    the world, all in one CUDA graph.  Strong scaling vs the fused step on one GPU."""
+    import math as _m
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_17777_b200 import inputs as gen
+    from paper_2510_17777_b200 import seqpar, svl
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = gen.CONFIGS[WORKLOAD]
+    P_h = _m.gcd(world, wl.Hkv)
+    P_s = world // P_h
+    hg, s = rank % P_h, rank // P_h
+    seq_groups = [list(range(h, world, P_h)) for h in range(P_h)]
+    groups = [dist.new_group(r) for r in seq_groups] if world > 1 else [None] * P_h
+    my_group = groups[hg]
+    kv0, kv1 = hg * wl.Hkv // P_h, (hg + 1) * wl.Hkv // P_h
+    h0, h1 = kv0 * wl.g, kv1 * wl.g
+    xs = [gen.make_decode_inputs(wl, seed=8000 + l, device=dev) for l in range(SHARD_ROT)]
+    states = [seqpar.ShardState(x["q_dec"][:, h0:h1].contiguous(), x["K"][:, kv0:kv1], x["V"][:, kv0:kv1],
+                                x["seq_len"], wl.vb, wl.nv, wl.k, P_s, s) for x in xs]
+    full = [torch.empty(world, wl.B, h1 - h0, wl.d, device=dev) for _ in range(SHARD_ROT)]
+
+    def gather_seq(t):
+        if P_s == 1:
+            return t.unsqueeze(0)
+        buf = t.new_empty((P_s,) + tuple(t.shape))
+        dist.all_gather_into_tensor(buf, t.contiguous(), group=my_group)
+        return buf
+
+    def step():
+        for l in range(LAYERS):
+            r = l % SHARD_ROT
+            out, _ = seqpar.distributed_step(states[r], my_group, gather=gather_seq)
+            if world > 1:
+                dist.all_gather_into_tensor(full[r], out)
+            else:
+                full[r][0].copy_(out)
+
+    def graph_of(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                fn()
+        torch.cuda.synchronize()
+        return g
+
+    steps = max(5, min(args.steps, 200))
+    warm = max(3, min(args.warmup, 20))
+    t1 = None
+    if rank == 0:
+        wsf = svl.Workspace(dev)
+        of = [torch.empty(wl.B, wl.H, wl.d, device=dev) for _ in range(SHARD_ROT)]
+        g1 = graph_of(lambda: [svl.fresh_decode_step(xs[l % SHARD_ROT]["q_dec"], xs[l % SHARD_ROT]["K"],
+                                                     xs[l % SHARD_ROT]["V"], xs[l % SHARD_ROT]["seq_len"], wl.vb,
+                                                     wl.nv, wl.k, out=of[l % SHARD_ROT], ws=wsf)
+                               for l in range(LAYERS)])
+        for _ in range(warm):
+            g1.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            g1.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        t1 = e0.elapsed_time(e1) / steps
+        del g1
+    if world > 1:
+        dist.barrier()
+    g = graph_of(step)
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    total = step_bytes(wl)["total"] * LAYERS
+    if rank == 0:
+        print(json.dumps({
+            "metric": "decode step HBM GB/s (retrieve+sparse attn) @32k visual tok, one request sequence-split",
+            "value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded generator)",
+            "config": {"workload": f"long-video B=1, {LAYERS} layers ({SHARD_ROT} rotating caches): {P_h} KV-head "
+                                   f"groups x {P_s} sequence shards, 3 exchanges per layer in the sequence group + "
+                                   "the head-output all-gather", "P_h": P_h, "P_s": P_s},
+            "us_per_layer": ms * 1e3 / LAYERS,
+            "one_gpu_fused": {"ms_per_step": t1} if t1 else None,
+            "E_strong": (t1 / (world * ms)) if t1 else None,
+            "gpu_launches": LAYERS * steps * 8, "clocks": clk.summary()}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def free_port():
     import socket
     sck = socket.socket()
@@ -692,11 +813,13 @@ def main():
     ap.add_argument("--impl", default="svl", choices=["svl", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON checks)")
-    ap.add_argument("--mode", default="auto", choices=["auto", "headline", "replicas", "sweep-heads", "heads"],
+    ap.add_argument("--mode", default="auto",
+                    choices=["auto", "headline", "replicas", "sweep-heads", "heads", "seq-split"],
                     help="auto: headline at N = 1, sweep-heads at N > 1; replicas: every rank serves its "
                          "own long-video request (weak); sweep-heads: the B 16 / 64k sweep sharded over "
                          "(batch x KV head) with a per-layer NCCL all-gather of the head outputs (strong); "
-                         "heads: the same for the multi-turn batch")
+                         "heads: the same for the multi-turn batch; seq-split: one long-video request over "
+                         "KV-head groups x sequence shards (SURVEY 8(f) f3)")
     ap.add_argument("--fused-gather", action="store_true",
                     help="sweep-heads: replace the NCCL all-gather by svl_sparse_decode_attn_push into "
                          "symmetric-memory peer buffers (eager launches: the epoch is a call argument)")
@@ -717,6 +840,8 @@ def main():
         return run_sharded(args, "sweep")
     if mode == "heads":
         return run_sharded(args, "multi-turn")
+    if mode == "seq-split":
+        return run_seq_split(args)
     return run_headline(args)
 
 

@@ -72,6 +72,14 @@ typedef enum {
 /* svl_fresh_decode_step: always run the two separate calls (svl_retrieve then
  * svl_sparse_decode_attn) instead of the fused kernel (A/B measurements, tests). */
 #define SVL_FRESH_UNFUSED 0x400u
+/* svl_sparse_decode_attn: vis_idx entries equal to -1 after the valid
+ * (ascending) entries of a unit are padding, skipped without a device flag
+ * (a shard's share of a sequence-split selection, svl_shard_indices). */
+#define SVL_IDX_PADDED 0x800u
+/* svl_retrieve / svl_retrieve_partial_lse: the K view is one shard of a
+ * sequence-split cache: seq_len >= vb + visual_len suffices
+ * (the query rows live in another shard's view). */
+#define SVL_SHARD_VIEW 0x1000u
 /* Split-count pin, flags bits 24..31 (0 = the planner's choice).
  * svl_sparse_decode_attn(_push): exactly n CTAs per (b, KV group) unit
  * (B*Hkv*n must not exceed the co-resident CTA count when n > 1, else
@@ -345,6 +353,45 @@ int32_t svl_fresh_decode_plan(int32_t B, int32_t H, int32_t Hkv, int32_t d, int3
 
 size_t svl_fresh_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                        int32_t visual_len, int32_t capacity, uint32_t flags);
+
+/* -------------------- sequence split of one request */
+/*
+ * A (b, KV group) unit's visual span is split over P_s ranks (B = 1 on 8 GPUs:
+ * 4 KV heads x 2 halves); each rank passes a K/V view of its shard (system text
+ * on the first shard, later text on the last; SVL_SHARD_VIEW).  The fresh step
+ * then needs three exchanges between the shards (the harness's collectives):
+ *   1. svl_retrieve_partial_lse on the view -> local LSE [B][n_q][H];
+ *      exchange; svl_lse_combine -> the full-prefix LSE;
+ *   2. svl_retrieve(..., SVL_RETRIEVE_SELECT_ONLY | SVL_SHARD_VIEW, lse_in =
+ *      that LSE, scores_out) -> the shard's relevance scores; exchange (the
+ *      shards' scores side by side = the unit's scores); svl_topk -> the unit's
+ *      kept rows (identical on every shard); svl_shard_indices -> this shard's;
+ *   3. svl_sparse_decode_attn(view, SVL_IDX_PADDED) -> (out, lse) partial;
+ *      exchange; svl_merge_partials -> out, lse.
+ * paper_2510_17777_b200/seqpar.py drives the sequence (tests, bench).
+ */
+/* Natural-log LSE of scale * q . K_j over the view's normalisation domain (visual
+ * rows, plus the view's text rows unless SVL_NORM_VISUAL_ONLY); leaves the
+ * logits in the workspace for a following SVL_RETRIEVE_SELECT_ONLY call with
+ * identical arguments.  n_q * g <= 32.  Workspace: svl_retrieve_workspace_size. */
+svl_status svl_retrieve_partial_lse(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                    svl_kv K, svl_span span, float scale, uint32_t flags, float* lse_out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+/* out[i] = M + log sum_p exp(parts[p][i] - M), p in rank order; device fp32. */
+svl_status svl_lse_combine(const float* parts, int32_t P, int32_t n, float* out, void* stream);
+/* Top-k of scores [units][n] per unit (ties -> lower index), ascending indices
+ * [units][k]; the selection kernels of svl_retrieve.  Workspace: header. */
+svl_status svl_topk(const float* scores, int32_t units, int32_t n, int32_t k, int32_t* idx_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+size_t svl_topk_workspace_size(int32_t units, int32_t n);
+/* The entries of each unit's ascending idx [units][k] inside [lo, hi), minus
+ * lo, then -1 padding: out [units][k] (SVL_IDX_PADDED vis_idx of the shard). */
+svl_status svl_shard_indices(const int32_t* idx, int32_t units, int32_t k, int32_t lo, int32_t hi, int32_t* out,
+                             void* stream);
+/* out [rows][d], lse [rows] (nullable) from P partials out_parts [P][rows][d],
+ * lse_parts [P][rows] (natural log), rank order: the a5 log-sum-exp merge. */
+svl_status svl_merge_partials(const float* out_parts, const float* lse_parts, int32_t P, int32_t rows, int32_t d,
+                              float* out, float* lse_out, void* stream);
 
 /* ------------------------------------ page-summary retrieval (Quest-style) */
 /*

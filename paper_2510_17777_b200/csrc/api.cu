@@ -334,15 +334,16 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     if (!q || (!idx_out && k > 0) || !span.seq_len)
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
     if (flags & ~(SVL_NORM_VISUAL_ONLY | SVL_SELECT_SHARED | SVL_RETRIEVE_SCORE_ONLY |
-                  SVL_RETRIEVE_SELECT_ONLY))
+                  SVL_RETRIEVE_SELECT_ONLY | SVL_SHARD_VIEW))
         return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
     if ((flags & SVL_RETRIEVE_SCORE_ONLY) && (flags & SVL_RETRIEVE_SELECT_ONLY))
         return fail(SVL_ERR_INVALID_ARGUMENT, "SCORE_ONLY and SELECT_ONLY are exclusive%s");
     if (B < 1 || n_q < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, n_q, H, Hkv must be >= 1%s");
     if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
     if (span.visual_len < 1) return fail(SVL_ERR_SHAPE, "no visual rows to retrieve from%s");
+    const int q_rows = (flags & SVL_SHARD_VIEW) ? 0 : n_q;  // a shard view need not hold the query rows
     if (span.visual_begin < 0 ||
-        (int64_t)span.visual_begin + span.visual_len + n_q > (int64_t)K.capacity)
+        (int64_t)span.visual_begin + span.visual_len + q_rows > (int64_t)K.capacity)
         return fail(SVL_ERR_SHAPE, "visual span + query rows outside the KV capacity%s");
     if (k < 0 || k > span.visual_len) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, visual_len]%s");
     if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
@@ -362,6 +363,7 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     if (st != SVL_OK) return st;
 
     const int units = B * Hkv;
+    if (tc && (flags & SVL_SHARD_VIEW)) return fail(SVL_ERR_UNSUPPORTED, "SVL_SHARD_VIEW needs n_q * g <= 32%s");
     if (tc) return retrieve_tc(q, B, n_q, H, Hkv, d, K, span, lse_in, k, scale, flags, idx_out, scores_out,
                                ws, ws_bytes, (cudaStream_t)stream);
     ScorePlan pl = plan_score(units, n_q, g, span.visual_len, device_sm_count());
@@ -381,6 +383,7 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     sp.C = pl.C; sp.rows_per_chunk = pl.rows_per_chunk;
     sp.need_partials = lse_in ? 0 : 1;
     sp.use_text = (!lse_in && !(flags & SVL_NORM_VISUAL_ONLY)) ? 1 : 0;
+    sp.q_rows_in_view = (flags & SVL_SHARD_VIEW) ? 0 : n_q;
     sp.scale2 = scale * kLog2e;
     sp.logits = reinterpret_cast<float*>(w + lay.logits);
     sp.part = reinterpret_cast<float2*>(w + lay.part);
@@ -409,6 +412,120 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     return SVL_OK;
 }
 
+// ------------------------------------------- sequence split
+svl_status svl_retrieve_partial_lse(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                    svl_kv K, svl_span span, float scale, uint32_t flags, float* lse_out, void* ws,
+                                    size_t ws_bytes, void* stream) {
+    if (!q || !lse_out || !span.seq_len) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags & ~(SVL_NORM_VISUAL_ONLY | SVL_SHARD_VIEW)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (B < 1 || n_q < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, n_q, H, Hkv must be >= 1%s");
+    if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
+    if (span.visual_len < 1) return fail(SVL_ERR_SHAPE, "no visual rows%s");
+    const int q_rows = (flags & SVL_SHARD_VIEW) ? 0 : n_q;
+    if (span.visual_begin < 0 || (int64_t)span.visual_begin + span.visual_len + q_rows > (int64_t)K.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span + query rows outside the KV capacity%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    const int g = H / Hkv;
+    if (n_q * g > 32) return fail(SVL_ERR_UNSUPPORTED, "partial LSE needs n_q * g <= 32%s");
+    if (!aligned16(q)) return fail(SVL_ERR_ALIGNMENT, "q not 16-byte aligned%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+    const int units = B * Hkv;
+    ScorePlan pl = plan_score(units, n_q, g, span.visual_len, device_sm_count());
+    RetrieveLayout lay = retrieve_layout(B, Hkv, span.visual_len, pl);
+    if (ws_bytes < lay.total) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    ScoreParams sp;
+    sp.q = static_cast<const uint16_t*>(q);
+    sp.K = static_cast<const uint16_t*>(K.data);
+    sp.sb = K.stride_b; sp.sh = K.stride_h; sp.st = K.stride_t;
+    sp.seq_len = span.seq_len;
+    sp.B = B; sp.n_q = n_q; sp.H = H; sp.Hkv = Hkv; sp.g = g;
+    sp.NC = n_q * g; sp.NCP = pl.NCP;
+    sp.vb = span.visual_begin; sp.nv = span.visual_len; sp.capacity = K.capacity;
+    sp.C = pl.C; sp.rows_per_chunk = pl.rows_per_chunk;
+    sp.need_partials = 1;
+    sp.use_text = (flags & SVL_NORM_VISUAL_ONLY) ? 0 : 1;
+    sp.q_rows_in_view = q_rows;
+    sp.scale2 = scale * kLog2e;
+    sp.logits = reinterpret_cast<float*>(w + lay.logits);
+    sp.part = reinterpret_cast<float2*>(w + lay.part);
+    sp.flags = reinterpret_cast<uint32_t*>(w);
+    cudaError_t e = launch_score(sp, d, pl.NT, (cudaStream_t)stream);
+    if (e == cudaSuccess)
+        e = launch_lse_from_partials(sp.part, units, pl.C, pl.NCP, sp.NC, g, n_q, H, Hkv, lse_out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve_partial_lse");
+    return SVL_OK;
+}
+
+svl_status svl_lse_combine(const float* parts, int32_t P, int32_t n, float* out, void* stream) {
+    if (!parts || !out) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (P < 1 || n < 0) return fail(SVL_ERR_SHAPE, "P >= 1, n >= 0%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    if (n == 0) return SVL_OK;
+    cudaError_t e = launch_lse_combine(parts, P, n, out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_lse_combine");
+    return SVL_OK;
+}
+
+size_t svl_topk_workspace_size(int32_t units, int32_t n) {
+    (void)units;
+    (void)n;
+    return kWsHeader;
+}
+
+svl_status svl_topk(const float* scores, int32_t units, int32_t n, int32_t k, int32_t* idx_out, void* ws,
+                    size_t ws_bytes, void* stream) {
+    if (!scores || (!idx_out && k > 0)) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (units < 1 || n < 1) return fail(SVL_ERR_SHAPE, "units, n must be >= 1%s");
+    if (k < 0 || k > n) return fail(SVL_ERR_INVALID_ARGUMENT, "k outside [0, n]%s");
+    if (n > 16 * kSelectThreads * kSelectMaxPerThread) return fail(SVL_ERR_UNSUPPORTED, "n > 131072%s");
+    if (!ws || !aligned16(ws) || ws_bytes < kWsHeader) return fail(SVL_ERR_WORKSPACE, "workspace NULL, misaligned or too small%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    if (k == 0) return SVL_OK;
+    SelectParams se = {};
+    se.mode = 2;
+    se.scores_in = scores;
+    se.Hkv = 1;
+    se.shared = 0;
+    se.nv = n; se.k = k;
+    se.idx_out = idx_out;
+    se.flags = static_cast<uint32_t*>(ws);
+    se.CS = select_cluster_size(n);
+    cudaError_t e = launch_select(se, units, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_topk");
+    return SVL_OK;
+}
+
+svl_status svl_shard_indices(const int32_t* idx, int32_t units, int32_t k, int32_t lo, int32_t hi, int32_t* out,
+                             void* stream) {
+    if ((!idx || !out) && k > 0) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (units < 1 || k < 0 || lo < 0 || hi < lo) return fail(SVL_ERR_SHAPE, "units >= 1, k >= 0, 0 <= lo <= hi%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    if (k == 0) return SVL_OK;
+    cudaError_t e = launch_shard_indices(idx, units, k, lo, hi, out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_shard_indices");
+    return SVL_OK;
+}
+
+svl_status svl_merge_partials(const float* out_parts, const float* lse_parts, int32_t P, int32_t rows, int32_t d,
+                              float* out, float* lse_out, void* stream) {
+    if (!out_parts || !lse_parts || !out) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (P < 1 || rows < 1 || d < 1) return fail(SVL_ERR_SHAPE, "P, rows, d must be >= 1%s");
+    svl_status st = check_device();
+    if (st != SVL_OK) return st;
+    cudaError_t e = launch_merge_partials(out_parts, lse_parts, P, rows, d, out, lse_out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_merge_partials");
+    return SVL_OK;
+}
+
 // ------------------------------------------------------------ sparse decode
 size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32_t d, int32_t k,
                                         int32_t visual_len, int32_t capacity, uint32_t flags) {
@@ -433,7 +550,8 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
                                      const PushArgs& push, const char* name) {
     if (!q || (!out && push.P == 0) || !span.seq_len || (k > 0 && !vis_idx))
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
-    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK)) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK | SVL_IDX_PADDED))
+        return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
     if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
     if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
     if (span.visual_begin < 0 || span.visual_len < 0 ||
@@ -473,6 +591,7 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     p.B = B; p.H = H; p.Hkv = Hkv; p.g = g;
     p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k;
     p.shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
+    p.padded = (flags & SVL_IDX_PADDED) ? 1 : 0;
     p.capacity = K.capacity;
     p.S = S;
     // rows of one split <= ceil(vb / S) + ceil(k / S) + ceil(T_max / S) (three segments)

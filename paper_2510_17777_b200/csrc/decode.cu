@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         if (i < ns) return s0 + i;
         if (i < ns + nm) {
             if (r.x >= 0 && r.x < p.nv && r.xp < r.x) return p.vb + r.x;
+            if (p.padded && r.x == -1) return -1;  // trailing padding (SVL_IDX_PADDED)
             raise_flag(p.flags, 1u /*SVL_DEVFLAG_INDEX*/);
             return -1;
         }

@@ -19,6 +19,7 @@ struct ScoreParams {
     int C;               // chunks per unit
     int rows_per_chunk;  // visual rows per chunk (multiple of 16)
     int use_text;        // normalise over text rows too (FULL_PREFIX and no lse_in)
+    int q_rows_in_view;  // n_q, or 0 for a shard view (SVL_SHARD_VIEW): seq_len >= vb + nv only
     int need_partials;   // 0 when lse_in supplies the normaliser
     float scale2;        // scale * log2(e)
     float* logits;       // [units][nv][NCP] base-2 logits
@@ -65,6 +66,7 @@ struct DecodeParams {
     int B, H, Hkv, g, vb, nv, k, shared, capacity;
     int S;             // splits (CTAs) per unit; the grid (S x units) is co-resident
     int single_batch;  // every split has <= kDecodeRowsMax rows (host bound): one gather buffer
+    int padded;        // SVL_IDX_PADDED: trailing -1 entries of vis_idx are skipped silently
     float scale2;  // scale * log2(e)
     float* out;    // [B][H][d]
     float* lse_out;
@@ -181,6 +183,13 @@ struct PageRetrParams {
     float* scores;  // [units][np]
 };
 cudaError_t launch_page_summary(const PageSumParams& p, cudaStream_t s);
+// --------------------------------- sequence-split exchanges
+cudaError_t launch_lse_from_partials(const float2* part, int units, int C, int NCP, int NC, int g, int n_q, int H,
+                                     int Hkv, float* lse_out, cudaStream_t s);
+cudaError_t launch_lse_combine(const float* parts, int P, int n, float* out, cudaStream_t s);
+cudaError_t launch_shard_indices(const int32_t* idx, int units, int k, int lo, int hi, int32_t* out, cudaStream_t s);
+cudaError_t launch_merge_partials(const float* out_parts, const float* lse_parts, int P, int rows, int d, float* out,
+                                  float* lse_out, cudaStream_t s);
 cudaError_t launch_page_scores(const PageRetrParams& p, cudaStream_t s);
 cudaError_t launch_page_expand(const int32_t* pidx, int units, int kp, int page, int32_t* rows, cudaStream_t s);
 // -------------------------------------------- RoPE remap

@@ -50,9 +50,9 @@ __global__ void __launch_bounds__(kScoreThreads, 1) score_kernel(const ScorePara
     const int b = u / p.Hkv, G = u % p.Hkv;
 
     int L = p.seq_len[b];
-    if (L < p.vb + p.nv + p.n_q || L > p.capacity) {
+    if (L < p.vb + p.nv + p.q_rows_in_view || L > p.capacity) {
         if (threadIdx.x == 0 && c == 0) raise_flag(p.flags, 4u /*SVL_DEVFLAG_SPAN*/);
-        L = min(max(L, p.vb + p.nv + p.n_q), p.capacity);
+        L = min(max(L, p.vb + p.nv + p.q_rows_in_view), p.capacity);
     }
 
     // ---- work list: visual rows of this chunk, then this chunk's share of text rows

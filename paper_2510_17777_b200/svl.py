@@ -24,6 +24,8 @@ SVL_RETRIEVE_SCORE_ONLY = 0x100
 SVL_RETRIEVE_SELECT_ONLY = 0x200
 SVL_FRESH_UNFUSED = 0x400
 WORKSPACE_HEADER_BYTES = 1024  # SVL_WORKSPACE_HEADER_BYTES
+SVL_IDX_PADDED = 0x800
+SVL_SHARD_VIEW = 0x1000
 SVL_PIN_SPLITS_MASK = 0xff000000
 
 
@@ -44,7 +46,8 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_reset_device_flags", "svl_version", "svl_sparse_decode_attn_push",
            "svl_wait_flags", "svl_pack_kv", "svl_rope_remap", "svl_fresh_decode_plan",
            "svl_page_summary", "svl_retrieve_pages", "svl_retrieve_pages_workspace_size",
-           "svl_mrope_remap", "svl_mrope_remap_workspace_size"]
+           "svl_mrope_remap", "svl_mrope_remap_workspace_size", "svl_retrieve_partial_lse",
+           "svl_lse_combine", "svl_topk", "svl_topk_workspace_size", "svl_shard_indices", "svl_merge_partials"]
 
 
 class SvlError(RuntimeError):
@@ -98,6 +101,19 @@ def lib():
         L.svl_fresh_decode_step.restype = ctypes.c_int
         L.svl_fresh_decode_step.argtypes = [P, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, I32,
                                             F, U32, P, P, P, P, SZ, P]
+        L.svl_retrieve_partial_lse.restype = ctypes.c_int
+        L.svl_retrieve_partial_lse.argtypes = [P, I32, I32, I32, I32, I32, svl_kv, svl_span, ctypes.c_float, U32, P,
+                                               P, SZ, P]
+        L.svl_lse_combine.restype = ctypes.c_int
+        L.svl_lse_combine.argtypes = [P, I32, I32, P, P]
+        L.svl_topk.restype = ctypes.c_int
+        L.svl_topk.argtypes = [P, I32, I32, I32, P, P, SZ, P]
+        L.svl_topk_workspace_size.restype = SZ
+        L.svl_topk_workspace_size.argtypes = [I32, I32]
+        L.svl_shard_indices.restype = ctypes.c_int
+        L.svl_shard_indices.argtypes = [P, I32, I32, I32, I32, P, P]
+        L.svl_merge_partials.restype = ctypes.c_int
+        L.svl_merge_partials.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.svl_mrope_remap.restype = ctypes.c_int
         L.svl_mrope_remap.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, P, I32, ctypes.c_double, P,
                                       svl_kv, svl_kv, P, P, P, SZ, P]
@@ -529,3 +545,78 @@ def mrope_remap(K_pre: torch.Tensor, V: Optional[torch.Tensor], seq_len: torch.T
         kv_view(K_out, "K_out"), kv_view(V_out, "V_out") if V_out is not None else empty,
         nc.data_ptr(), ts.data_ptr(), w.data_ptr(), w.numel(), _stream(stream)))
     return K_out, V_out, nc, ts
+
+
+# ------------------------------------------- sequence split
+
+def retrieve_partial_lse(q: torch.Tensor, K: torch.Tensor, seq_len: torch.Tensor, visual_begin: int,
+                         visual_len: int, flags: int = 0, scale: Optional[float] = None,
+                         lse_out: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None, stream=None):
+    """svl_retrieve_partial_lse.  q bf16 [B][n_q][H][d] -> natural-log LSE fp32 [B][n_q][H]."""
+    B, n_q, H, d = q.shape
+    Hkv = K.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if lse_out is None:
+        lse_out = torch.empty(B, n_q, H, dtype=torch.float32, device=q.device)
+    w = _ws(ws, q.device).get(retrieve_workspace_size(B, n_q, H, Hkv, d, visual_len, flags & SVL_NORM_VISUAL_ONLY))
+    _check(lib().svl_retrieve_partial_lse(q.data_ptr(), B, n_q, H, Hkv, d, kv_view(K, "K"),
+                                          span(visual_begin, visual_len, seq_len), scale, flags,
+                                          _cuda(lse_out, "lse_out", torch.float32), w.data_ptr(), w.numel(),
+                                          _stream(stream)))
+    return lse_out
+
+
+def lse_combine(parts: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """svl_lse_combine.  parts fp32 [P][...] -> [...] (log-sum-exp over P in rank order)."""
+    parts = parts.contiguous()
+    P = parts.shape[0]
+    if out is None:
+        out = torch.empty(parts.shape[1:], dtype=torch.float32, device=parts.device)
+    _check(lib().svl_lse_combine(_cuda(parts, "parts", torch.float32), P, parts[0].numel(),
+                                 _cuda(out, "out", torch.float32), _stream(stream)))
+    return out
+
+
+def topk(scores: torch.Tensor, k: int, idx_out: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None,
+         stream=None) -> torch.Tensor:
+    """svl_topk.  scores fp32 [units][n] -> ascending indices int32 [units][k] (ties -> lower index)."""
+    scores = scores.contiguous()
+    units, n = scores.shape
+    if idx_out is None:
+        idx_out = torch.empty(units, k, dtype=torch.int32, device=scores.device)
+    w = _ws(ws, scores.device).get(lib().svl_topk_workspace_size(units, n))
+    _check(lib().svl_topk(_cuda(scores, "scores", torch.float32), units, n, k, _cuda(idx_out, "idx_out", torch.int32),
+                          w.data_ptr(), w.numel(), _stream(stream)))
+    return idx_out
+
+
+def shard_indices(idx: torch.Tensor, lo: int, hi: int, out: Optional[torch.Tensor] = None, stream=None):
+    """svl_shard_indices.  idx int32 [..., k] ascending -> this shard's entries minus lo, -1 padded."""
+    idx = idx.contiguous()
+    k = idx.shape[-1]
+    units = idx.numel() // max(k, 1)
+    if out is None:
+        out = torch.empty_like(idx)
+    _check(lib().svl_shard_indices(_cuda(idx, "idx", torch.int32), units, k, lo, hi, _cuda(out, "out", torch.int32),
+                                   _stream(stream)))
+    return out
+
+
+def merge_partials(out_parts: torch.Tensor, lse_parts: torch.Tensor, out: Optional[torch.Tensor] = None,
+                   lse_out: Optional[torch.Tensor] = None, stream=None):
+    """svl_merge_partials.  out_parts fp32 [P][...][d], lse_parts fp32 [P][...] -> (out, lse)."""
+    out_parts = out_parts.contiguous()
+    lse_parts = lse_parts.contiguous()
+    P, d = out_parts.shape[0], out_parts.shape[-1]
+    rows = lse_parts[0].numel()
+    if out is None:
+        out = torch.empty(out_parts.shape[1:], dtype=torch.float32, device=out_parts.device)
+    if lse_out is None:
+        lse_out = torch.empty(lse_parts.shape[1:], dtype=torch.float32, device=out_parts.device)
+    _check(lib().svl_merge_partials(_cuda(out_parts, "out_parts", torch.float32),
+                                    _cuda(lse_parts, "lse_parts", torch.float32), P, rows, d,
+                                    _cuda(out, "out", torch.float32), _cuda(lse_out, "lse_out", torch.float32),
+                                    _stream(stream)))
+    return out, lse_out
