@@ -155,6 +155,13 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                          \
         trs[(ph)] = tnow;                                                                 \
     }
+    auto tstamp = [&](int slot) {  // stamp from the calling thread (debug builds)
+        if (p.trace) {
+            uint64_t tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            trs[slot] = tnow;
+        }
+    };
     if (p.trace && tid < 64) trs[tid] = 0;
     SVL_TRACE(0);
     if (p.trace && tid == 0) trs[30] = clock64();
@@ -288,7 +295,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             // before the PDL wait only L2 prefetches of the first stages (a hint: the data
             // is read into shared memory after the wait, so an upstream kernel that writes
             // visual K rows -- svl_rope_remap, svl_pack_kv -- is always seen)
-            for (int i = 0; i < min(NST, nstages); ++i)
+#ifndef SVL_L2PF_STAGES
+#define SVL_L2PF_STAGES 0  // measured (28-layer graph, long-video): 0 stages 29.17, NST 29.50, all 16 30.50 us/layer
+#endif
+            for (int i = 0; i < min(SVL_L2PF_STAGES, nstages); ++i)
 #pragma unroll
                 for (int hf = 0; hf < D / 64; ++hf)
                     tma_prefetch_4d(&p.ktmap, hf * 64, p.vb + v0 + i * STAGE_ROWS, G, b);
@@ -407,27 +417,42 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             if (i * STAGE_ROWS + q4 * 32 + lane < nvis) {
 #pragma unroll
                 for (int c = 0; c < NCP; ++c) {
+#ifndef SVL_LSE_ONE_EXP
+#define SVL_LSE_ONE_EXP 1  // measured: 29.29 -> 28.81 us/layer (long-video 28-layer graph)
+#endif
+#if SVL_LSE_ONE_EXP
+                    // one exponential per element: e = exp2(-|y - m|) rescales whichever side
+                    // is smaller (y finite; m starts at -inf: d = +inf, e = 0 -> l = 1)
+                    const float y = x[c] * p.scale2;
+                    const float dd = y - rm[c];
+                    const float e = fast_exp2(-fabsf(dd));
+                    rl[c] = (dd > 0.f) ? fmaf(rl[c], e, 1.f) : rl[c] + e;
+                    rm[c] = fmaxf(rm[c], y);
+#else
                     const float y = x[c] * p.scale2;
                     const float M = fmaxf(rm[c], y);
                     rl[c] = rl[c] * fast_exp2(rm[c] - M) + fast_exp2(y - M);
                     rm[c] = M;
+#endif
                 }
             }
         }
+        if (warp == 4 && lane == 0) tstamp(13);
+        // warp fold: the max first (shuffles only), then each lane's sum rescaled to it
+        // once and summed (one exponential per column instead of one per level)
 #pragma unroll
         for (int c = 0; c < NCP; ++c) {
+            float M = rm[c];
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const float m2 = __shfl_xor_sync(0xffffffffu, rm[c], off);
-                const float l2 = __shfl_xor_sync(0xffffffffu, rl[c], off);
-                const float M = fmaxf(rm[c], m2);
-                if (M != -INFINITY) {
-                    rl[c] = rl[c] * fast_exp2(rm[c] - M) + l2 * fast_exp2(m2 - M);
-                    rm[c] = M;
-                }
-            }
+            for (int off = 1; off < 32; off <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            float l = (M == -INFINITY) ? 0.f : rl[c] * fast_exp2(rm[c] - M);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+            rm[c] = M;
+            rl[c] = l;
             if (lane == 0) wpart[warp * NCP + c] = make_float2(rm[c], rl[c]);
         }
+        if (warp == 4 && lane == 0) tstamp(14);
     } else if (warp >= 8) {
         // visual stages, second half of d: warp w takes tile j = 2 (w % 4) + (w - 8) / 4
         // (rows 16 j .. 16 j + 15 lie in its TMEM lane quarter w % 4), mma.sync from the
@@ -571,9 +596,11 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 }
                 if (gid == 0) wpart[warp * NCP + nt * 8 + 2 * t + e2] = make_float2(rm[nt][e2], rl[nt][e2]);
             }
+        if (warp == 8 && lane == 0) tstamp(15);
     }
     if (warp < 4)
         for (int c = lane; c < NCP; c += 32) wpart[warp * NCP + c] = make_float2(-INFINITY, 0.f);
+    if (warp == 1 && lane == 0) tstamp(29);
     tc_fence_before();
     cta_sync();  // ring drained: every MMA completed (accf waited), text stage consumed
     tc_fence_after();

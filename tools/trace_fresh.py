@@ -1,8 +1,13 @@
 """Phase timeline of the fused fresh-step kernel (SVL_TRACE=1 debug stamps).
 usage: python tools/trace_fresh.py [config]"""
-import os, sys
-os.environ["SVL_TRACE"] = "1"
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+if "SVL_LIB" not in os.environ:  # a phase-stamp build (SVL_TRACE_BUILD) in build/trace/
+    env = dict(os.environ, SVL_VARIANT="trace", SVL_DEFS="-DSVL_TRACE_BUILD=1")
+    subprocess.run([sys.executable, "-m", "paper_2510_17777_b200.build"], cwd=ROOT, env=env, check=True,
+                   stdout=subprocess.DEVNULL)
+    os.environ["SVL_LIB"] = os.path.join(ROOT, "build", "trace", "libsparsevila.so")
 import torch
 from paper_2510_17777_b200 import inputs as gen, svl
 name = sys.argv[1] if len(sys.argv) > 1 else "long-video"
@@ -10,7 +15,11 @@ wl = gen.CONFIGS[name]
 NL = int(os.environ.get("TRACE_LAYERS", "28"))  # rotating layers: the traced one is cold in L2
 xs = [gen.make_decode_inputs(wl, seed=s, device="cuda") for s in range(NL)]
 ws = svl.Workspace()
-ws.get(svl.fresh_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
+ws.get(max(svl.fresh_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity), 1024 + (1 << 20)))
+_a = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+_b = torch.empty_like(_a)
+for _ in range(2000):  # ~1 s of copies: the SM clock ramps up from idle
+    _b.copy_(_a)
 for rep in range(2):
     for it in range(NL):
         x = xs[it]
@@ -30,6 +39,14 @@ for ph, nm in names.items():
         continue
     v = (col - t0).double() / 1e3
     print(f"  {ph:2d} {nm:10s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
+
+post = {13: "LSE warps: last stage", 14: "LSE warps: folded", 15: "LDS warps: folded", 29: "MMA warp: done"}
+print("end of the stream (us from start, median):")
+for j, nm in post.items():
+    col = tr[:, j]
+    if (col == 0).any():
+        continue
+    print(f"   {nm:24s} {((col - tr[:, 0]).double() / 1e3).median().item():8.2f}")
 
 sub = ["cand-hist", "find", "flags", "mine", "scan", "off", "-", "-", "-", "-", "-", "-", "-"]
 print("resolve internals (us from gather-issue, median):")
