@@ -80,6 +80,10 @@ typedef enum {
  * sequence-split cache: seq_len >= vb + visual_len suffices
  * (the query rows live in another shard's view). */
 #define SVL_SHARD_VIEW 0x1000u
+/* svl_sparse_decode_attn(_push): merge the splits through L2 (epoch-tagged
+ * partials, co-resident grid) even when the split count would allow a
+ * thread-block cluster per unit merged over DSMEM (A/B measurements, tests). */
+#define SVL_DECODE_GRID_MERGE 0x2000u
 /* Split-count pin, flags bits 24..31 (0 = the planner's choice).
  * svl_sparse_decode_attn(_push): exactly n CTAs per (b, KV group) unit
  * (B*Hkv*n must not exceed the co-resident CTA count when n > 1, else

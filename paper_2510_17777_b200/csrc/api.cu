@@ -123,7 +123,8 @@ static RetrieveTcLayout retrieve_tc_layout(int B, int n_q, int H, int Hkv, int d
 // Splits per unit.  The grid (units x S CTAs) never exceeds the co-resident CTA
 // count (the split merge is a grid-wide barrier), so S = floor(SMs * occ / units)
 // for occ in {1, 2} CTAs per SM, at least kDecodeMinRows attended rows per CTA;
-// of the two the one with the smaller per-SM row load (ties: more CTAs).
+// of the two the one with the smaller per-SM row load (ties: more CTAs); <= 16 splits run
+// as one thread-block cluster per unit (DSMEM merge), more as a co-resident grid (L2 merge).
 constexpr int kDecodeMinRows = 32;
 #ifndef SVL_DECODE_OCC
 #define SVL_DECODE_OCC 2  // (the kernel's shared memory allows one CTA per SM today)
@@ -148,6 +149,10 @@ static int plan_splits(int units, int n_att_max, int d, uint32_t flags) {
             bestS = S;
         }
     }
+    // few units (<= 7 co-resident clusters of 16): one 16-CTA cluster per unit merging over
+    // DSMEM beats spreading the unit over more SMs with the L2 merge (measured, us/layer:
+    // long-video 9.65 vs 10.37 at S = 37, nvila-4k 7.32 vs 8.69)
+    if (bestS > 16 && units * 16 <= 7 * 16 && !(flags & SVL_DECODE_GRID_MERGE)) bestS = std::min(16, smax);
     return bestS;
 }
 
@@ -550,7 +555,7 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
                                      const PushArgs& push, const char* name) {
     if (!q || (!out && push.P == 0) || !span.seq_len || (k > 0 && !vis_idx))
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
-    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK | SVL_IDX_PADDED))
+    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK | SVL_IDX_PADDED | SVL_DECODE_GRID_MERGE))
         return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
     if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
     if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
@@ -576,7 +581,10 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     const int units = B * Hkv;
     const int n_att_max = std::max(1, k + std::max(0, K.capacity - span.visual_len));
     const int S = plan_splits(units, n_att_max, d, flags);
-    if (S > 1 && ((long)units * S > decode_slots(d) || units > kWsEpochs))
+    // <= 16 splits: the unit's CTAs form one cluster and merge over DSMEM (no co-residency
+    // requirement across units); more: the grid merge through L2 (co-resident grid)
+    const int cluster = (S > 1 && S <= 16 && !(flags & SVL_DECODE_GRID_MERGE)) ? 1 : 0;
+    if (S > 1 && !cluster && ((long)units * S > decode_slots(d) || units > kWsEpochs))
         return fail(SVL_ERR_UNSUPPORTED, "pinned split count: B*Hkv*n exceeds the co-resident CTA count%s");
     if (ws_bytes < decode_ws_bytes(units, S, d)) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
 
@@ -592,6 +600,7 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     p.vb = span.visual_begin; p.nv = span.visual_len; p.k = k;
     p.shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
     p.padded = (flags & SVL_IDX_PADDED) ? 1 : 0;
+    p.cluster = cluster;
     p.capacity = K.capacity;
     p.S = S;
     // rows of one split <= ceil(vb / S) + ceil(k / S) + ceil(T_max / S) (three segments)

@@ -55,7 +55,12 @@ struct DecodeSmem {
     static constexpr int WML_OFF = ROWS_OFF + NB * RB * 4;          // per-warp m, l [2][NW][16] fp32
     static constexpr int RUN_OFF = WML_OFF + 2 * NW * 16 * 4;       // CTA M[16], l[16]
     static constexpr int SC_OFF = RUN_OFF + 32 * 4;                 // warp scales [NW][16]
-    static constexpr int BYTES = SC_OFF + NW * 16 * 4;
+    // cluster merge (DSMEM): every peer's share of this CTA's items [S][per] and its M, l
+    // [S][32]; per = ceil(g D / S) -> S * per <= 16 D + 16; mbarrier counting the bytes
+    static constexpr int RCV_OFF = SC_OFF + NW * 16 * 4;
+    static constexpr int RML_OFF = RCV_OFF + (16 * D + 16) * 4;
+    static constexpr int MB_OFF = RML_OFF + 16 * 32 * 4;
+    static constexpr int BYTES = MB_OFF + 16;
 };
 
 // swizzles (physical 16-byte chunk within a row)
@@ -122,13 +127,26 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
 #endif
     // programmatic dependent launch: nothing an upstream kernel may write (seq_len,
     // idx, q, the appended K/V row) is read before the wait
+    // cluster merge: one local arrival + the bytes every peer will push (its share of this
+    // CTA's items and its 32 M, l values); peers push only after their cluster_wait
+    const uint32_t mbar = smem_u32(smem + SM::MB_OFF);
+    if (p.cluster) {
+        if (tid == 0) {
+            const int items = p.g * D, per = (items + S - 1) / S;
+            const int mine = max(0, min(per, items - split * per));
+            mbar_init(mbar, 1);
+            mbar_arrive_expect_tx(mbar, (uint32_t)(S * (mine + 32) * 4));
+            fence_mbar_init();
+        }
+        cluster_arrive_relaxed();
+    }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int b = u / p.Hkv, G = u % p.Hkv;
     const int U = p.shared ? 1 : p.Hkv;
     const int uG = p.shared ? 0 : G;
     // this call's epoch of the unit (advanced by split 0 at the end of the previous call)
-    const uint32_t tag_epoch = (S > 1) ? ld_relaxed_u32(p.epochs + u) : 0u;
+    const uint32_t tag_epoch = (S > 1 && !p.cluster) ? ld_relaxed_u32(p.epochs + u) : 0u;
     // tag = hash(epoch, unit, S): a slot left by another call -- another epoch, or another
     // split layout of the same workspace -- does not match (zero-filled slots never do)
     const uint32_t tag = partial_tag(tag_epoch, (uint32_t)u, (uint32_t)S);
@@ -415,6 +433,54 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             const float den = run[16 + h];
             finalize(h, c, den > 0.f ? cta_o(h, c) / den : 0.f, run[h], den);
         }
+    } else if (p.cluster) {
+        // the S CTAs of the unit form one cluster: every CTA pushes each item of the unit's
+        // g x D block to its owner q = i / per (st.async into q's receive buffer, counted on
+        // q's mbarrier) and its 32 (M, l) to every peer; owners merge in rank order
+        const int items = p.g * D, per = (items + S - 1) / S;
+        float* rcv = reinterpret_cast<float*>(smem + SM::RCV_OFF);  // [S][per]
+        float* rml = reinterpret_cast<float*>(smem + SM::RML_OFF);  // [S][32]
+        cluster_wait();  // every peer has armed its barrier
+        const uint32_t rcv_a = smem_u32(rcv), rml_a = smem_u32(rml);
+        for (int i = tid; i < items; i += NTH) {
+            const int q = i / per;
+            st_async_f32(mapa_shared(rcv_a + (uint32_t)(split * per + (i - q * per)) * 4u, q),
+                         cta_o(i / D, i % D), mapa_shared(mbar, q));
+        }
+        for (int i = tid; i < 32 * S; i += NTH) {
+            const int q = i >> 5, h = i & 31;
+            st_async_f32(mapa_shared(rml_a + (uint32_t)(split * 32 + h) * 4u, q), run[h], mapa_shared(mbar, q));
+        }
+        stamp(5);
+        mbar_wait(mbar, 0);  // every peer's bytes landed
+        __syncwarp();
+        stamp(8);
+        const int i0 = split * per, ni = max(0, min(per, items - i0));
+        int T = 32;
+        while (T > 1 && T * ni > 2 * NTH) T >>= 1;
+        for (int jb = 0; jb < ni; jb += NTH / T) {
+            const int j = jb + tid / T, sub = tid & (T - 1);
+            const int h = (j < ni) ? (i0 + j) / D : 0;
+            float M = -INFINITY;
+            if (j < ni)
+                for (int q = sub; q < S; q += T) M = fmaxf(M, rml[q * 32 + h]);
+            for (int off = T >> 1; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            float num = 0.f, den = 0.f;
+            if (j < ni && M != -INFINITY)
+                for (int q = sub; q < S; q += T) {
+                    const float w = fast_exp2(rml[q * 32 + h] - M);
+                    num += w * rcv[q * per + j];
+                    den += w * rml[q * 32 + 16 + h];
+                }
+            for (int off = T >> 1; off > 0; off >>= 1) {
+                num += __shfl_xor_sync(0xffffffffu, num, off);
+                den += __shfl_xor_sync(0xffffffffu, den, off);
+            }
+            if (sub == 0 && j < ni) finalize(h, (i0 + j) % D, (den > 0.f) ? num / den : 0.f, M, den);
+        }
+        stamp(9);
+        // no closing cluster barrier: nobody reads a peer's shared memory, and every CTA
+        // waited for all the bytes pushed into it before getting here
     } else {
         // Partial (o, M, l) of this split -> workspace slot (u, split), every value stored as a
         // 64-bit (bits, tag) pair with one single-copy-atomic store; tag = the unit's call
@@ -576,6 +642,7 @@ cudaError_t prepare_decode_t() {
     cudaGetDevice(&dev);
     if (dev < 64 && attr_done[dev]) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(decode_kernel<D, NB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess) e = set_max_carveout(decode_kernel<D, NB>);
     if (e == cudaSuccess && dev < 64) attr_done[dev] = true;
     return e;
@@ -594,10 +661,17 @@ cudaError_t launch_decode_t(const DecodeParams& p, cudaStream_t s) {
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see griddepcontrol in the kernel
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    // the merge polls other CTAs' partials: every CTA must be resident -- the grid is sized
-    // to the co-resident count, and a cooperative launch makes the runtime guarantee it
-    attr[1].id = cudaLaunchAttributeCooperative;
-    attr[1].val.cooperative = 1;
+    if (p.cluster) {  // the unit's S CTAs merge over DSMEM
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = p.S;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+    } else {
+        // the grid merge polls other CTAs' partials: every CTA must be resident -- the grid is
+        // sized to the co-resident count, and a cooperative launch makes the runtime guarantee it
+        attr[1].id = cudaLaunchAttributeCooperative;
+        attr[1].val.cooperative = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = p.S > 1 ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, decode_kernel<D, NB>, p);

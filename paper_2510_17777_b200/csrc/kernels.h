@@ -67,6 +67,7 @@ struct DecodeParams {
     int S;             // splits (CTAs) per unit; the grid (S x units) is co-resident
     int single_batch;  // every split has <= kDecodeRowsMax rows (host bound): one gather buffer
     int padded;        // SVL_IDX_PADDED: trailing -1 entries of vis_idx are skipped silently
+    int cluster;       // 1: the S CTAs of a unit are one thread-block cluster, merged over DSMEM
     float scale2;  // scale * log2(e)
     float* out;    // [B][H][d]
     float* lse_out;

@@ -36,22 +36,25 @@ def _case(orc, name, seed):
     return wl, dev, torch.as_tensor(oi).cuda(), oo, ol
 
 
-@pytest.mark.parametrize("name,splits", [("toy", [1, 2, 7, 74]),
-                                         ("long-video", [1, 3, 16, 37])])
+@pytest.mark.parametrize("name,splits", [("toy", [1, 2, 7, 16, 74]),
+                                         ("long-video", [1, 3, 8, 16, 37])])
 def test_decode_any_split_count_matches_oracle(svl, orc, name, splits):
     wl, dev, idx, oo, ol = _case(orc, name, seed=81)
     ws = svl.Workspace()
     for S in splits:
-        lse = torch.empty(wl.B, wl.H, device="cuda")
-        a, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
-                                      flags=svl.SVL_PIN_SPLITS(S), lse_out=lse, ws=ws)
-        a, lse_a = a.clone(), lse.clone()
-        b, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
-                                      flags=svl.SVL_PIN_SPLITS(S), lse_out=lse, ws=ws)
-        torch.cuda.synchronize()
-        assert torch.equal(a, b) and torch.equal(lse_a, lse), f"S={S} not bitwise repeatable"
-        mx, rel = parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)
-        print(f"{name} S={S}: max-abs {mx:.2e} rel {rel:.2e}")
+        # S <= 16: the cluster (DSMEM) merge by default, and the grid (L2) merge forced
+        for extra in ((0, svl.SVL_DECODE_GRID_MERGE) if 1 < S <= 16 else (0,)):
+            fl = svl.SVL_PIN_SPLITS(S) | extra
+            lse = torch.empty(wl.B, wl.H, device="cuda")
+            a, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                          flags=fl, lse_out=lse, ws=ws)
+            a, lse_a = a.clone(), lse.clone()
+            b, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                          flags=fl, lse_out=lse, ws=ws)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b) and torch.equal(lse_a, lse), f"S={S} not bitwise repeatable"
+            mx, rel = parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)
+            print(f"{name} S={S} flags={fl:#x}: max-abs {mx:.2e} rel {rel:.2e}")
     assert ws.flags() == 0
     # the header counters are back to zero after every call
     assert int(ws.buf[12:16].view(torch.int32).abs().sum()) == 0  # the push counter (header word 3)

@@ -16,7 +16,7 @@ def run(name, pins, layers=28, steps=200):
     res = {}
     for pin in pins:
         ws = svl.Workspace()
-        fl = svl.SVL_PIN_SPLITS(pin) if pin else 0
+        fl = (svl.SVL_PIN_SPLITS(abs(pin)) if pin else 0) | (svl.SVL_DECODE_GRID_MERGE if pin < 0 else 0)
         def body():
             for l in range(nl):
                 svl.sparse_decode_attn(xs[l]["q_dec"], xs[l]["K"], xs[l]["V"], xs[l]["seq_len"], wl.vb, wl.nv,
@@ -58,7 +58,7 @@ for _ in range(2000):  # ~1 s of copies: the SM clock ramps up from idle (a GEMM
     _b.copy_(_a)
 torch.cuda.synchronize()
 print("lib", svl.LIB_PATH, tag)
-run("long-video", [0, 37, 16, 8])
-run("nvila-4k", [0, 37, 16])
-run("multi-turn", [0, 4, 9])
-run("sweep", [0, 2, 4])
+run("long-video", [0, 16, -16, 8, 4])
+run("nvila-4k", [0, 16, 8])
+run("multi-turn", [0, -4, 4, 2])
+run("sweep", [0, -2, 2, 1])
