@@ -59,7 +59,7 @@ struct DecodeSmem {
     // [S][32]; per = ceil(g D / S) -> S * per <= 16 D + 16; mbarrier counting the bytes
     static constexpr int RCV_OFF = SC_OFF + NW * 16 * 4;
     static constexpr int RML_OFF = RCV_OFF + (16 * D + 16) * 4;
-    static constexpr int MB_OFF = RML_OFF + 16 * 32 * 4;
+    static constexpr int MB_OFF = RML_OFF + 16 * 33 * 4;  // rml rows padded to 33 (bank-conflict free)
     static constexpr int BYTES = MB_OFF + 16;
 };
 
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         // q's mbarrier) and its 32 (M, l) to every peer; owners merge in rank order
         const int items = p.g * D, per = (items + S - 1) / S;
         float* rcv = reinterpret_cast<float*>(smem + SM::RCV_OFF);  // [S][per]
-        float* rml = reinterpret_cast<float*>(smem + SM::RML_OFF);  // [S][32]
+        float* rml = reinterpret_cast<float*>(smem + SM::RML_OFF);  // [S][33]: M[16], l[16], pad
         cluster_wait();  // every peer has armed its barrier
         const uint32_t rcv_a = smem_u32(rcv), rml_a = smem_u32(rml);
         for (int i = tid; i < items; i += NTH) {
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         }
         for (int i = tid; i < 32 * S; i += NTH) {
             const int q = i >> 5, h = i & 31;
-            st_async_f32(mapa_shared(rml_a + (uint32_t)(split * 32 + h) * 4u, q), run[h], mapa_shared(mbar, q));
+            st_async_f32(mapa_shared(rml_a + (uint32_t)(split * 33 + h) * 4u, q), run[h], mapa_shared(mbar, q));
         }
         stamp(5);
         mbar_wait(mbar, 0);  // every peer's bytes landed
@@ -463,14 +463,14 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             const int h = (j < ni) ? (i0 + j) / D : 0;
             float M = -INFINITY;
             if (j < ni)
-                for (int q = sub; q < S; q += T) M = fmaxf(M, rml[q * 32 + h]);
+                for (int q = sub; q < S; q += T) M = fmaxf(M, rml[q * 33 + h]);
             for (int off = T >> 1; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
             float num = 0.f, den = 0.f;
             if (j < ni && M != -INFINITY)
                 for (int q = sub; q < S; q += T) {
-                    const float w = fast_exp2(rml[q * 32 + h] - M);
+                    const float w = fast_exp2(rml[q * 33 + h] - M);
                     num += w * rcv[q * per + j];
-                    den += w * rml[q * 32 + 16 + h];
+                    den += w * rml[q * 33 + 16 + h];
                 }
             for (int off = T >> 1; off > 0; off >>= 1) {
                 num += __shfl_xor_sync(0xffffffffu, num, off);

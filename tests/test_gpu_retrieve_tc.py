@@ -99,3 +99,11 @@ def test_retrieve_tc_deterministic(svl):
         idx = svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k, scores_out=sc)
         outs.append((idx.clone(), sc.clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_retrieve_tc_four_wave_row_lse_branch(svl, orc):
+    """n_q = 512 question rows (3584 per KV group, 28 query blocks): the row-LSE pass takes
+    the planner's 4-wave branch (units x query blocks x 2 >= SMs) that the bench's n_q = 512
+    run uses (retrieve_tc.cu plan_retrieve_tc); FULL_PREFIX, scores and indices vs the oracle."""
+    wl = gen.DecodeWorkload("tc4w", 1, 28, 4, 128, 32, 4096, 600, 1024, 512, 256)
+    _run(svl, orc, wl, seed=77)

@@ -46,9 +46,8 @@ tr = tr[tr[:, 0] > 0]
 # stamps 0..13: SM cycles (clock64) of the CTA; 14 / 15: globaltimer at start / end
 f_ghz = ((tr[:, 7] - tr[:, 0]).double() / (tr[:, 15] - tr[:, 14]).double())
 print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {f_ghz.median() * 1e3:.0f} MHz")
-names = {1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 10: "b0 scores+max",
-         11: "b0 P table", 4: "compute done", 5: "partial stored", 8: "merge loads (polled)",
-         9: "merge weights", 7: "merged"}
+names = {1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 4: "compute done",
+         5: "partial stored/pushed", 8: "partials landed", 9: "merged", 7: "end"}
 print(f"{name} decode pin={pin}: {tr.shape[0]} CTAs; per-CTA cycles from its start -> us at its clock "
       f"(min / median / max); kernel span {((tr[:, 15].max() - tr[:, 14].min()) / 1e3).item():.2f} us")
 for ph, nm in names.items():
