@@ -831,7 +831,9 @@ def main():
     if "WORLD_SIZE" in os.environ and args.gpus not in (1, world):
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.launch_check:
-        print(json.dumps({"launch_check": True, "rank": rank, "world": world, "local_rank": local}), flush=True)
+        # one write(2) per rank: the ranks share the pipe, and print's separate newline write interleaves
+        sys.stdout.flush()
+        os.write(1, (json.dumps({"launch_check": True, "rank": rank, "world": world, "local_rank": local}) + "\n").encode())
         return 0
     if args.impl == "reference":
         return run_reference(args)

@@ -160,6 +160,44 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
 size_t svl_retrieve_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
                                    int32_t visual_len, uint32_t flags);
 
+/*
+ * svl_question_attention -- the attention output of the question chunk, the
+ * prefill-attention product the retrieval pass accompanies (PAPER.md:124,
+ * section 3.2: the relevance kernel "executes concurrently with the
+ * FlashAttention2 path during prefill").  For each
+ * (b, r, h), r < n_q the question rows (the last n_q rows of seq_len[b]),
+ * G = h / g, over the key range j of svl_retrieve's normalisation (the causal
+ * prefix j <= seq_len[b] - n_q + r, or the visual rows only with
+ * SVL_NORM_VISUAL_ONLY):
+ *   LSE[r,h]   = lse_in[b,r,h] if lse_in != NULL, else log sum_j exp(s[r,h,j])
+ *   out[r,h,:] = sum_j exp(s[r,h,j] - LSE[r,h]) V[b,G,j,:]
+ * with s = scale * q . K_j.  All steps run on the tensor cores (tcgen05): the
+ * row-LSE pass of svl_retrieve (skipped with lse_in), then one pass per key
+ * chunk computing S, P = exp(S - LSE) rounded to bf16 (reading A24) and P.V;
+ * the chunks' partial outputs are summed in chunk order (deterministic).
+ * Passing this call's lse_out as svl_retrieve's lse_in runs the retrieval's
+ * column-mass pass on the same normalisation without recomputing the LSE.
+ *
+ * q        device bf16 [B][n_q][H][d] contiguous; n_q * g <= 4096.
+ * K, V     device KV views (svl_kv), both encodable as TMA tensor maps
+ *          (16-B aligned base, strides multiples of 8 elements), else
+ *          SVL_ERR_UNSUPPORTED.
+ * span     as svl_retrieve; visual_begin + visual_len + n_q <= capacity.
+ * lse_in   device fp32 [B][n_q][H] (natural log) or NULL.
+ * flags    0 or SVL_NORM_VISUAL_ONLY.
+ * out      device fp32 [B][n_q][H][d] (written).
+ * lse_out  device fp32 [B][n_q][H] natural-log LSE used, or NULL.
+ * workspace  svl_question_attention_workspace_size bytes, 16-B aligned.
+ * Device flags: SVL_DEVFLAG_SPAN when seq_len[b] is outside
+ * [visual_begin + visual_len + n_q, capacity] (clamped).
+ */
+svl_status svl_question_attention(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                  svl_kv K, svl_kv V, svl_span span, const float* lse_in, float scale,
+                                  uint32_t flags, float* out, float* lse_out, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+size_t svl_question_attention_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                             int32_t visual_len, uint32_t flags);
+
 /* ---------------------------------------------------- sparse decode attn */
 /*
  * svl_sparse_decode_attn -- decode attention over the active set

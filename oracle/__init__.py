@@ -255,6 +255,56 @@ def retrieve_pages(q, kmax, kmin, k_pages: int, scale: float | None = None):
     return idx, sc, gap
 
 
+def question_attention(q, K, V, seq_len, vb: int, nv: int, scale: float | None = None, flags: int = 0,
+                       lse_in=None):
+    """The question chunk's attention output: PAPER.md:124 runs the
+    query-aware retrieval "concurrently with the FlashAttention2 path during prefill";
+    this is that path's product for the n_q question rows (the last n_q rows of seq_len[b]),
+    written from the definition of softmax attention, in float64 numpy:
+        s[r,h,j] = scale * q[b,r,h,:] . K[b,G,j,:],  G = h // g,
+                   j in the causal prefix j <= seq_len - n_q + r
+                   (the visual rows [vb, vb+nv) only with VISUAL_ONLY),
+        LSE[r,h] = lse_in[b,r,h] if given else log sum_j exp(s[r,h,j]),
+        out[r,h] = sum_j exp(s[r,h,j] - LSE[r,h]) V[b,G,j,:].
+    Returns (out [B][n_q][H][d], lse [B][n_q][H], absmass [B][n_q][H][d] =
+    sum_j exp(s - LSE) |V_j| -- the scale of the rounding bound on out, reading A24)."""
+    B, n_q, H, d = q.shape
+    Hkv = K.shape[1]
+    g = H // Hkv
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    qd = q.to(torch.float64).numpy()
+    Kd = K.to(torch.float64).numpy()
+    Vd = V.to(torch.float64).numpy()
+    sl = seq_len.to(torch.int64).numpy()
+    li = None if lse_in is None else np.asarray(lse_in, dtype=np.float64).reshape(B, n_q, H)
+    out = np.zeros((B, n_q, H, d))
+    lse = np.zeros((B, n_q, H))
+    absmass = np.zeros((B, n_q, H, d))
+    for b in range(B):
+        L = int(sl[b])
+        for G in range(Hkv):
+            for r in range(n_q):
+                if flags & VISUAL_ONLY:
+                    lo, hi = vb, vb + nv
+                else:
+                    lo, hi = 0, L - n_q + r + 1
+                Kr = Kd[b, G, lo:hi]                       # [n][d]
+                Vr = Vd[b, G, lo:hi]
+                qr = qd[b, r, G * g:(G + 1) * g]            # [g][d]
+                s = scale * (Kr @ qr.T)                     # [n][g]
+                if li is None:
+                    m = s.max(axis=0)
+                    lr = m + np.log(np.exp(s - m).sum(axis=0))
+                else:
+                    lr = li[b, r, G * g:(G + 1) * g]
+                p = np.exp(s - lr)                          # [n][g]
+                out[b, r, G * g:(G + 1) * g] = p.T @ Vr
+                absmass[b, r, G * g:(G + 1) * g] = p.T @ np.abs(Vr)
+                lse[b, r, G * g:(G + 1) * g] = lr
+    return out, lse, absmass
+
+
 def pages_to_rows(page_idx, page: int):
     """Ascending page indices -> the ascending visual rows they cover (relative to vb)."""
     pi = np.asarray(page_idx, dtype=np.int64)

@@ -264,6 +264,7 @@ static svl_status check_kv(const svl_kv& kv, int B, int Hkv, int d, const char* 
         return fail(SVL_ERR_ALIGNMENT, "%s strides must be multiples of 8 elements", name);
     if (kv.stride_t < d || kv.capacity < 1)
         return fail(SVL_ERR_SHAPE, "%s stride_t < d or capacity < 1", name);
+    if (kv.stride_h < 0 || kv.stride_b < 0) return fail(SVL_ERR_SHAPE, "%s has a negative stride", name);
     (void)B;
     (void)Hkv;
     return SVL_OK;
@@ -330,6 +331,77 @@ size_t svl_retrieve_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hk
             .total;
     ScorePlan pl = plan_score(B * Hkv, n_q, g, visual_len, device_sm_count());
     return retrieve_layout(B, Hkv, visual_len, pl).total;
+}
+
+// ------------------------------------- question-chunk attention
+static size_t question_attn_part_off(const RetrieveTcLayout& l) { return l.total; }
+static size_t question_attn_total(const RetrieveTcLayout& l, int units, int d) {
+    return round_up(l.total + (size_t)units * l.NQP * l.nkc * d * sizeof(float), 256);
+}
+
+size_t svl_question_attention_workspace_size(int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                             int32_t visual_len, uint32_t flags) {
+    if (B < 1 || n_q < 1 || Hkv < 1 || H % Hkv || visual_len < 1 || (d != 64 && d != 128)) return 0;
+    const RetrieveTcLayout l =
+        retrieve_tc_layout(B, n_q, H, Hkv, d, visual_len, visual_len, (flags & SVL_NORM_VISUAL_ONLY) != 0);
+    return question_attn_total(l, B * Hkv, d);
+}
+
+svl_status svl_question_attention(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,
+                                  svl_kv K, svl_kv V, svl_span span, const float* lse_in, float scale,
+                                  uint32_t flags, float* out, float* lse_out, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    if (!q || !out || !span.seq_len) return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
+    if (flags & ~SVL_NORM_VISUAL_ONLY) return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
+    if (B < 1 || n_q < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, n_q, H, Hkv must be >= 1%s");
+    if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
+    if (span.visual_len < 1) return fail(SVL_ERR_SHAPE, "no visual rows%s");
+    if (span.visual_begin < 0 || (int64_t)span.visual_begin + span.visual_len + n_q > (int64_t)K.capacity ||
+        K.capacity != V.capacity)
+        return fail(SVL_ERR_SHAPE, "visual span + query rows outside the KV capacity (or K/V capacities differ)%s");
+    if (!(scale > 0.f) || !isfinite(scale)) return fail(SVL_ERR_INVALID_ARGUMENT, "scale must be finite > 0%s");
+    if (d != 64 && d != 128) return fail(SVL_ERR_UNSUPPORTED, "head dim must be 64 or 128%s");
+    const int g = H / Hkv;
+    if (n_q * g > kRtMaxNQ) return fail(SVL_ERR_UNSUPPORTED, "n_q * g must be <= 4096%s");
+    if (!aligned16(q) || !aligned16(out)) return fail(SVL_ERR_ALIGNMENT, "q / out not 16-byte aligned%s");
+    svl_status st = check_kv(K, B, Hkv, d, "K");
+    if (st != SVL_OK) return st;
+    st = check_kv(V, B, Hkv, d, "V");
+    if (st != SVL_OK) return st;
+    if (!ws || !aligned16(ws)) return fail(SVL_ERR_WORKSPACE, "workspace NULL or misaligned%s");
+    st = check_device();
+    if (st != SVL_OK) return st;
+    const int units = B * Hkv;
+    const bool vis_only = (flags & SVL_NORM_VISUAL_ONLY) != 0;
+    RetrieveTcLayout lay = retrieve_tc_layout(B, n_q, H, Hkv, d, span.visual_len, K.capacity, vis_only);
+    if (ws_bytes < question_attn_total(lay, units, d)) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    RetrTcParams p;
+    memset(&p, 0, sizeof(p));
+    const int64_t qstride = (int64_t)lay.NQP * d;
+    if (!encode_kv_tensor_map(&p.qmap_x, w + lay.qpack, d, lay.NQP, 1, units, qstride, qstride, d, 128) ||
+        !encode_kv_tensor_map(&p.kmap_x, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 128) ||
+        !encode_kv_tensor_map(&p.kmap_y, K.data, d, K.capacity, Hkv, B, K.stride_b, K.stride_h, K.stride_t, 256) ||
+        !encode_kv_tensor_map(&p.vmap, V.data, d, V.capacity, Hkv, B, V.stride_b, V.stride_h, V.stride_t, 128))
+        return fail(SVL_ERR_UNSUPPORTED, "question attention: K / V view not encodable as a TMA tensor map%s");
+    p.q = static_cast<const uint16_t*>(q);
+    p.qpack = reinterpret_cast<uint16_t*>(w + lay.qpack);
+    p.seq_len = span.seq_len;
+    p.lse_in = lse_in;
+    p.B = B; p.n_q = n_q; p.H = H; p.Hkv = Hkv; p.g = g; p.NQ = lay.NQ; p.NQP = lay.NQP;
+    p.vb = span.visual_begin; p.nv = span.visual_len; p.capacity = K.capacity;
+    p.visual_only = vis_only ? 1 : 0;
+    p.chunk = lay.chunk; p.nkc = lay.nkc; p.npart = 4 * lay.nkc;
+    p.scale2 = scale * kLog2e;
+    p.part = reinterpret_cast<float2*>(w + lay.part);
+    p.lse2 = reinterpret_cast<float*>(w + lay.lse2);
+    p.flags = reinterpret_cast<uint32_t*>(w);
+    p.part_o = reinterpret_cast<float*>(w + question_attn_part_off(lay));
+    p.out = out;
+    p.lse_out = lse_out;
+    const cudaError_t e = launch_question_attn_tc(p, d, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "svl_question_attention");
+    return SVL_OK;
 }
 
 svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_t Hkv, int32_t d,

@@ -136,6 +136,7 @@ struct RetrTcParams {
     CUtensorMap xmap, ymap;      // set by the launcher per pass (resident X tile, streamed Y stages)
     CUtensorMap qmap_x, qmap_y;  // Qpack as 4-D {d, NQP, 1, units}, boxes of 128 / 256 rows
     CUtensorMap kmap_x, kmap_y;  // K cache view {d, capacity, Hkv, B}, boxes of 128 / 256 rows
+    CUtensorMap vmap;            // V cache view, boxes of 128 rows (svl_question_attention)
     const uint16_t* q;           // [B][n_q][H][d]
     uint16_t* qpack;             // [units][NQP][d] (workspace)
     const int32_t* seq_len;
@@ -148,10 +149,14 @@ struct RetrTcParams {
     float* lse2;                 // [units][NQP] base-2 LSE (+inf on padding rows)
     float* scores;               // [units][nv] relevance
     uint32_t* flags;
+    float* part_o;               // [units][NQP][nkc][d] partial outputs (svl_question_attention)
+    float* out;                  // [B][n_q][H][d]
+    float* lse_out;              // [B][n_q][H] natural log, or null
 };
 void plan_retrieve_tc(int units, int n_q, int g, int nv, int capacity, bool visual_only, int sms, int* chunk,
                       int* nkc);
 cudaError_t launch_retrieve_tc(const RetrTcParams& p, int d, cudaStream_t s);
+cudaError_t launch_question_attn_tc(const RetrTcParams& p, int d, cudaStream_t s);
 // ------------------------------------------------------ pack-once
 struct PackParams {
     const uint16_t* K;

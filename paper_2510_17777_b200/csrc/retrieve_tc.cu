@@ -485,6 +485,280 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_mass_qres_kernel(const __g
     }
 }
 
+// ---------------------------------------------------------------------------
+// Question-chunk attention output (svl_question_attention):
+// the attention output the prefill pass produces beside the row LSE
+// (PAPER.md:124 runs the retrieval "concurrently with the FlashAttention2
+// path"; this is that path on the same tensor-core machinery):
+//   O[n] = sum_j 2^(s[n,j] * scale2 - LSE2[n]) V[j]
+// over exactly the key range and causal limit pass 0 folds, with the FINAL
+// LSE2 (pass 0 + combine, or lse_in), so a key chunk's partial output is
+// already normalised and the chunks add without rescaling (no online-softmax
+// correction in TMEM).  Per stage of 128 keys:
+//   S_a = Q_blk K_s^T        tcgen05 M128 N128 K16 x D/16, TMEM columns a*128
+//   P   = 2^(S*scale2 - LSE2) masked, rounded to bf16 (as FlashAttention-2 does
+//         on bf16 inputs, reading A24), written by the epilogue warps into a
+//         K-major 128-B-swizzled shared tile
+//   O  += P V_s              tcgen05 M128 N=D K16 x 8, B = V stage MN-major
+//                            (the TMA tile of V is [keys][d]: d contiguous),
+//                            TMEM columns 256..256+D
+// The MMA issuer runs one stage ahead (S of stage s before P.V of stage s-1),
+// so the exponentials of one stage overlap the products of the next.
+template <int D>
+struct RoSmem {
+    static constexpr int NB = D / 64;
+    static constexpr int KROWS = 128;                    // keys per stage
+    static constexpr int Q_BYTES = NB * RT_XROWS * 128;  // resident Q block
+    static constexpr int KV_BYTES = NB * KROWS * 128;    // one K (or V) stage
+    static constexpr int P_BYTES = 2 * RT_XROWS * 128;   // 128 rows x 128 keys bf16: two 64-key swizzle blocks
+    static constexpr int Q_OFF = 0;
+    static constexpr int K_OFF = Q_OFF + Q_BYTES;       // [2] K stages
+    static constexpr int V_OFF = K_OFF + 2 * KV_BYTES;  // [2] V stages
+    static constexpr int P_OFF = V_OFF + 2 * KV_BYTES;  // [2] P tiles
+    static constexpr int LSE_OFF = P_OFF + 2 * P_BYTES;
+    static constexpr int BAR_OFF = LSE_OFF + RT_XROWS * 4;
+    static constexpr int BYTES = BAR_OFF + 256;
+    static_assert(K_OFF % 1024 == 0 && V_OFF % 1024 == 0 && P_OFF % 1024 == 0, "swizzle atoms");
+    static_assert(BYTES <= 227 * 1024, "shared memory");
+};
+
+// MN-major operand, 128-B swizzle: 8 K-rows of 128 B (64 MN elements) per
+// 1024-B atom; SBO = 1024 (next 8 K rows), LBO = `lbo` bytes (next 64 MN
+// elements).  Advancing K by 16 = +2048 B on the start address.
+SVL_DEV uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)(1024u >> 4) << 32) | ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+
+template <int D>
+__global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_constant__ RetrTcParams p) {
+    using SM = RoSmem<D>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int KR = SM::KROWS;
+    constexpr uint32_t IDESC_S = umma_idesc_bf16(RT_XROWS, KR);
+    constexpr uint32_t IDESC_O = umma_idesc_bf16(RT_XROWS, D) | (1u << 16);  // B (= V) MN-major
+    constexpr int OCOLS = D / 4;                                             // O columns per epilogue warp
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+    const uint32_t qfull = smem_u32(bars), kvfull0 = smem_u32(bars + 1), kvempty0 = smem_u32(bars + 3);
+    const uint32_t sfull0 = smem_u32(bars + 5), sempty0 = smem_u32(bars + 7);
+    const uint32_t pfull0 = smem_u32(bars + 9), pempty0 = smem_u32(bars + 11), ofull = smem_u32(bars + 13);
+    const uint32_t vfix = smem_u32(bars + 14);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 15);
+    const uint32_t sQ = smem_u32(smem + SM::Q_OFF), sK = smem_u32(smem + SM::K_OFF);
+    const uint32_t sV = smem_u32(smem + SM::V_OFF), sP = smem_u32(smem + SM::P_OFF);
+    float* lse_s = reinterpret_cast<float*>(smem + SM::LSE_OFF);
+
+    const int u = blockIdx.z, b = u / p.Hkv, G = u % p.Hkv;
+    int L = p.seq_len[b];
+    if (L < p.vb + p.nv + p.n_q || L > p.capacity) {
+        if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) raise_flag(p.flags, 4u /*SPAN*/);
+        L = min(max(L, p.vb + p.nv + p.n_q), p.capacity);
+    }
+    const int lo = p.visual_only ? p.vb : 0;
+    const int hi = p.visual_only ? p.vb + p.nv : L;
+    const int y0 = lo + blockIdx.x * p.chunk;
+    const int y1 = min(hi, y0 + p.chunk);
+    const int xrow0 = blockIdx.y * RT_XROWS;
+    const int nst = y1 > y0 ? (y1 - y0 + KR - 1) / KR : 0;
+    const int q4 = warp & 3, cg = (warp - 4) >> 2;  // epilogue: TMEM lane quarter, 32-key column group
+    const int row = 32 * q4 + lane;
+    // valid rows of the last stage: V rows past the key range (past seq_len: possibly never
+    // written) are zeroed in shared memory before the last P.V, since 0 * NaN = NaN
+    const int tail = y1 - (y0 + (nst - 1) * KR);
+    float* po = p.part_o + (((int64_t)u * p.NQP + xrow0 + row) * p.nkc + blockIdx.x) * D + cg * OCOLS;
+    if (nst == 0) {  // empty key chunk: a zero partial
+        if (warp >= 4)
+            for (int c = 0; c < OCOLS; c += 4) *reinterpret_cast<float4*>(po + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+
+    if (tid == 0) {
+        mbar_init(qfull, 1);
+        mbar_init(ofull, 1);
+        mbar_init(vfix, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(kvfull0 + 8 * i, 1);
+            mbar_init(kvempty0 + 8 * i, 1);
+            mbar_init(sfull0 + 8 * i, 1);
+            mbar_init(sempty0 + 8 * i, RT_EPI_WARPS);
+            mbar_init(pfull0 + 8 * i, RT_EPI_WARPS);
+            mbar_init(pempty0 + 8 * i, 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(smem_u32(tslot), 512);
+    for (int i = tid; i < RT_XROWS; i += RT_THREADS) lse_s[i] = p.lse2[(int64_t)u * p.NQP + xrow0 + i];
+    tc_fence_before();
+    cta_sync();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(qfull, (uint32_t)SM::Q_BYTES);
+#pragma unroll
+            for (int hf = 0; hf < SM::NB; ++hf)
+                tma_load_4d(sQ + hf * (RT_XROWS * 128), &p.xmap, hf * 64, xrow0, 0, u, qfull);
+            for (int s = 0; s < nst; ++s) {
+                const int slot = s & 1;
+                if (s >= 2) mbar_wait(kvempty0 + 8 * slot, ((s >> 1) - 1) & 1);
+                const uint32_t bar = kvfull0 + 8 * slot;
+                mbar_arrive_expect_tx(bar, (uint32_t)(2 * SM::KV_BYTES));
+#pragma unroll
+                for (int hf = 0; hf < SM::NB; ++hf) {
+                    const int off = slot * SM::KV_BYTES + hf * (KR * 128);
+                    tma_load_4d(sK + off, &p.ymap, hf * 64, y0 + s * KR, G, b, bar);
+                    tma_load_4d(sV + off, &p.vmap, hf * 64, y0 + s * KR, G, b, bar);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_wait(qfull, 0);
+            for (int s = 0; s <= nst; ++s) {
+                if (s < nst) {  // S of stage s
+                    const int a = s & 1;
+                    mbar_wait(kvfull0 + 8 * a, (s >> 1) & 1);
+                    if (s >= 2) mbar_wait(sempty0 + 8 * a, ((s >> 1) - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t kb = sK + a * SM::KV_BYTES;
+#pragma unroll
+                    for (int j = 0; j < D / 16; ++j) {
+                        const int hf = j >> 2, kk = j & 3;
+                        umma_bf16(tbase + a * KR, sw128_desc(sQ + hf * (RT_XROWS * 128) + kk * 32),
+                                  sw128_desc(kb + hf * (KR * 128) + kk * 32), IDESC_S, j > 0 ? 1u : 0u);
+                    }
+                    umma_commit(sfull0 + 8 * a);
+                }
+                if (s >= 1) {  // P.V of stage s - 1
+                    const int t = s - 1, a = t & 1;
+                    mbar_wait(pfull0 + 8 * a, (t >> 1) & 1);
+                    if (t == nst - 1 && tail < KR) mbar_wait(vfix, 0);
+                    tc_fence_after();
+                    const uint32_t pb = sP + a * SM::P_BYTES, vb = sV + a * SM::KV_BYTES;
+#pragma unroll
+                    for (int j = 0; j < KR / 16; ++j) {
+                        const int hf = j >> 2, kk = j & 3;
+                        umma_bf16(tbase + 2 * KR, sw128_desc(pb + hf * (RT_XROWS * 128) + kk * 32),
+                                  sw128_mn_desc(vb + j * 16 * 128, KR * 128), IDESC_O, (t > 0 || j > 0) ? 1u : 0u);
+                    }
+                    umma_commit(kvempty0 + 8 * a);  // K and V of stage t consumed
+                    umma_commit(pempty0 + 8 * a);
+                }
+            }
+            umma_commit(ofull);
+        }
+        __syncwarp();
+    } else if (warp == 3) {
+        if (tail < KR) {
+            const int a = (nst - 1) & 1;
+            mbar_wait(kvfull0 + 8 * a, ((nst - 1) >> 1) & 1);
+#pragma unroll
+            for (int hf = 0; hf < SM::NB; ++hf)
+                for (int i = tail * 8 + lane; i < KR * 8; i += 32)  // 16-B chunks, 8 per 128-B row
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(sV + a * SM::KV_BYTES +
+                                                                                hf * (KR * 128) + i * 16),
+                                 "r"(0u)
+                                 : "memory");
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(vfix);
+        }
+    } else if (warp >= 4) {
+        const uint32_t trow = tbase + ((uint32_t)(32 * q4) << 16);
+        const int n = xrow0 + row;
+        const int r = n / p.g;
+        const int jend = p.visual_only ? y1 : min(y1, L - p.n_q + r + 1);
+        const float lse = lse_s[row];  // +inf on padding rows: P = 0
+        const uint32_t prow = (uint32_t)((cg >> 1) * (RT_XROWS * 128) + row * 128);
+        for (int s = 0; s < nst; ++s) {
+            const int a = s & 1;
+            mbar_wait(sfull0 + 8 * a, (s >> 1) & 1);
+            __syncwarp();  // tcgen05.ld is .aligned
+            tc_fence_after();
+            uint32_t v[32];
+            tmem_ld32_nowait(trow + a * KR + cg * 32, v);
+            tmem_wait_ld_tie(v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sempty0 + 8 * a);
+            const int j0 = y0 + s * KR + cg * 32;
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float x0 = fmaf(__uint_as_float(v[i]), p.scale2, -lse);
+                const float x1 = fmaf(__uint_as_float(v[i + 1]), p.scale2, -lse);
+                float e0 = fast_exp2(x0);
+                float e1 = ((i & 2) == 0) ? fast_exp2(x1) : ((x1 < -126.f) ? 0.f : poly_exp2(x1));
+                if (j0 + i >= jend) e0 = 0.f;
+                if (j0 + i + 1 >= jend) e1 = 0.f;
+                pk[i >> 1] = pack_bf16(e0, e1);
+            }
+            if (s >= 2) mbar_wait(pempty0 + 8 * a, ((s >> 1) - 1) & 1);
+            const uint32_t pbase = sP + a * SM::P_BYTES + prow;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t chunk = (uint32_t)((cg & 1) * 4 + c) ^ (uint32_t)(row & 7);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pbase + chunk * 16), "r"(pk[4 * c]),
+                             "r"(pk[4 * c + 1]), "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
+                             : "memory");
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pfull0 + 8 * a);
+        }
+        mbar_wait(ofull, 0);
+        __syncwarp();
+        tc_fence_after();
+        const uint32_t to = trow + 2 * KR + cg * OCOLS;
+        if constexpr (OCOLS == 32) {
+            uint32_t o[32];
+            tmem_ld32(to, o);
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+                *reinterpret_cast<float4*>(po + c) = make_float4(__uint_as_float(o[c]), __uint_as_float(o[c + 1]),
+                                                                 __uint_as_float(o[c + 2]), __uint_as_float(o[c + 3]));
+        } else {
+            uint32_t o[16];
+            tmem_ld16(to, o);
+#pragma unroll
+            for (int c = 0; c < 16; c += 4)
+                *reinterpret_cast<float4*>(po + c) = make_float4(__uint_as_float(o[c]), __uint_as_float(o[c + 1]),
+                                                                 __uint_as_float(o[c + 2]), __uint_as_float(o[c + 3]));
+        }
+    }
+    tc_fence_before();
+    cta_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tbase, 512);
+    }
+}
+
+// out[b][r][h][:] = sum over key chunks (chunk order) of the partial outputs;
+// lse_out = LSE2 * ln 2.  One thread per (row, 4 columns).
+__global__ void out_combine_kernel(const RetrTcParams p, int D) {
+    const int C4 = D / 4;
+    const int64_t total = (int64_t)p.B * p.Hkv * p.NQ * C4;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c4 = (int)(e % C4);
+        const int n = (int)((e / C4) % p.NQ);
+        const int u = (int)(e / C4 / p.NQ);
+        const float4* src = reinterpret_cast<const float4*>(p.part_o + ((int64_t)u * p.NQP + n) * p.nkc * D) + c4;
+        float4 acc = src[0];
+        for (int k = 1; k < p.nkc; ++k) {
+            const float4 x = src[(int64_t)k * C4];
+            acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+        }
+        const int b = u / p.Hkv, G = u % p.Hkv, r = n / p.g, h = G * p.g + n % p.g;
+        const int64_t orow = ((int64_t)b * p.n_q + r) * p.H + h;
+        reinterpret_cast<float4*>(p.out + orow * D)[c4] = acc;
+        if (c4 == 0 && p.lse_out) p.lse_out[orow] = p.lse2[(int64_t)u * p.NQP + n] * kLn2;
+    }
+}
+
 template <int MODE, int D>
 cudaError_t launch_tc(const RetrTcParams& p, dim3 grid, cudaStream_t s) {
     static bool attr_done[64] = {};
@@ -502,6 +776,50 @@ cudaError_t launch_tc(const RetrTcParams& p, dim3 grid, cudaStream_t s) {
 }
 
 }  // namespace
+
+cudaError_t launch_question_attn_tc(const RetrTcParams& p, int d, cudaStream_t s) {
+    const int units = p.B * p.Hkv;
+    const int sms = device_sm_count();
+    const int64_t qchunks = (int64_t)units * p.NQP * (d / 8);
+    qpack_kernel<<<(int)std::min<int64_t>((qchunks + 255) / 256, 8L * sms), 256, 0, s>>>(p, d);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    RetrTcParams p0 = p;
+    p0.xmap = p.qmap_x;  // X = Q blocks
+    p0.ymap = p.kmap_y;  // Y = K stages (256 rows)
+    const int nqb = (p.NQ + RT_XROWS - 1) / RT_XROWS;
+    if (!p.lse_in) {
+        const dim3 g0(p.nkc, nqb, units);
+        e = d == 128 ? launch_tc<0, 128>(p0, g0, s) : launch_tc<0, 64>(p0, g0, s);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t rows = (int64_t)units * p.NQP;
+    lse_combine_kernel<<<(int)std::min<int64_t>((rows + 7) / 8, 8L * sms), 256, 0, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    RetrTcParams p2 = p;
+    p2.xmap = p.qmap_x;  // X = Q blocks
+    p2.ymap = p.kmap_x;  // K stages of 128 rows (p.vmap: V stages of 128 rows)
+    static bool attr_done[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev][d == 128]) {
+        e = d == 128 ? cudaFuncSetAttribute(retr_out_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            RoSmem<128>::BYTES)
+                     : cudaFuncSetAttribute(retr_out_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            RoSmem<64>::BYTES);
+        if (e != cudaSuccess) return e;
+        attr_done[dev][d == 128] = true;
+    }
+    const dim3 g2(p.nkc, nqb, units);
+    if (d == 128) retr_out_kernel<128><<<g2, RT_THREADS, RoSmem<128>::BYTES, s>>>(p2);
+    else retr_out_kernel<64><<<g2, RT_THREADS, RoSmem<64>::BYTES, s>>>(p2);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t n4 = (int64_t)units * p.NQ * (d / 4);
+    out_combine_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 8L * sms), 256, 0, s>>>(p, d);
+    return cudaGetLastError();
+}
 
 // host plan of pass 0: a fixed number of key chunks per (unit, query block) --
 // about two waves of CTAs, independent of the key range (so the workspace size

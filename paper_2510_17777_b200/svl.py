@@ -48,7 +48,8 @@ EXPORTS = ["svl_retrieve", "svl_retrieve_workspace_size", "svl_sparse_decode_att
            "svl_wait_flags", "svl_pack_kv", "svl_rope_remap", "svl_fresh_decode_plan",
            "svl_page_summary", "svl_retrieve_pages", "svl_retrieve_pages_workspace_size",
            "svl_mrope_remap", "svl_mrope_remap_workspace_size", "svl_retrieve_partial_lse",
-           "svl_lse_combine", "svl_topk", "svl_topk_workspace_size", "svl_shard_indices", "svl_merge_partials"]
+           "svl_lse_combine", "svl_topk", "svl_topk_workspace_size", "svl_shard_indices", "svl_merge_partials",
+           "svl_question_attention", "svl_question_attention_workspace_size"]
 
 
 class SvlError(RuntimeError):
@@ -86,6 +87,11 @@ def lib():
                                    P, P, P, SZ, P]
         L.svl_retrieve_workspace_size.restype = SZ
         L.svl_retrieve_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, U32]
+        L.svl_question_attention.restype = ctypes.c_int
+        L.svl_question_attention.argtypes = [P, I32, I32, I32, I32, I32, svl_kv, svl_kv, svl_span, P, F, U32,
+                                             P, P, P, SZ, P]
+        L.svl_question_attention_workspace_size.restype = SZ
+        L.svl_question_attention_workspace_size.argtypes = [I32, I32, I32, I32, I32, I32, U32]
         if hasattr(L, "svl_rope_remap"):
             L.svl_rope_remap.restype = ctypes.c_int
             L.svl_rope_remap.argtypes = [svl_kv, svl_kv, I32, I32, I32, svl_span, P, I32, D, svl_kv, svl_kv,
@@ -269,6 +275,37 @@ def retrieve(q: torch.Tensor, K: torch.Tensor, seq_len: torch.Tensor, visual_beg
         _cuda(scores_out, "scores_out", torch.float32) if scores_out is not None else None,
         w.data_ptr(), w.numel(), _stream(stream)))
     return idx_out
+
+
+def question_attention_workspace_size(B, n_q, H, Hkv, d, visual_len, flags=0) -> int:
+    return int(lib().svl_question_attention_workspace_size(B, n_q, H, Hkv, d, visual_len, flags))
+
+
+def question_attention(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seq_len: torch.Tensor,
+                       visual_begin: int, visual_len: int, scale: Optional[float] = None, flags: int = 0,
+                       lse_in: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                       lse_out: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None, stream=None):
+    """svl_question_attention (the question chunk's attention output).
+    q bf16 [B][n_q][H][d]; K, V bf16 [B][Hkv][cap][d].  Returns (out fp32 [B][n_q][H][d],
+    lse fp32 [B][n_q][H] natural log)."""
+    B, n_q, H, d = q.shape
+    Hkv = K.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    _cuda(q, "q", torch.bfloat16)
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous")
+    if out is None:
+        out = torch.empty(B, n_q, H, d, dtype=torch.float32, device=q.device)
+    if lse_out is None:
+        lse_out = torch.empty(B, n_q, H, dtype=torch.float32, device=q.device)
+    w = _ws(ws, q.device).get(question_attention_workspace_size(B, n_q, H, Hkv, d, visual_len, flags))
+    _check(lib().svl_question_attention(
+        q.data_ptr(), B, n_q, H, Hkv, d, kv_view(K), kv_view(V, "V"), span(visual_begin, visual_len, seq_len),
+        _cuda(lse_in, "lse_in", torch.float32) if lse_in is not None else None, scale, flags,
+        _cuda(out, "out", torch.float32), _cuda(lse_out, "lse_out", torch.float32),
+        w.data_ptr(), w.numel(), _stream(stream)))
+    return out, lse_out
 
 
 def rope_remap(K_pre: torch.Tensor, V: Optional[torch.Tensor], seq_len: torch.Tensor, visual_begin: int,
