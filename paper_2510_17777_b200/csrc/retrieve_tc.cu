@@ -504,17 +504,28 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_mass_qres_kernel(const __g
 //                            TMEM columns 256..256+D
 // The MMA issuer runs one stage ahead (S of stage s before P.V of stage s-1),
 // so the exponentials of one stage overlap the products of the next.
-template <int D>
+// PT (default): P goes to tensor memory and the P.V product takes its A operand
+// from TMEM (tcgen05.mma [d], [a_tmem], b_desc) -- no shared-memory P tile, so
+// the K/V ring gets three stages; !PT (A/B builds, SVL_QA_P_SMEM): P in a
+// 128-B-swizzled shared tile, two K/V stages.
+#ifdef SVL_QA_P_SMEM
+constexpr bool kQaPTmem = false;
+#else
+constexpr bool kQaPTmem = true;
+#endif
+
+template <int D, bool PT>
 struct RoSmem {
     static constexpr int NB = D / 64;
     static constexpr int KROWS = 128;                    // keys per stage
+    static constexpr int NKV = PT ? 3 : 2;               // K/V ring stages
     static constexpr int Q_BYTES = NB * RT_XROWS * 128;  // resident Q block
     static constexpr int KV_BYTES = NB * KROWS * 128;    // one K (or V) stage
-    static constexpr int P_BYTES = 2 * RT_XROWS * 128;   // 128 rows x 128 keys bf16: two 64-key swizzle blocks
+    static constexpr int P_BYTES = PT ? 0 : 2 * RT_XROWS * 128;  // 128 rows x 128 keys bf16, two 64-key blocks
     static constexpr int Q_OFF = 0;
-    static constexpr int K_OFF = Q_OFF + Q_BYTES;       // [2] K stages
-    static constexpr int V_OFF = K_OFF + 2 * KV_BYTES;  // [2] V stages
-    static constexpr int P_OFF = V_OFF + 2 * KV_BYTES;  // [2] P tiles
+    static constexpr int K_OFF = Q_OFF + Q_BYTES;         // [NKV] K stages
+    static constexpr int V_OFF = K_OFF + NKV * KV_BYTES;  // [NKV] V stages
+    static constexpr int P_OFF = V_OFF + NKV * KV_BYTES;  // [2] P tiles (!PT)
     static constexpr int LSE_OFF = P_OFF + 2 * P_BYTES;
     static constexpr int BAR_OFF = LSE_OFF + RT_XROWS * 4;
     static constexpr int BYTES = BAR_OFF + 256;
@@ -529,22 +540,33 @@ SVL_DEV uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
            ((uint64_t)(1024u >> 4) << 32) | ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
+// D[tmem] (+)= A[tmem] . B[smem]^T: A (M x 16, bf16 pairs per 32-bit column, lane = row)
+// read from tensor memory.
+SVL_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 
-template <int D>
+// TMEM columns: S_0 [0,128), S_1 [128,256), O [256,256+D), P_0 [384,448), P_1 [448,512)
+template <int D, bool PT>
 __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_constant__ RetrTcParams p) {
-    using SM = RoSmem<D>;
+    using SM = RoSmem<D, PT>;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int KR = SM::KROWS;
+    constexpr int KR = SM::KROWS, NKV = SM::NKV;
+    constexpr int OCOL = 2 * KR, PCOL = 384;
     constexpr uint32_t IDESC_S = umma_idesc_bf16(RT_XROWS, KR);
     constexpr uint32_t IDESC_O = umma_idesc_bf16(RT_XROWS, D) | (1u << 16);  // B (= V) MN-major
     constexpr int OCOLS = D / 4;                                             // O columns per epilogue warp
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
-    const uint32_t qfull = smem_u32(bars), kvfull0 = smem_u32(bars + 1), kvempty0 = smem_u32(bars + 3);
-    const uint32_t sfull0 = smem_u32(bars + 5), sempty0 = smem_u32(bars + 7);
-    const uint32_t pfull0 = smem_u32(bars + 9), pempty0 = smem_u32(bars + 11), ofull = smem_u32(bars + 13);
-    const uint32_t vfix = smem_u32(bars + 14);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 15);
+    const uint32_t qfull = smem_u32(bars), kvfull0 = smem_u32(bars + 1), kvempty0 = smem_u32(bars + 4);
+    const uint32_t sfull0 = smem_u32(bars + 7), sempty0 = smem_u32(bars + 9);
+    const uint32_t pfull0 = smem_u32(bars + 11), pempty0 = smem_u32(bars + 13), ofull = smem_u32(bars + 15);
+    const uint32_t vfix = smem_u32(bars + 16);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 17);
     const uint32_t sQ = smem_u32(smem + SM::Q_OFF), sK = smem_u32(smem + SM::K_OFF);
     const uint32_t sV = smem_u32(smem + SM::V_OFF), sP = smem_u32(smem + SM::P_OFF);
     float* lse_s = reinterpret_cast<float*>(smem + SM::LSE_OFF);
@@ -577,9 +599,11 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_co
         mbar_init(qfull, 1);
         mbar_init(ofull, 1);
         mbar_init(vfix, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NKV; ++i) {
             mbar_init(kvfull0 + 8 * i, 1);
             mbar_init(kvempty0 + 8 * i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(sfull0 + 8 * i, 1);
             mbar_init(sempty0 + 8 * i, RT_EPI_WARPS);
             mbar_init(pfull0 + 8 * i, RT_EPI_WARPS);
@@ -601,8 +625,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_co
             for (int hf = 0; hf < SM::NB; ++hf)
                 tma_load_4d(sQ + hf * (RT_XROWS * 128), &p.xmap, hf * 64, xrow0, 0, u, qfull);
             for (int s = 0; s < nst; ++s) {
-                const int slot = s & 1;
-                if (s >= 2) mbar_wait(kvempty0 + 8 * slot, ((s >> 1) - 1) & 1);
+                const int slot = s % NKV;
+                if (s >= NKV) mbar_wait(kvempty0 + 8 * slot, ((s / NKV) - 1) & 1);
                 const uint32_t bar = kvfull0 + 8 * slot;
                 mbar_arrive_expect_tx(bar, (uint32_t)(2 * SM::KV_BYTES));
 #pragma unroll
@@ -619,11 +643,11 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_co
             mbar_wait(qfull, 0);
             for (int s = 0; s <= nst; ++s) {
                 if (s < nst) {  // S of stage s
-                    const int a = s & 1;
-                    mbar_wait(kvfull0 + 8 * a, (s >> 1) & 1);
+                    const int a = s & 1, slot = s % NKV;
+                    mbar_wait(kvfull0 + 8 * slot, (s / NKV) & 1);
                     if (s >= 2) mbar_wait(sempty0 + 8 * a, ((s >> 1) - 1) & 1);
                     tc_fence_after();
-                    const uint32_t kb = sK + a * SM::KV_BYTES;
+                    const uint32_t kb = sK + slot * SM::KV_BYTES;
 #pragma unroll
                     for (int j = 0; j < D / 16; ++j) {
                         const int hf = j >> 2, kk = j & 3;
@@ -633,18 +657,25 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_co
                     umma_commit(sfull0 + 8 * a);
                 }
                 if (s >= 1) {  // P.V of stage s - 1
-                    const int t = s - 1, a = t & 1;
+                    const int t = s - 1, a = t & 1, slot = t % NKV;
                     mbar_wait(pfull0 + 8 * a, (t >> 1) & 1);
                     if (t == nst - 1 && tail < KR) mbar_wait(vfix, 0);
                     tc_fence_after();
-                    const uint32_t pb = sP + a * SM::P_BYTES, vb = sV + a * SM::KV_BYTES;
+                    const uint32_t vb = sV + slot * SM::KV_BYTES;
 #pragma unroll
                     for (int j = 0; j < KR / 16; ++j) {
-                        const int hf = j >> 2, kk = j & 3;
-                        umma_bf16(tbase + 2 * KR, sw128_desc(pb + hf * (RT_XROWS * 128) + kk * 32),
-                                  sw128_mn_desc(vb + j * 16 * 128, KR * 128), IDESC_O, (t > 0 || j > 0) ? 1u : 0u);
+                        const uint64_t bd = sw128_mn_desc(vb + j * 16 * 128, KR * 128);
+                        const uint32_t acc = (t > 0 || j > 0) ? 1u : 0u;
+                        if constexpr (PT) {
+                            umma_bf16_ts(tbase + OCOL, tbase + PCOL + a * 64 + j * 8, bd, IDESC_O, acc);
+                        } else {
+                            const int hf = j >> 2, kk = j & 3;
+                            umma_bf16(tbase + OCOL,
+                                      sw128_desc(sP + a * SM::P_BYTES + hf * (RT_XROWS * 128) + kk * 32), bd,
+                                      IDESC_O, acc);
+                        }
                     }
-                    umma_commit(kvempty0 + 8 * a);  // K and V of stage t consumed
+                    umma_commit(kvempty0 + 8 * slot);  // K and V of stage t consumed
                     umma_commit(pempty0 + 8 * a);
                 }
             }
@@ -653,12 +684,12 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_co
         __syncwarp();
     } else if (warp == 3) {
         if (tail < KR) {
-            const int a = (nst - 1) & 1;
-            mbar_wait(kvfull0 + 8 * a, ((nst - 1) >> 1) & 1);
+            const int slot = (nst - 1) % NKV;
+            mbar_wait(kvfull0 + 8 * slot, ((nst - 1) / NKV) & 1);
 #pragma unroll
             for (int hf = 0; hf < SM::NB; ++hf)
                 for (int i = tail * 8 + lane; i < KR * 8; i += 32)  // 16-B chunks, 8 per 128-B row
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(sV + a * SM::KV_BYTES +
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(sV + slot * SM::KV_BYTES +
                                                                                 hf * (KR * 128) + i * 16),
                                  "r"(0u)
                                  : "memory");
@@ -697,22 +728,30 @@ __global__ void __launch_bounds__(RT_THREADS, 1) retr_out_kernel(const __grid_co
                 pk[i >> 1] = pack_bf16(e0, e1);
             }
             if (s >= 2) mbar_wait(pempty0 + 8 * a, ((s >> 1) - 1) & 1);
-            const uint32_t pbase = sP + a * SM::P_BYTES + prow;
+            if constexpr (PT) {
+                float pf[16];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint32_t chunk = (uint32_t)((cg & 1) * 4 + c) ^ (uint32_t)(row & 7);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pbase + chunk * 16), "r"(pk[4 * c]),
-                             "r"(pk[4 * c + 1]), "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
-                             : "memory");
+                for (int i = 0; i < 16; ++i) pf[i] = __uint_as_float(pk[i]);
+                tmem_st16(trow + PCOL + a * 64 + cg * 16, pf);  // includes tcgen05.wait::st
+                tc_fence_before();
+            } else {
+                const uint32_t pbase = sP + a * SM::P_BYTES + prow;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t chunk = (uint32_t)((cg & 1) * 4 + c) ^ (uint32_t)(row & 7);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pbase + chunk * 16), "r"(pk[4 * c]),
+                                 "r"(pk[4 * c + 1]), "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
+                                 : "memory");
+                }
+                fence_proxy_async_smem();
             }
-            fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(pfull0 + 8 * a);
         }
         mbar_wait(ofull, 0);
         __syncwarp();
         tc_fence_after();
-        const uint32_t to = trow + 2 * KR + cg * OCOLS;
+        const uint32_t to = trow + OCOL + cg * OCOLS;
         if constexpr (OCOLS == 32) {
             uint32_t o[32];
             tmem_ld32(to, o);
@@ -804,16 +843,16 @@ cudaError_t launch_question_attn_tc(const RetrTcParams& p, int d, cudaStream_t s
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_done[dev][d == 128]) {
-        e = d == 128 ? cudaFuncSetAttribute(retr_out_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            RoSmem<128>::BYTES)
-                     : cudaFuncSetAttribute(retr_out_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            RoSmem<64>::BYTES);
+        e = d == 128 ? cudaFuncSetAttribute(retr_out_kernel<128, kQaPTmem>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, RoSmem<128, kQaPTmem>::BYTES)
+                     : cudaFuncSetAttribute(retr_out_kernel<64, kQaPTmem>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, RoSmem<64, kQaPTmem>::BYTES);
         if (e != cudaSuccess) return e;
         attr_done[dev][d == 128] = true;
     }
     const dim3 g2(p.nkc, nqb, units);
-    if (d == 128) retr_out_kernel<128><<<g2, RT_THREADS, RoSmem<128>::BYTES, s>>>(p2);
-    else retr_out_kernel<64><<<g2, RT_THREADS, RoSmem<64>::BYTES, s>>>(p2);
+    if (d == 128) retr_out_kernel<128, kQaPTmem><<<g2, RT_THREADS, RoSmem<128, kQaPTmem>::BYTES, s>>>(p2);
+    else retr_out_kernel<64, kQaPTmem><<<g2, RT_THREADS, RoSmem<64, kQaPTmem>::BYTES, s>>>(p2);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int64_t n4 = (int64_t)units * p.NQ * (d / 4);
