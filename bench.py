@@ -1126,19 +1126,44 @@ def run_headline(args):
                 svl.retrieve(xq["q"], xq["K"], xq["seq_len"], wq.vb, wq.nv, wq.k, idx_out=idx_q, ws=ws_q)
 
             ms_q = timed(graph_of(rq), 20, 3)
+            # f1's attention output (svl_question_attention: row-LSE pass + output pass), alone and
+            # followed by the retrieval on its LSE (lse_in: the column-mass pass reuses it)
+            out_q = torch.empty(wq.B, n_q, wq.H, wq.d, dtype=torch.float32, device=dev)
+            lse_q = torch.empty(wq.B, n_q, wq.H, dtype=torch.float32, device=dev)
+            ws_a = svl.Workspace(dev)
+
+            def ra(xq=xq, wq=wq, ws_a=ws_a, out_q=out_q, lse_q=lse_q):
+                svl.question_attention(xq["q"], xq["K"], xq["V"], xq["seq_len"], wq.vb, wq.nv, out=out_q,
+                                       lse_out=lse_q, ws=ws_a)
+
+            def rar(xq=xq, wq=wq, ws_q=ws_q, idx_q=idx_q, lse_q=lse_q):
+                ra()
+                svl.retrieve(xq["q"], xq["K"], xq["seq_len"], wq.vb, wq.nv, wq.k, idx_out=idx_q, ws=ws_q,
+                             lse_in=lse_q)
+
+            ms_a = timed(graph_of(ra), 20, 3)
+            ms_ar = timed(graph_of(rar), 20, 3)
             L, units = wq.seq_len, wq.B * wq.Hkv
             keys_p0 = wq.g * (n_q * (L - n_q) + n_q * (n_q + 1) // 2)  # causal prefix per query row
             flops_q = 2 * wq.d * units * (keys_p0 + n_q * wq.g * wq.nv)  # row-LSE pass + column-mass pass
             n_exp = units * (keys_p0 + 256 * ((n_q * wq.g + 255) // 256) * wq.nv)
             tf = flops_q / (ms_q * 1e-3) / 1e12
+            flops_a = 6 * wq.d * units * keys_p0  # row-LSE pass (2d) + S and P.V of the output pass (4d)
+            tf_a = flops_a / (ms_a * 1e-3) / 1e12
             runs.append({"n_q": n_q, "query_rows_per_unit": n_q * wq.g, "us": ms_q * 1e3, "tflops": tf,
                          "frac_bf16_peak": tf / bf16_peak_q if bf16_peak_q else None,
-                         "exp2_per_s": n_exp / (ms_q * 1e-3)})
-            del xq, ws_q
+                         "exp2_per_s": n_exp / (ms_q * 1e-3),
+                         "attention_output_us": ms_a * 1e3, "attention_output_tflops": tf_a,
+                         "attention_output_frac_bf16_peak": tf_a / bf16_peak_q if bf16_peak_q else None,
+                         "attention_then_retrieve_us": ms_ar * 1e3})
+            del xq, ws_q, ws_a, out_q, lse_q
         qret = {"what": "svl_retrieve, n_q question rows (tensor-core path: row-LSE pass + column-mass pass + "
                         "cluster top-k), long-video cache (32768 visual + 768 text rows, 28/4 heads, d 128), "
                         "k = 3277 per KV group, one layer",
-                "flops_accounting": "2 d per (query row, visible key) for each of the two passes",
+                "flops_accounting": "2 d per (query row, visible key) for each of the two passes; "
+                                    "attention_output (svl_question_attention): 6 d per (query row, visible "
+                                    "key) = row-LSE pass + S and P.V; attention_then_retrieve = the output "
+                                    "call followed by svl_retrieve with its LSE as lse_in",
                 "bound": "exp2 (SFU + FP32-pipe polynomial) at d = 128: one exponential per 256 flop",
                 "bf16_peak_tflops": bf16_peak_q, "runs": runs}
 
