@@ -85,7 +85,7 @@ static ScorePlan plan_score(int units, int n_q, int g, int nv, int sms) {
 }
 
 struct RetrieveLayout {
-    size_t logits, part, total;
+    size_t logits, part, scores, total;
 };
 
 static RetrieveLayout retrieve_layout(int B, int Hkv, int nv, const ScorePlan& pl) {
@@ -93,7 +93,8 @@ static RetrieveLayout retrieve_layout(int B, int Hkv, int nv, const ScorePlan& p
     const size_t units = (size_t)B * Hkv;
     l.logits = kWsHeader;
     l.part = round_up(l.logits + units * nv * pl.NCP * sizeof(float), 256);
-    l.total = round_up(l.part + units * pl.C * pl.NCP * sizeof(float2), 256);
+    l.scores = round_up(l.part + units * pl.C * pl.NCP * sizeof(float2), 256);  // relevance [units][nv]
+    l.total = round_up(l.scores + units * nv * sizeof(float), 256);
     return l;
 }
 
@@ -484,6 +485,22 @@ svl_status svl_retrieve(const void* q, int32_t B, int32_t n_q, int32_t H, int32_
     se.scores_out = scores_out;
     se.flags = sp.flags;
     se.CS = select_cluster_size(span.visual_len);
+    // Past one wave of selection clusters (units x CS > 2 CTAs per SM), the relevance runs as
+    // its own streaming pass (full occupancy) and the top-k over 4 B per row in few, larger
+    // clusters (8192-row slices), since each wave of clusters pays the whole exchange chain.
+#ifndef SVL_SELECT_MODE0
+    const int cs3 = relevance_select_cs(span.visual_len);
+    if (!shared && (long)units * se.CS > 2L * device_sm_count() &&
+        (span.visual_len + cs3 - 1) / cs3 <= 8192) {
+        float* rel = scores_out ? scores_out : reinterpret_cast<float*>(w + lay.scores);
+        e = launch_relevance(se, rel, units, s);
+        if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve/relevance");
+        se.mode = 3;
+        se.scores_in = rel;
+        se.scores_out = nullptr;
+        se.CS = cs3;
+    }
+#endif
     e = launch_select(se, shared ? B : units, s);
     if (e != cudaSuccess) return cuda_fail(e, "svl_retrieve/select");
     return SVL_OK;

@@ -729,6 +729,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
 #endif
     } else {
+#if SVL_EXP_FLAG_STAGE2
+        if (stage == 2 && tid == 0 && rank == 0) raise_flag(p.flags, 0x100u);
+#endif
         if (stage == 2) {
             // the generic scratch aliases the V staging: every CTA's text-row gather
             // must land before any peer pushes into it (text rows are re-gathered)

@@ -28,7 +28,8 @@ struct ScoreParams {
 };
 
 struct SelectParams {
-    int mode;  // 0 = retrieve (logits + LSE), 1 = prune (float scores), 2 = retrieve from relevance scores
+    int mode;  // 0 = retrieve (logits + LSE), 1 = prune (float scores), 2 = retrieve from relevance scores,
+               // 3 = as 2, one decode query's relevance (64 threshold candidates, 8192-row slices)
     // retrieve source
     const float* logits;
     const float2* part;
@@ -244,6 +245,9 @@ constexpr int kDecodeRowsMax = 128;  // rows per gather batch
 
 cudaError_t launch_score(const ScoreParams& p, int d, int NT, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s);
+// relevance scores [units][nv] from the retrieve logits (mode-0 arithmetic), for a mode-2 select
+cudaError_t launch_relevance(const SelectParams& p, float* scores, int units, cudaStream_t s);
+int relevance_select_cs(int nv);  // cluster size of the mode-3 select (slices <= 8192 rows)
 cudaError_t launch_prune_select(const SelectParams& p, const PruneTable& tab, int n_units, cudaStream_t s);
 cudaError_t launch_decode(const DecodeParams& p, int d, cudaStream_t s);
 cudaError_t launch_salience(const SalienceParams& p, cudaStream_t s);

@@ -183,7 +183,7 @@ struct FsLayout {
     static_assert(BYTES <= 113 * 1024, "two CTAs per SM");
 };
 
-template <int MODE, int NT, int CANDS>
+template <int MODE, int NT, int CANDS, bool REFINE = false>
 __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams p) {
     using FsLayout = svl::FsLayout<CANDS>;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
         mbar_init(smem_u32(&bars[0]), 1);  // histograms: CS x 1 KB
         mbar_arrive_expect_tx(smem_u32(&bars[0]), (uint32_t)(CS * 1024));
         mbar_init(smem_u32(&bars[1]), 1);  // candidates (armed in threshold())
+        mbar_init(smem_u32(&bars[2]), 1);  // refinement histograms (armed in threshold(), if needed)
         fence_mbar_init();
     }
     cluster_arrive_relaxed();
@@ -244,17 +245,29 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
             if (lane == 0) lse2s[cc] = lse2;
         }
     }
-    FastSelect<NTH, CANDS> sel(cl, *reinterpret_cast<typename FsLayout::FsSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0,
+    FastSelect<NTH, CANDS, REFINE> sel(cl, *reinterpret_cast<typename FsLayout::FsSelSmem*>(smem + FsLayout::FS_OFF), nloc, j0,
                                slice, n, k,
                         reinterpret_cast<uint32_t*>(smem + FsLayout::KEYS_OFF), smem + FsLayout::STATE_OFF, p.flags,
                         reinterpret_cast<uint32_t*>(smem + FsLayout::WHIST_OFF));
     sel.hbar = &bars[0];
     sel.cbar = &bars[1];
+    sel.h2bar = &bars[2];
     int stage = 0;
     if (!sel.trivial()) {
         sel.zero_hist();
         cta_sync();
-        for (int i = tid; i < nloc; i += NTH) {
+        if (MODE == 2 && nG == 1) {
+            // precomputed relevance: all of the thread's loads in flight before the first key
+            constexpr int R = FsLayout::kFsSliceMax / NTH;
+            const float* src = p.scores_in + ((int64_t)(b * p.Hkv + G0)) * p.nv + j0;
+            float v[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) v[q] = (tid + q * NTH < nloc) ? src[tid + q * NTH] : 0.f;
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (tid + q * NTH < nloc) sel.add_key(tid + q * NTH, v[q]);
+        }
+        for (int i = (MODE == 2 && nG == 1) ? nloc : tid; i < nloc; i += NTH) {
             const int j = j0 + i;
             float sc = 0.f;
             if (MODE == 0) {
@@ -295,6 +308,75 @@ __global__ void __launch_bounds__(NTH, 2) select_fast_kernel(const SelectParams 
                                reinterpret_cast<int*>(smem + FsLayout::KEYS_OFF));
     }
     cluster_sync(cl);  // no CTA leaves while a peer may still address its shared memory
+}
+
+// Relevance of every visual row, score[u][j] = sum_c exp2(s2[j,c] - LSE2[c]) (the
+// select kernels' mode-0 arithmetic, same fold and summation order, so the scores
+// are bitwise those mode 0 computes), as a plain streaming pass: every thread
+// keeps RR rows' logits in flight, full occupancy; the cluster top-k then reads
+// 4 B per row (mode 2) instead of the 8 NT logits.
+constexpr int kRelThreads = 256;
+constexpr int kRelRows = 4;       // rows per thread per pass (all loads issued first)
+constexpr int kRelPasses = 4;     // passes per CTA
+template <int NT>
+__global__ void __launch_bounds__(kRelThreads) relevance_kernel(const SelectParams p, float* scores) {
+    __shared__ float lse2s[NT * 8];
+    const int u = blockIdx.y, b = u / p.Hkv, G = u % p.Hkv;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int col = warp; col < p.NC; col += kRelThreads / 32) {
+        float lse2;
+        if (p.lse_in) {
+            const int r = col / p.g, h = G * p.g + col % p.g;
+            lse2 = p.lse_in[((int64_t)b * p.n_q + r) * p.H + h] * kLog2e;
+        } else {
+            float m = -INFINITY, l = 0.f;
+            for (int i = lane; i < p.C; i += 32) {
+                const float2 pr = p.part[((int64_t)u * p.C + i) * p.NCP + col];
+                const float M = fmaxf(m, pr.x);
+                if (M != -INFINITY) {
+                    l = l * exp2f(m - M) + pr.y * exp2f(pr.x - M);
+                    m = M;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+                const float l2 = __shfl_xor_sync(0xffffffffu, l, off);
+                const float M = fmaxf(m, m2);
+                if (M != -INFINITY) {
+                    l = l * exp2f(m - M) + l2 * exp2f(m2 - M);
+                    m = M;
+                }
+            }
+            lse2 = m + log2f(l);
+        }
+        if (lane == 0) lse2s[col] = lse2;
+    }
+    __syncthreads();
+    const float4* lg = reinterpret_cast<const float4*>(p.logits + (int64_t)u * p.nv * (NT * 8));
+    float* out = scores + (int64_t)u * p.nv;
+    constexpr int SPAN = kRelThreads * kRelRows;
+    for (int j0 = blockIdx.x * SPAN; j0 < p.nv; j0 += gridDim.x * SPAN) {
+        float4 v[kRelRows][2 * NT];
+#pragma unroll
+        for (int q = 0; q < kRelRows; ++q) {
+            const int j = j0 + q * kRelThreads + tid;
+#pragma unroll
+            for (int i = 0; i < 2 * NT; ++i)
+                v[q][i] = (j < p.nv) ? lg[(int64_t)j * (2 * NT) + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < kRelRows; ++q) {
+            const int j = j0 + q * kRelThreads + tid;
+            if (j >= p.nv) continue;
+            const float* lv = reinterpret_cast<const float*>(v[q]);
+            float sc = 0.f;
+#pragma unroll
+            for (int col = 0; col < NT * 8; ++col)
+                if (col < p.NC) sc += exp2f(lv[col] - lse2s[col]);
+            out[j] = sc;
+        }
+    }
 }
 
 template <int NT>
@@ -452,6 +534,12 @@ cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
 #else
     const bool fast = false;  // A/B builds only
 #endif
+    if (p.mode == 3) {  // relevance scores of one decode query (svl_retrieve's split path): 64 candidates
+        if (slice > FsLayout<64>::kFsSliceMax) return cudaErrorInvalidValue;
+        SelectParams q = p;
+        q.mode = 2;
+        return launch_fast<64>(select_fast_kernel<2, 1, 64, true>, q, n_units, s, *attr_flag(11));
+    }
     if (fast && p.mode == 2 && slice <= FsLayout<256>::kFsSliceMax)
         return launch_fast<256>(select_fast_kernel<2, 1, 256>, p, n_units, s, *attr_flag(6));
     if (fast && p.mode == 0 && slice <= FsLayout<64>::kFsSliceMax) {
@@ -471,6 +559,29 @@ cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
         case 4: return launch_cluster(select_retrieve_kernel<4>, p.CS, n_units, s, *attr_flag(4), p);
     }
     return cudaErrorInvalidValue;
+}
+
+// cluster size of the split path's select: slices of up to kFsSliceMax (8192) rows, so few
+// small clusters -- the selection is a chain of cluster exchanges, paid once per wave
+int relevance_select_cs(int nv) {
+    int cs = (nv + FsLayout<64>::kFsSliceMax - 1) / FsLayout<64>::kFsSliceMax;
+    if (cs < 2) cs = 2;
+    int c = 1;
+    while (c < cs) c <<= 1;
+    return c;
+}
+
+cudaError_t launch_relevance(const SelectParams& p, float* scores, int units, cudaStream_t s) {
+    constexpr int per = kRelThreads * kRelRows * kRelPasses;
+    const dim3 grid((unsigned)((p.nv + per - 1) / per), (unsigned)units);
+    switch (p.NCP / 8) {
+        case 1: relevance_kernel<1><<<grid, kRelThreads, 0, s>>>(p, scores); break;
+        case 2: relevance_kernel<2><<<grid, kRelThreads, 0, s>>>(p, scores); break;
+        case 3: relevance_kernel<3><<<grid, kRelThreads, 0, s>>>(p, scores); break;
+        case 4: relevance_kernel<4><<<grid, kRelThreads, 0, s>>>(p, scores); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_prune_select(const SelectParams& p, const PruneTable& tab, int n_units,

@@ -16,8 +16,11 @@
 //     local 8-bit radix pass (bits 19..12) and an exact ranking within the
 //     final sub-bin (key desc, index asc), derives every CTA's output offset
 //     from the gathered counts, and writes its kept indices.
-// If b* is the catch-all bin 0 or a CTA holds more than 64 keys of b*, the
-// generic exact radix of select_push.cuh takes over (generic_or_trivial).
+// If a CTA holds more than CANDS keys of b* (smooth score distributions over
+// long slices) and the caller gave h2bar, one more all-gathered histogram of
+// key bits 19..12 inside b* narrows the cut bin first (the resolve then uses
+// bits 11..4).  If b* is the catch-all bin 0, or the refined bin still
+// overflows, the generic exact radix of select_push.cuh takes over.
 // Per-row state after the selection: 2 (kKeySel) = kept, 0 = not kept.
 #pragma once
 
@@ -88,8 +91,11 @@ __device__ __noinline__ void warp_find_nb(const uint32_t* bins, uint32_t need, u
     }
 }
 
-// CANDS: candidates of the threshold bin a CTA may hold (more -> the generic radix)
-template <int NTH, int CANDS = kFastCandPerCta>
+// CANDS: candidates of the threshold bin a CTA may hold (more -> the refinement round if
+// REFINE, else / then the generic radix).  REFINE is a template switch: the refinement's
+// code in threshold() measurably slows the instantiations that never need it (the fused
+// kernel: 28.6 -> 29.25 us/layer at long-video).
+template <int NTH, int CANDS = kFastCandPerCta, bool REFINE = false>
 struct FastSelect {
     cg::cluster_group& cl;
     FastSelSmemT<CANDS>& s;
@@ -99,6 +105,8 @@ struct FastSelect {
     uint32_t* flags;
     uint32_t* whist;  // [NTH/32][256] private histograms (scratch, dead after the push)
     int bstar = 0;
+    int sub = -1;   // >= 0: the cut was refined inside b* to sub-bin `sub` of key bits 19..12
+    int rsh = 12;   // resolve radix: key bits rsh + 7 .. rsh (4 after the refinement)
     uint32_t krem = 0;
     uint32_t pre_gt = 0, pre_eq = 0;  // rows above b* / in b* before this thread's rows (CTA-local)
     bool nan_seen = false;
@@ -107,6 +115,8 @@ struct FastSelect {
     // histograms at init; cbar armed here once the candidate counts are known
     uint64_t* hbar = nullptr;
     uint64_t* cbar = nullptr;
+    // optional (count 1, unarmed): the refinement round's histograms, CS x 1 KB into whist
+    uint64_t* h2bar = nullptr;
 
     SVL_DEV FastSelect(cg::cluster_group& cl_, FastSelSmemT<CANDS>& s_, int nvis_, int v0_, int slice_, int nv_, int k_,
                        uint32_t* keys_, uint8_t* state_, uint32_t* flags_, uint32_t* whist_)
@@ -121,6 +131,15 @@ struct FastSelect {
     }
 
     SVL_DEV bool trivial() const { return k <= 0 || k >= nv; }
+
+    // 2: above the cut bin (kept), 1: in it (a candidate), 0: below
+    SVL_DEV int cls(uint32_t key) const {
+        const int d = rel_digit(key);
+        if (d != bstar) return d > bstar ? 2 : 0;
+        if (!REFINE || sub < 0) return 1;
+        const int sd = (int)((key >> 12) & 255u);
+        return sd > sub ? 2 : (sd == sub ? 1 : 0);
+    }
 
     // 1. (caller) zero_hist(); barrier; add_key(i, score) for every local row; then threshold()
     SVL_DEV void zero_hist() {
@@ -198,7 +217,61 @@ struct FastSelect {
             maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
             totc += (q < CS) ? s.cnt_q[q] : 0u;
         }
-        const int st = (bstar == 0 || maxc > (uint32_t)CANDS) ? 2 : 1;
+        int st = (bstar == 0 || maxc > (uint32_t)CANDS) ? 2 : 1;
+        if (REFINE && st == 2 && bstar != 0 && bstar != 255 && h2bar != nullptr) {
+            // Too many keys share b* (a smooth score distribution around the cut, e.g. 64k rows
+            // per unit): one more all-gathered histogram, of key bits 19..12 inside b* (its
+            // keys share bits 30..20), instead of the generic radix.
+            if (tid == 0) mbar_arrive_expect_tx(smem_u32(h2bar), (uint32_t)(CS * 1024));
+            for (int b = tid; b < 256; b += NTH) s.hist[b] = 0u;  // (round 1's values left by value)
+            cta_sync();
+            for (int i = tid; i < nvis; i += NTH) {
+                const uint32_t key = keys[i];
+                if (rel_digit(key) == bstar) atomicAdd(&s.hist[(key >> 12) & 255u], 1u);
+            }
+            cta_sync();
+            uint32_t(*allh2)[256] = reinterpret_cast<uint32_t(*)[256]>(whist);  // dead since round 1's fold
+            for (int i = tid; i < CS * 64; i += NTH) {
+                const int q = i >> 6, c = i & 63;
+                st_async_u4(mapa_shared(smem_u32(&allh2[rank][4 * c]), q), reinterpret_cast<const uint4*>(s.hist)[c],
+                            mapa_shared(smem_u32(h2bar), q));
+            }
+            mbar_wait(smem_u32(h2bar), 0);
+            __syncwarp();
+            for (int b = tid; b < 256; b += NTH) {
+                uint32_t acc = 0u;
+                for (int q = 0; q < CS; ++q) acc += allh2[q][b];
+                s.tot[b] = acc;
+            }
+            cta_sync();
+            if (warp == 0) warp_find_nb<256>(s.tot, krem, s.bcast + 8);
+            cta_sync();
+            sub = (int)s.bcast[8];
+            krem -= s.bcast[9];
+            rsh = 4;
+            for (int q = warp; q < CS; q += NTH / 32) {
+                uint32_t a = 0u;
+                for (int b = sub + 1 + lane; b < 256; b += 32) a += allh2[q][b];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+                if (lane == 0) {
+                    s.above_q[q] += a;
+                    s.cnt_q[q] = allh2[q][sub];
+                }
+            }
+            cta_sync();
+            maxc = 0u;
+            totc = 0u;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                maxc = max(maxc, (q < CS) ? s.cnt_q[q] : 0u);
+                totc += (q < CS) ? s.cnt_q[q] : 0u;
+            }
+            st = (maxc > (uint32_t)CANDS) ? 2 : 1;
+#if SVL_EXP_FLAG_STAGE2
+            if (tid == 0 && rank == 0) raise_flag(flags, 0x200u);  // A/B builds: the refinement ran
+#endif
+        }
         if (st == 1 && tid == 0) mbar_arrive_expect_tx(smem_u32(cbar), totc * 8u);  // the candidates to come
         return st;
     }
@@ -211,9 +284,9 @@ struct FastSelect {
         my_rows(i0, i1);
         uint32_t ge = 0u, eq = 0u;
         for (int i = i0; i < i1; ++i) {
-            const int d = rel_digit(keys[i]);
-            ge += d >= bstar;
-            eq += d == bstar;
+            const int c = cls(keys[i]);
+            ge += c >= 1;
+            eq += c == 1;
         }
         uint32_t tot;
         const uint32_t pre = block_scan_excl<NTH>(ge | (eq << 16), s.warp_sums, &tot);
@@ -222,10 +295,10 @@ struct FastSelect {
         pre_eq = peq;
         for (int i = i0; i < i1; ++i) {
             const uint32_t key = keys[i];
-            const int d = rel_digit(key);
+            const int cl_ = cls(key);
             uint8_t st = 0;
-            if (d >= bstar && att_sel) att_sel[pge++] = i;  // (null: the caller needs no V slots)
-            if (d == bstar) {
+            if (cl_ >= 1 && att_sel) att_sel[pge++] = i;  // (null: the caller needs no V slots)
+            if (cl_ == 1) {
                 st = (uint8_t)(CANDS > 254 ? min(peq + 1u, 255u) : peq + 1u);  // candidate marker
                 const uint2 c = make_uint2(key, (uint32_t)(v0 + i));
                 const uint32_t dst = smem_u32(&s.cand[rank][peq]), bar = smem_u32(cbar);
@@ -242,6 +315,7 @@ struct FastSelect {
 
     SVL_DEV void resolve_and_emit(int32_t* idx_out) {
         const int tid = threadIdx.x, warp = tid >> 5;
+        const int rsh = REFINE ? this->rsh : 12;
         const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
         // one radix pass on key bits 19..12 over all candidates
         for (int i = tid; i < 256; i += NTH) s.hist[i] = 0u;
@@ -249,7 +323,7 @@ struct FastSelect {
         cta_sync();
         for (int sl = tid; sl < 16 * CANDS; sl += NTH) {
             const int q = sl / CANDS, j = sl % CANDS;
-            if (q < CS && (uint32_t)j < s.cnt_q[q]) atomicAdd(&s.hist[(s.cand[q][j].x >> 12) & 255u], 1u);
+            if (q < CS && (uint32_t)j < s.cnt_q[q]) atomicAdd(&s.hist[(s.cand[q][j].x >> rsh) & 255u], 1u);
         }
         cta_sync();
         stamp(tr, 0);
@@ -268,7 +342,7 @@ struct FastSelect {
                 const int q = sl / CANDS, j = sl % CANDS;
                 if (q < CS && (uint32_t)j < s.cnt_q[q]) {
                     const uint2 c = s.cand[q][j];
-                    if (((c.x >> 12) & 255u) == bA) s.sub[atomicAdd(&s.bcast[6], 1u)] = c;
+                    if (((c.x >> rsh) & 255u) == bA) s.sub[atomicAdd(&s.bcast[6], 1u)] = c;
                 }
             }
             cta_sync();
@@ -278,7 +352,7 @@ struct FastSelect {
             bool take = false;
             if (q < CS && (uint32_t)j < s.cnt_q[q]) {
                 const uint2 c = s.cand[q][j];
-                const uint32_t dA = (c.x >> 12) & 255u;
+                const uint32_t dA = (c.x >> rsh) & 255u;
                 take = dA > bA;
                 if (dA == bA) {  // exact rank inside the sub-bin: (key desc, index asc)
                     uint32_t r = 0u;
@@ -291,7 +365,7 @@ struct FastSelect {
                         for (int q2 = 0; q2 < CS; ++q2)
                             for (uint32_t j2 = 0; j2 < s.cnt_q[q2]; ++j2) {
                                 const uint2 d = s.cand[q2][j2];
-                                r += (((d.x >> 12) & 255u) == bA) && (d.x > c.x || (d.x == c.x && d.y < c.y));
+                                r += (((d.x >> rsh) & 255u) == bA) && (d.x > c.x || (d.x == c.x && d.y < c.y));
                             }
                     }
                     take = r < need;
@@ -335,12 +409,12 @@ struct FastSelect {
         };
         uint32_t gtc = pre_gt, eqc = pre_eq;
         for (int i = i0; i < i1; ++i) {
-            const int d = rel_digit(keys[i]);
-            bool kept = d > bstar;
-            if (d == bstar) kept = s.cflag[rank][eqc] != 0;
+            const int c = cls(keys[i]);
+            bool kept = c == 2;
+            if (c == 1) kept = s.cflag[rank][eqc] != 0;
             if (kept) idx_out[off + gtc + kept_cands_before(eqc)] = v0 + i;
-            gtc += d > bstar;
-            eqc += d == bstar;
+            gtc += c == 2;
+            eqc += c == 1;
             state[i] = kept ? kKeySel : kKeyOut;
         }
         stamp(tr, 3);

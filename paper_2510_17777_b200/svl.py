@@ -215,12 +215,16 @@ class Workspace:
         return self.buf
 
     def flags(self, stream=None) -> int:
+        if self.buf is None:  # never used: nothing raised
+            return 0
         out = ctypes.c_uint32(0)
         _check(lib().svl_read_device_flags(ctypes.c_void_p(self.buf.data_ptr()),
                                            ctypes.c_void_p(_stream(stream)), ctypes.byref(out)))
         return out.value
 
     def reset_flags(self, stream=None):
+        if self.buf is None:
+            return
         _check(lib().svl_reset_device_flags(ctypes.c_void_p(self.buf.data_ptr()),
                                             ctypes.c_void_p(_stream(stream))))
 

@@ -1,0 +1,6 @@
+#!/bin/bash
+for v in head new head new; do
+  if [ $v = new ]; then L=paper_2510_17777_b200/libsparsevila.so; else L=build/$v/libsparsevila.so; fi
+  SVL_LIB=$L timeout 300 python tools/exp/twocall_bench.py $v 2>&1 | tail -3
+  SVL_LIB=$L timeout 300 python tools/exp/fresh_bench.py $v 2>&1 | tail -2
+done
