@@ -108,7 +108,7 @@ struct FastSelect {
     int sub = -1;   // >= 0: the cut was refined inside b* to sub-bin `sub` of key bits 19..12
     int rsh = 12;   // resolve radix: key bits rsh + 7 .. rsh (4 after the refinement)
     uint32_t krem = 0;
-    uint32_t pre_gt = 0, pre_eq = 0;  // rows above b* / in b* before this thread's rows (CTA-local)
+    uint32_t pre_gt = 0, pre_eq = 0;  // rows above the cut / candidates before this warp's rows (CTA-local)
     bool nan_seen = false;
     uint64_t* tr = nullptr;  // debug stamps (SVL_TRACE)
     // st.async exchange barriers (caller-initialised, count 1): hbar armed for CS x 1 KB of
@@ -123,7 +123,15 @@ struct FastSelect {
         : cl(cl_), s(s_), nvis(nvis_), v0(v0_), slice(slice_), nv(nv_), k(k_), keys(keys_), state(state_),
           flags(flags_), whist(whist_) {}
 
-    // contiguous ownership for slots / emit: thread tid handles rows [i0, i1)
+    // ownership for slots / emit: warp w takes the contiguous rows [32 E w, 32 E (w + 1)),
+    // row base + 32 j + lane in step j (conflict-free key reads; positions in index order
+    // from ballots and the warp's prefix)
+    SVL_DEV void warp_rows(int& base, int& E) const {
+        E = (nvis + NTH - 1) / NTH;
+        base = (int)(threadIdx.x >> 5) * 32 * E;
+    }
+    // (REFINE = false, the fused kernel's short slices) contiguous ownership: thread tid
+    // handles rows [i0, i1) -- measured faster there than the warp-interleaved loops
     SVL_DEV void my_rows(int& i0, int& i1) const {
         const int E = (nvis + NTH - 1) / NTH;
         i0 = min(nvis, (int)threadIdx.x * E);
@@ -279,6 +287,12 @@ struct FastSelect {
     // V slots for every row with digit >= b* (att_sel[slot] = local row, in
     // index order); keys of b* pushed to the peers; returns the slot count.
     SVL_DEV int assign_slots_and_push_candidates(int* att_sel) {
+        if constexpr (REFINE) return assign_warp_rows(att_sel);
+        else return assign_contiguous(att_sel);
+    }
+
+    // (!REFINE) contiguous rows per thread, one block scan
+    SVL_DEV int assign_contiguous(int* att_sel) {
         const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
         int i0, i1;
         my_rows(i0, i1);
@@ -307,6 +321,56 @@ struct FastSelect {
                 ++peq;
             }
             state[i] = st;
+        }
+        mbar_wait(smem_u32(cbar), 0);  // every peer's candidates landed
+        __syncwarp();
+        return (int)(tot & 0xffffu);
+    }
+
+    // (REFINE: slices of up to 8192 rows) warp-interleaved rows, ballot prefixes
+    SVL_DEV int assign_warp_rows(int* att_sel) {
+        const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const unsigned lt = (1u << lane) - 1u;
+        int base, E;
+        warp_rows(base, E);
+        uint32_t ge = 0u, eq = 0u;
+        for (int j = 0; j < E; ++j) {
+            const int i = base + 32 * j + lane;
+            const int c = (i < nvis) ? cls(keys[i]) : 0;
+            ge += (uint32_t)__popc(__ballot_sync(0xffffffffu, c >= 1));
+            eq += (uint32_t)__popc(__ballot_sync(0xffffffffu, c == 1));
+        }
+        if (lane == 0) s.warp_sums[warp] = ge | (eq << 16);
+        cta_sync();
+        uint32_t pre = 0u, tot = 0u;
+#pragma unroll
+        for (int w = 0; w < NTH / 32; ++w) {
+            const uint32_t x = s.warp_sums[w];
+            pre += (w < warp) ? x : 0u;
+            tot += x;
+        }
+        uint32_t pge = pre & 0xffffu, peq = pre >> 16;
+        pre_gt = pge - peq;
+        pre_eq = peq;
+        for (int j = 0; j < E; ++j) {
+            const int i = base + 32 * j + lane;
+            const uint32_t key = (i < nvis) ? keys[i] : 0u;
+            const int cl_ = (i < nvis) ? cls(key) : 0;
+            const unsigned bg = __ballot_sync(0xffffffffu, cl_ >= 1), be = __ballot_sync(0xffffffffu, cl_ == 1);
+            const uint32_t mg = pge + (uint32_t)__popc(bg & lt), me = peq + (uint32_t)__popc(be & lt);
+            uint8_t st = 0;
+            if (cl_ >= 1 && att_sel) att_sel[mg] = i;  // (null: the caller needs no V slots)
+            if (cl_ == 1) {
+                st = (uint8_t)(CANDS > 254 ? min(me + 1u, 255u) : me + 1u);  // candidate marker
+                const uint2 c = make_uint2(key, (uint32_t)(v0 + i));
+                const uint32_t dst = smem_u32(&s.cand[rank][me]), bar = smem_u32(cbar);
+                if (me < (uint32_t)CANDS)  // always true on this path (threshold() checked); defensive
+                    for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), c, mapa_shared(bar, q));
+            }
+            if (i < nvis) state[i] = st;
+            pge += (uint32_t)__popc(bg);
+            peq += (uint32_t)__popc(be);
         }
         mbar_wait(smem_u32(cbar), 0);  // every peer's candidates landed
         __syncwarp();
@@ -388,11 +452,9 @@ struct FastSelect {
         stamp(tr, 2);
         uint32_t off = 0u;
         for (int q = 0; q < rank; ++q) off += s.above_q[q] + s.sel_q[q];
-        int i0, i1;
-        my_rows(i0, i1);
         stamp(tr, 5);
-        // output slot of a kept row = off + (rows above b* before it) + (kept b* candidates
-        // before it); both prefixes come from the slot-assignment scan and the candidate
+        // output slot of a kept row = off + (rows above the cut before it) + (kept candidates
+        // before it); both prefixes come from the slot-assignment prefixes and the candidate
         // ballot masks, so no second block scan
         const uint32_t* msk = s.sel2[rank];
         const uint32_t m0 = msk[0], m1 = msk[1];
@@ -407,15 +469,37 @@ struct FastSelect {
                 return c;
             }
         };
-        uint32_t gtc = pre_gt, eqc = pre_eq;
-        for (int i = i0; i < i1; ++i) {
-            const int c = cls(keys[i]);
-            bool kept = c == 2;
-            if (c == 1) kept = s.cflag[rank][eqc] != 0;
-            if (kept) idx_out[off + gtc + kept_cands_before(eqc)] = v0 + i;
-            gtc += c == 2;
-            eqc += c == 1;
-            state[i] = kept ? kKeySel : kKeyOut;
+        if constexpr (!REFINE) {
+            int i0, i1;
+            my_rows(i0, i1);
+            uint32_t gtc = pre_gt, eqc = pre_eq;
+            for (int i = i0; i < i1; ++i) {
+                const int c = cls(keys[i]);
+                bool kept = c == 2;
+                if (c == 1) kept = s.cflag[rank][eqc] != 0;
+                if (kept) idx_out[off + gtc + kept_cands_before(eqc)] = v0 + i;
+                gtc += c == 2;
+                eqc += c == 1;
+                state[i] = kept ? kKeySel : kKeyOut;
+            }
+        } else {
+            const int lane = tid & 31;
+            const unsigned lt = (1u << lane) - 1u;
+            int base, E;
+            warp_rows(base, E);
+            uint32_t gtc = pre_gt, eqc = pre_eq;
+            for (int j = 0; j < E; ++j) {
+                const int i = base + 32 * j + lane;
+                const int c = (i < nvis) ? cls(keys[i]) : 0;
+                const unsigned ba = __ballot_sync(0xffffffffu, c == 2), be = __ballot_sync(0xffffffffu, c == 1);
+                const uint32_t ma = gtc + (uint32_t)__popc(ba & lt), me = eqc + (uint32_t)__popc(be & lt);
+                bool kept = c == 2;
+                if (c == 1) kept = s.cflag[rank][me] != 0;
+                if (kept) idx_out[off + ma + kept_cands_before(me)] = v0 + i;
+                if (i < nvis) state[i] = kept ? kKeySel : kKeyOut;
+                gtc += (uint32_t)__popc(ba);
+                eqc += (uint32_t)__popc(be);
+            }
         }
         stamp(tr, 3);
         stamp(tr, 4);
