@@ -563,25 +563,49 @@ cudaError_t launch_select(const SelectParams& p, int n_units, cudaStream_t s) {
 
 // cluster size of the split path's select: slices of up to kFsSliceMax (8192) rows, so few
 // small clusters -- the selection is a chain of cluster exchanges, paid once per wave
+#ifndef SVL_REL_SLICE
+#define SVL_REL_SLICE 8192  // rows per CTA of the mode-3 select (<= FsLayout<64>::kFsSliceMax)
+#endif
 int relevance_select_cs(int nv) {
-    int cs = (nv + FsLayout<64>::kFsSliceMax - 1) / FsLayout<64>::kFsSliceMax;
+    int cs = (nv + SVL_REL_SLICE - 1) / SVL_REL_SLICE;
     if (cs < 2) cs = 2;
     int c = 1;
     while (c < cs) c <<= 1;
     return c;
 }
 
-cudaError_t launch_relevance(const SelectParams& p, float* scores, int units, cudaStream_t s) {
-    constexpr int per = kRelThreads * kRelRows * kRelPasses;
-    const dim3 grid((unsigned)((p.nv + per - 1) / per), (unsigned)units);
-    switch (p.NCP / 8) {
-        case 1: relevance_kernel<1><<<grid, kRelThreads, 0, s>>>(p, scores); break;
-        case 2: relevance_kernel<2><<<grid, kRelThreads, 0, s>>>(p, scores); break;
-        case 3: relevance_kernel<3><<<grid, kRelThreads, 0, s>>>(p, scores); break;
-        case 4: relevance_kernel<4><<<grid, kRelThreads, 0, s>>>(p, scores); break;
-        default: return cudaErrorInvalidValue;
+template <int NT>
+static cudaError_t launch_relevance_t(const SelectParams& p, float* scores, int units, cudaStream_t s) {
+    // one wave: CTAs per unit = resident CTAs / units (each grid-strides over its unit's rows)
+    static int occ[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && occ[dev] == 0) {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, relevance_kernel<NT>, kRelThreads, 0) != cudaSuccess)
+            o = 1;
+        occ[dev] = std::max(1, o);
     }
+    const int slots = device_sm_count() * (dev < 64 ? occ[dev] : 1);
+    constexpr int per = kRelThreads * kRelRows;
+    int x = (p.nv + per - 1) / per;
+#if !defined(SVL_REL_ONEWAVE) || SVL_REL_ONEWAVE
+    x = std::max(1, std::min(x, slots / std::max(1, units)));
+#else
+    x = (p.nv + per * kRelPasses - 1) / (per * kRelPasses);
+#endif
+    relevance_kernel<NT><<<dim3((unsigned)x, (unsigned)units), kRelThreads, 0, s>>>(p, scores);
     return cudaGetLastError();
+}
+
+cudaError_t launch_relevance(const SelectParams& p, float* scores, int units, cudaStream_t s) {
+    switch (p.NCP / 8) {
+        case 1: return launch_relevance_t<1>(p, scores, units, s);
+        case 2: return launch_relevance_t<2>(p, scores, units, s);
+        case 3: return launch_relevance_t<3>(p, scores, units, s);
+        case 4: return launch_relevance_t<4>(p, scores, units, s);
+    }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_prune_select(const SelectParams& p, const PruneTable& tab, int n_units,
