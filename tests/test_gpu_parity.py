@@ -360,3 +360,45 @@ def test_topk_fallback_massive_ties(svl, orc):
     idx, sc, oi, osc, gap = _retrieve_both(svl, orc, wl, cpu, dev)
     assert np.array_equal(idx, oi)
     assert idx[0, 0].tolist() == list(range(3000))
+
+
+# ------------------------------------------- many units: relevance pass + refined select
+# B * Hkv * CS > 2 CTAs per SM: svl_retrieve runs the relevance pass and the 8192-row-slice
+# select (mode 3), whose threshold bin overflows 64 candidates per CTA on these smooth score
+# distributions and is narrowed by the refinement round (tools/exp/sanitize_new.py checks the
+# path with the A/B flag build).
+MANY = gen.DecodeWorkload("many", 10, 28, 4, 128, 32, 16384, 300, 1638, 1, 256)
+
+
+def test_retrieve_many_units_refined(svl, orc):
+    cpu, dev = _gen(MANY, seed=31, big=True)
+    idx, sc, oi, osc, gap = _retrieve_both(svl, orc, MANY, cpu, dev)
+    _check_scores(sc, osc)
+    parity.check_indices(idx, osc, gap, MANY.k)
+
+
+def test_retrieve_many_units_gapped_exact(svl, orc):
+    for gamma in (4.0, 8.0, 16.0):
+        wl = gen.DecodeWorkload(**{**MANY.__dict__, "gap_gamma": gamma, "sinks": 0, "needles": 0})
+        cpu, dev = _gen(wl, seed=32, big=True)
+        idx, sc, oi, osc, gap = _retrieve_both(svl, orc, wl, cpu, dev)
+        if gap.min() > 1e-3:
+            break
+    assert gap.min() > 1e-3, gap.min()
+    assert np.array_equal(idx, oi)
+
+
+def test_retrieve_many_units_duplicates_and_ties(svl, orc):
+    cpu, dev = _gen(MANY, seed=33, big=True)
+    _, _, oi, osc, _ = _retrieve_both(svl, orc, MANY, cpu, dev)
+    for b in (0, 7):
+        for G in (0, 3):
+            order = np.lexsort((np.arange(MANY.nv), -osc[b, G]))
+            kth = int(order[MANY.k - 1])
+            for dup in order[MANY.k:MANY.k + 40].tolist()[:6]:  # copies of the k-th key past the cut
+                cpu["K"][b, G, MANY.vb + dup] = cpu["K"][b, G, MANY.vb + kth]
+    cpu["K"][9, 2, MANY.vb:MANY.vb + MANY.nv] = cpu["K"][9, 2, MANY.vb]  # a unit of identical keys
+    dev["K"] = cpu["K"].cuda()
+    idx, sc, oi, osc, gap = _retrieve_both(svl, orc, MANY, cpu, dev)
+    assert np.array_equal(idx, oi)                      # exact at gap 0: ties to the lower index
+    assert idx[9, 2].tolist() == list(range(MANY.k))
