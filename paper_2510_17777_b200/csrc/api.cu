@@ -201,8 +201,9 @@ bool encode_kv_tensor_map(CUtensorMap* map, const void* data, int d, int capacit
 extern "C" {
 
 const char* svl_version(void) {
-    return "libsparsevila 0.2 sm_100a (fused fresh step: TMA + tcgen05 K stream, cluster top-k over DSMEM; "
-           "steady decode: all-SM split-K gather with a grid-barrier merge)";
+    return "libsparsevila 0.3 sm_100a (fused fresh step: TMA + tcgen05 K stream, cluster top-k over DSMEM; "
+           "steady decode: split-K gather, cluster DSMEM merge (<= 16 splits) or epoch-tagged L2 merge; "
+           "question chunk: tcgen05 row LSE, column mass and attention output (P from TMEM))";
 }
 
 const char* svl_status_string(svl_status s) {
