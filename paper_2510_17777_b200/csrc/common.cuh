@@ -129,6 +129,21 @@ SVL_DEV void cta_sync() {
     __syncwarp();
     __syncthreads();
 }
+// Named barriers for warp groups (id 1..15; n = participating threads, a multiple of 32).
+// bar.arrive does not wait: the producer side of a one-way hand-off.
+SVL_DEV void named_bar_sync(int id, int n) {
+    __syncwarp();
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+SVL_DEV void named_bar_arrive(int id, int n) {
+    __syncwarp();
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// One arrival on `bar` once every cp.async this thread issued so far has landed (the
+// barrier's expected count includes it: .noinc).
+SVL_DEV void cp_async_mbar_arrive_noinc(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
 template <typename CL>
 SVL_DEV void cluster_sync(CL& cl) {
     __syncwarp();
@@ -245,6 +260,21 @@ SVL_DEV void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
 }
 // 32 lanes x 16 columns, NO wait (pair with tmem_wait_ld_tie16)
 SVL_DEV void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+}
+// 32 lanes x 8 columns, NO wait, into v[0..7] (v: a register array indexed by constants)
+SVL_DEV void tmem_ld8_nowait(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+SVL_DEV void tmem_ld16_nowait_p(uint32_t taddr, uint32_t* v) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),

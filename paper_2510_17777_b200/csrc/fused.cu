@@ -41,15 +41,19 @@
 #include "kernels.h"
 #include "select_fast.cuh"
 
+#ifndef SVL_TRACE_BUILD
+#define SVL_TRACE_BUILD 0
+#endif
+#ifndef SVL_EXP_HOTONLY
+#define SVL_EXP_HOTONLY 0  // timing experiment: the stage-0/2 and overflow paths compiled out
+#endif
+
 namespace svl {
 
 namespace {
 
 constexpr int FT = kFusedThreads;  // 512
 constexpr int STAGE_ROWS = 128;    // = UMMA M: one K stage is one tcgen05.mma row block
-#ifndef SVL_PTMEM
-#define SVL_PTMEM 1  // measured: 28.15 -> 28.09 us/layer (long-video), bitwise-identical results
-#endif
 #ifndef SVL_RING_KB
 #define SVL_RING_KB 192
 #endif
@@ -58,6 +62,23 @@ constexpr int TMAX = kFusedTextMax;
 constexpr int UMMA_N = 16;        // q columns per KV group (g <= 16, zero padded)
 constexpr int TMEM_COLS = 512;    // [0, 256): tcgen05 half of d, [256, 512): mma.sync half; 16 cols per stage
 constexpr int LDS_COL = 256;
+
+// Stage-1 selection state of the split pipeline (fresh_kernel, after the threshold bin).
+struct LeanSmem {
+    uint2 cand[16][kFastCandPerCta];  // every CTA's keys of the threshold bin: (key, unit index)
+    uint2 hdr[16];                    // every CTA's (rows above the threshold bin, candidates)
+    uint32_t rhist[256];              // resolve radix: candidate key bits 19..12
+    uint32_t ccnt[64];                // per 32-row chunk: rows above | candidates << 16
+    int32_t attc[kFastCandPerCta];    // own candidate -> local row
+    uint32_t wsum[8];
+    uint32_t bc[16];                  // b*, keys left in b*, stage, own rows above, own candidates; sub-bin, above
+    uint2 cut;                        // the last kept candidate (key, unit index)
+    uint32_t nsub, offc;
+    uint32_t sbc[8][2];               // per S warp: sub-bin, keys above it
+    uint32_t kmask[2];                // own kept candidates (bit j = candidate j)
+    uint16_t nab[kFastCandPerCta];    // candidate j: rows above b* before it
+    uint16_t ncb[2048];               // above row i: candidates before it
+};
 
 template <int D, int NT>
 struct FGeom {
@@ -78,10 +99,10 @@ struct FGeom {
     static constexpr int ATT_BYTES = (SMAX + TMAX) * 4;
     static constexpr int MISC_OFF = ATT_OFF + ATT_BYTES;
     static constexpr int NVS_MAX = SMAX / STAGE_ROWS;
-    static constexpr int MISC_BYTES = 2 * NST * 8 + 2 * NVS_MAX * 8 + 8 + 8 + 48 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
+    static constexpr int MISC_BYTES = 2 * NST * 8 + 2 * NVS_MAX * 8 + 8 + 8 + 56 + (FT / 32) * NCP * 8 + 16 * NCP * 8 + NCP * 4 +
                                       16 * 4 + 64 * 4 + 64 * 8;
     static constexpr int RCV_OFF = MISC_OFF + MISC_BYTES;       // merge receive [CS][per] + l [16][16] fp32
-    static constexpr int RCV_FLOATS = 16 * D + 16;              // CS * ceil(g D / CS) <= g D + CS
+    static constexpr int RCV_FLOATS = 16 * D + 32;              // CS * per <= g D + 2 CS (per even)
     static constexpr int BYTES = RCV_OFF + (RCV_FLOATS + 256) * 4;
     // ring re-use once streaming is over
     static constexpr int SEL_OFF = 0;                      // FastSelSmem
@@ -100,6 +121,25 @@ struct FGeom {
     static_assert(VST_OFF + VCAP * VROWB <= RING, "V staging inside the ring");
     static_assert(LRED_OFF + FT * 4 <= KEYS_OFF, "P table / O / l scratch below keys, state, slot_of");
     static_assert(RING % 1024 == 0 && QT_OFF % 1024 == 0, "128-B swizzle atoms are 1024-B aligned");
+    // split pipeline (stage 1): P table [VCL][16] hi + lo, then LeanSmem, below the keys;
+    // slot_of (uint16) over the per-row state; the gathered histograms and the resolve's
+    // sub-bin list in parts of the V staging / private histograms that are dead by then
+    static constexpr int LS_BYTES = (int)sizeof(LeanSmem);
+    static constexpr int VCL0 = (KEYS_OFF - LS_BYTES) / 64 / 16 * 16;
+    static constexpr int VCL1 = (WHIST_OFF - VST_OFF) / VROWB / 16 * 16;
+    static constexpr int VCL = VCL0 < VCL1 ? (VCL0 < 512 ? VCL0 : 512) : (VCL1 < 512 ? VCL1 : 512);
+    static constexpr int LPT_OFF = 0;
+    static constexpr int LS_OFF = VCL * 64;
+    static constexpr int LSLOT_OFF = STATE_OFF;
+    static constexpr int LHIST_OFF = (VST_OFF + TMAX * VROWB + 1023) / 1024 * 1024;
+    static constexpr int LSUB_OFF = WHIST_OFF;
+    static_assert(LS_OFF + LS_BYTES <= KEYS_OFF, "P table + LeanSmem below the keys");
+    static_assert(STATE_OFF + 2 * SMAX <= VST_OFF, "slot_of below the V staging");
+    static_assert(LHIST_OFF + 16 * 1024 <= WHIST_OFF, "gathered histograms above the text rows' V");
+    static_assert(VST_OFF + VCL * VROWB <= WHIST_OFF, "split-pipeline V staging below the sub-bin list");
+    static_assert(LSUB_OFF + 16 * kFastCandPerCta * 8 <= RING, "sub-bin list inside the ring");
+    static_assert(16 * D * 4 + FT * 4 <= VCL * 64, "O + l scratch over the dead P table");
+    static_assert(SMAX <= 2048 && VCL >= kFusedTextMax + kFastCandPerCta + 16, "chunk counts / batch sizes");
 };
 
 
@@ -115,6 +155,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     static_assert(GM::BYTES <= 227 * 1024, "shared memory budget");
 
     extern __shared__ __align__(1024) uint8_t smem[];
+    // phase stamps exist only in SVL_TRACE_BUILD builds: elsewhere the pointer is a
+    // compile-time null and every stamp (and its code) disappears
+    uint64_t* const trace_out = SVL_TRACE_BUILD ? p.trace : nullptr;
     cg::cluster_group cl = cg::this_cluster();
     const int CS = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
@@ -135,8 +178,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint64_t* vbar = ldsf + GM::NVS_MAX + 1;              // V gathers (TMA variant)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(vbar + 1);                   // TMEM base address
     uint64_t* tfull = vbar + 2;                                                 // text rows landed
-    uint64_t* xbar = vbar + 3;  // [4] DSMEM exchanges (st.async byte counts): LSE, histograms, candidates
-    float2* wpart = reinterpret_cast<float2*>(vbar + 7);                        // [16][NCP]
+    uint64_t* xbar = vbar + 3;  // [5] LSE, histograms, candidates (st.async byte counts); split pipeline: slots, V
+    float2* wpart = reinterpret_cast<float2*>(vbar + 8);                        // [16][NCP]
     float2* allpart = wpart + (FT / 32) * NCP;                   // [16][NCP] pushed by the peers
     float* lse2 = reinterpret_cast<float*>(allpart + 16 * NCP);  // [NCP]
     float* lh = lse2 + NCP;                                      // [16]
@@ -149,22 +192,31 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     uint16_t* slot_of = reinterpret_cast<uint16_t*>(smem + GM::KEYS_OFF);  // after the top-k
     uint8_t* state_s = smem + GM::STATE_OFF;
     FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(smem + GM::SEL_OFF);
+    // stamps: SM cycles (clock64, one counter for every warp of the SM); slots 0 and 10 also
+    // the global timer (CTA alignment), slots 30 / 31 the cycle counter at those two points
 #define SVL_TRACE(ph)                                                                     \
-    if (p.trace && tid == 0) {                                                            \
+    if (trace_out && tid == 0) {                                                          \
         uint64_t tnow;                                                                    \
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                          \
+        if ((ph) == 0 || (ph) == 10)                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow)::"memory");            \
+        else                                                                              \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(tnow)::"memory");               \
         trs[(ph)] = tnow;                                                                 \
     }
     auto tstamp = [&](int slot) {  // stamp from the calling thread (debug builds)
-        if (p.trace) {
+        if (trace_out) {
             uint64_t tnow;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(tnow)::"memory");
             trs[slot] = tnow;
         }
     };
-    if (p.trace && tid < 64) trs[tid] = 0;
+    if (trace_out && tid < 64) trs[tid] = 0;
     SVL_TRACE(0);
-    if (p.trace && tid == 0) trs[30] = clock64();
+    if (trace_out && tid == 0) {
+        uint64_t c0;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0)::"memory");
+        trs[30] = c0;
+    }
 
     // ------------------------------------------------------------ geometry
     // Programmatic dependent launch: the prologue (barrier init, TMEM allocation, L2
@@ -285,8 +337,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             mbar_init(smem_u32(&xbar[1]), 1);  // top-k histograms: CS x 256 words
             mbar_arrive_expect_tx(smem_u32(&xbar[1]), (uint32_t)(CS * 1024));
             mbar_init(smem_u32(&xbar[2]), 1);  // top-k candidates (armed once their count is known)
+            mbar_init(smem_u32(&xbar[3]), FT);  // split pipeline: every thread's slots / P rows
+            mbar_init(smem_u32(&xbar[4]), FT);  // ... and its V copies (cp.async arrivals)
             {
-                const int items = g * D, per = (items + CS - 1) / CS;
+                const int items = g * D, per = (((items + CS - 1) / CS) + 1) & ~1;  // (as the merge)
                 const int mine = max(0, min(per, items - rank * per));
                 mbar_init(smem_u32(mrg), 1);
                 mbar_arrive_expect_tx(smem_u32(mrg), (uint32_t)(CS * (mine + 16) * 4));
@@ -321,6 +375,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         ntext = TMAX;
     }
     nsys = max(0, min(ntext, p.vb - t0));
+    // the private top-k histograms lie past the text rows' K buffer: zeroed during the stream
+    const bool zero_early = GM::TXT_OFF + ntext * ROWB <= GM::WHIST_OFF;
     if (warp == 0) {
         if (lane == 0) {
             for (int i = 0; i < min(NST, nstages); ++i) issue(i);  // the first visual stages
@@ -376,9 +432,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 const int slot = i % NST;
                 mbar_wait(smem_u32(&full[slot]), (i / NST) & 1);
                 tc_fence_after();
-                if (p.trace && i < 32) {
+                if (trace_out && i < 32) {
                     uint64_t tnow;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                    asm volatile("mov.u64 %0, %%clock64;" : "=l"(tnow)::"memory");
                     trs[32 + i] = tnow;
                 }
                 const uint32_t sb = ring + slot * GM::STAGE_BYTES;
@@ -401,6 +457,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
 #endif
         }
         __syncwarp();
+    } else if (warp == 3) {
+        if (zero_early)
+            for (int i = lane; i < (FT / 32) * 64; i += 32)
+                reinterpret_cast<uint4*>(smem + GM::WHIST_OFF)[i] = make_uint4(0u, 0u, 0u, 0u);
     } else if (warp >= 4 && warp < 8) {
         // running (max, sum) of the visual logits, one TMEM lane (= stage row) per thread
         float rm[NCP], rl[NCP];
@@ -574,9 +634,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&ldsf[i]));
-            if (p.trace && tid == 256 && i < 16) {
+            if (trace_out && tid == 256 && i < 8) {
                 uint64_t tnow;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+                asm volatile("mov.u64 %0, %%clock64;" : "=l"(tnow)::"memory");
                 trs[48 + i] = tnow;
             }
         }
@@ -656,82 +716,498 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
 #pragma unroll
     for (int c = 0; c < NCP; ++c) nl[c] = (c < g) ? lse2[c] : INFINITY;
 
-    // ------------------------------------------------ 3. top-k (+ early V gather)
+    // ------------------------------------------------ 3. top-k
+    // Relevance keys + per-warp histograms (all warps), one all-gathered 256-bin
+    // histogram -> the threshold bin b* (identical in every CTA).  Then, when no CTA
+    // holds more than kFastCandPerCta keys of b* (stage 1, the common case), the
+    // split pipeline below; otherwise (stage 2: massive ties, b* = the catch-all bin)
+    // the generic exact radix and the batched decode; k <= 0 or k >= N_v: stage 0.
     int32_t* idx_out = p.idx_out + (int64_t)u * p.k;
-    FastSelect<FT> sel(cl, fs, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags,
-                       reinterpret_cast<uint32_t*>(smem + GM::WHIST_OFF));
-    if (p.trace) sel.tr = trs + 16;
-    sel.hbar = &xbar[1];
-    sel.cbar = &xbar[2];
-    int nslots = ntext;
-    uint32_t vphase = 0;
-    int stage = 0;  // 0 = all / none, 1 = fast path, 2 = generic
-    const bool ptmem_ready = !sel.trivial();  // the key pass (which leaves P in TMEM) runs
-    (void)ptmem_ready;
+    uint32_t* whist = reinterpret_cast<uint32_t*>(smem + GM::WHIST_OFF);
+    FastSelect<FT> sel(cl, fs, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags, whist);
+    if (trace_out) sel.tr = trs + 16;
+    LeanSmem& ls = *reinterpret_cast<LeanSmem*>(smem + GM::LS_OFF);
+    uint32_t* lhist = reinterpret_cast<uint32_t*>(smem + GM::LHIST_OFF);  // [CS][256] gathered histograms
+    int stage = 0;
     if (!sel.trivial()) {
-        sel.zero_hist();
-        cta_sync();
-        // relevance of each visual row = its share of the softmax mass, summed over the g heads
-        // (batching a warp's TMEM loads before one wait measured slower: 30.2 vs 29.7 us/layer)
-        for (int i = warp >> 2; i < nvs; i += FT / 128) {
-            float v[16];
-            load_full(i, v);
-            const int row = i * STAGE_ROWS + q4 * 32 + lane;
-#if SVL_PTMEM
-            // the decode weights p = exp2(s2 - LSE2[h]) are these exponentials: keep them,
-            // split into bf16 hi + lo pairs, in the row's TMEM columns (the P-table pass
-            // then only copies them)
-            {
-                float pv[16];
+        if (!zero_early) {  // (the text rows' K buffer reached the private histograms)
+            sel.zero_hist();
+            cta_sync();
+        }
+        // relevance of each visual row = its share of the softmax mass, summed over the g heads.
+        // A warp's stages (lane quarter warp % 4) are loaded from TMEM at once, one wait: the
+        // loop is a latency chain otherwise (load -> exponentials -> key -> histogram)
+        {
+            constexpr int NI = kFusedSliceMax / NT / STAGE_ROWS / (FT / 128);  // stages per warp
+            static_assert(NI * NCP == 32, "32 logit registers per thread");
+            uint32_t lv[32];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) pv[c] = (c < NCP) ? fast_exp2(v[c] * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
-                float packed[16];
-#pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2) {
-                    const uint32_t hw = pack_bf16(pv[2 * c2], pv[2 * c2 + 1]);
-                    packed[c2] = __uint_as_float(hw);
-                    packed[8 + c2] = __uint_as_float(pack_bf16(pv[2 * c2] - bf16lo(hw), pv[2 * c2 + 1] - bf16hi(hw)));
+            for (int m = 0; m < NI; ++m) {
+                const int i = (warp >> 2) + 4 * m;
+                if (i < nvs) {
+                    const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N;
+                    if constexpr (NCP == 8) tmem_ld8_nowait(ta, lv + m * NCP);
+                    else tmem_ld16_nowait_p(ta, lv + m * NCP);
                 }
-                tmem_st16(tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N, packed);
-                if (row < nvis) {
+            }
+            tmem_wait_ld_tie(lv);
+#pragma unroll
+            for (int m = 0; m < NI; ++m) {
+                const int i = (warp >> 2) + 4 * m;
+                const int row = i * STAGE_ROWS + q4 * 32 + lane;
+                if (i < nvs && row < nvis) {
                     float sc = 0.f;
 #pragma unroll
-                    for (int c = 0; c < NCP; ++c) sc += pv[c];
+                    for (int c = 0; c < NCP; ++c) sc += fast_exp2(__uint_as_float(lv[m * NCP + c]) * p.scale2 - nl[c]);
                     sel.add_key(row, sc);
                 }
-                continue;
-            }
-#endif
-            if (row < nvis) {
-                float sc = 0.f;
-#pragma unroll
-                for (int c = 0; c < NCP; ++c) sc += fast_exp2(v[c] * p.scale2 - nl[c]);
-                sel.add_key(row, sc);
             }
         }
-        stage = sel.threshold();
+        if (sel.nan_seen) raise_flag(p.flags, 2u /*NONFINITE*/);
+        if (tid == 0) tstamp(26);
+        tc_fence_before();
+        cta_sync();  // private histograms complete
+        tc_fence_after();
+        if (tid == 0) tstamp(27);
+        // threads 0..63 fold 4 bins of the 16 private histograms and push them to every peer
+        if (tid < 64) {
+            uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int w = 0; w < FT / 32; ++w) {
+                const uint4 h = *reinterpret_cast<const uint4*>(whist + w * 256 + 4 * tid);
+                acc.x += h.x, acc.y += h.y, acc.z += h.z, acc.w += h.w;
+            }
+            const uint32_t dst = smem_u32(lhist + rank * 256 + 4 * tid), hb = smem_u32(&xbar[1]);
+            for (int q = 0; q < CS; ++q) st_async_u4(mapa_shared(dst, q), acc, mapa_shared(hb, q));
+        }
+        if (warp == 0) {
+            // the threshold: bins 8 lane .. 8 lane + 7 summed over the CS histograms
+            mbar_wait(smem_u32(&xbar[1]), 0);
+            __syncwarp();
+            if (lane == 0) tstamp(28);
+            uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, grp = 0u, own = 0u;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {  // 2 x 16 B per histogram, all loads independent
+                if (q < CS) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(lhist + q * 256 + 8 * lane);
+                    const uint4 b2 = *reinterpret_cast<const uint4*>(lhist + q * 256 + 8 * lane + 4);
+                    c[0] += a.x, c[1] += a.y, c[2] += a.z, c[3] += a.w;
+                    c[4] += b2.x, c[5] += b2.y, c[6] += b2.z, c[7] += b2.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) grp += c[i];
+            uint32_t suf = grp;  // keys in bins >= 8 lane
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_down_sync(0xffffffffu, suf, off);
+                if (lane + off < 32) suf += y;
+            }
+            const unsigned ball = __ballot_sync(0xffffffffu, suf >= (uint32_t)p.k);
+            const int lstar = ball ? 31 - __clz(ball) : 0;
+            uint32_t above = suf - grp;
+            int bl = 8 * lane;
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+                if (above + c[i] >= (uint32_t)p.k) {
+                    bl = 8 * lane + i;
+                    break;
+                }
+                above += c[i];
+            }
+            const int bstar = __shfl_sync(0xffffffffu, bl, lstar);
+            above = __shfl_sync(0xffffffffu, above, lstar);
+            // per-CTA counts of b*, and this CTA's rows above it
+            const uint32_t cq = (lane < CS) ? lhist[lane * 256 + bstar] : 0u;
+            uint32_t maxc = cq, totc = cq;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) own += (8 * lane + i > bstar) ? lhist[rank * 256 + 8 * lane + i] : 0u;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, off));
+                totc += __shfl_xor_sync(0xffffffffu, totc, off);
+                own += __shfl_xor_sync(0xffffffffu, own, off);
+            }
+            const int st = (bstar == 0 || maxc > (uint32_t)kFastCandPerCta) ? 2 : 1;
+            if (lane == 0) {
+                ls.bc[0] = (uint32_t)bstar;
+                ls.bc[1] = (uint32_t)p.k - above;  // keys still to keep inside b*
+                ls.bc[2] = (uint32_t)st;
+                ls.bc[3] = own;
+                ls.bc[4] = lhist[rank * 256 + bstar];
+                // every CTA's (above, count) header + its candidates
+                if (st == 1) mbar_arrive_expect_tx(smem_u32(&xbar[2]), totc * 8u + (uint32_t)CS * 8u);
+            }
+        }
+        cta_sync();  // threshold published
+        stage = (int)ls.bc[2];
     }
     SVL_TRACE(3);
+
+    // ------------------------------------------------ 5. cluster merge layout (plain sums)
+    // CTA q owns output items [q*per, (q+1)*per) of the unit's g x D block (per even, so an
+    // element pair never straddles two owners); every CTA stores its partial of those items
+    // and its 16 l sums straight into the owner's receive buffer with st.async, counted on
+    // the owner's mbarrier; the owner waits for the bytes it expects and sums in sender order.
+    const int items = g * D;
+    const int per = (((items + CS - 1) / CS) + 1) & ~1;
+    float* rcv = reinterpret_cast<float*>(smem + GM::RCV_OFF);  // [CS][per]
+    float* lrcv = rcv + GM::RCV_FLOATS;                          // [16][16]
+    const uint32_t rcv_a = smem_u32(rcv), lrcv_a = smem_u32(lrcv), mrg_a = smem_u32(mrg);
+    int fin_threads = FT;  // threads that finish the owned items
+
+    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     if (stage == 1) {
-        // every row at or above the threshold bin gets a V slot now (superset of the kept rows)
-        nslots = ntext + sel.assign_slots_and_push_candidates(att + ntext);
+        // ============================================ split pipeline (stage 1)
+        // The post-stream chain is latency bound (a CTA barrier ~300 cycles, a cold branch
+        // target ~500: tools/icache_probe2.cu), so it is arranged for few barriers:
+        // U (all warps, one barrier): slots in index order for the rows above b* (kept for
+        //   sure) and the keys of b* (candidates); each warp writes its rows' P, issues their
+        //   V gathers and pushes its candidates to every peer.
+        // D (warps 0-7): P.V over the text + above rows as soon as their V lands, then over
+        //   the candidates once the cut is known; the output partials and the denominators
+        //   (an MMA against ones) go from registers straight to the owning peers.
+        // S (warps 8-15): the exact cut among the gathered candidates, handed to D, then this
+        //   CTA's kept indices (ascending) from prefix counts recorded by U.
+        const int bstar = (int)ls.bc[0];
+        const uint32_t krem = ls.bc[1];
+        const int na_loc = (int)ls.bc[3], nc_loc = (int)ls.bc[4];
+        const int candR = (nc_loc + 15) & ~15;
+        constexpr int VCL = GM::VCL;
+        const int capA = VCL - candR;   // P / V rows of the text + above batches; candidates at [capA, VCL)
+        const int nA = ntext + na_loc;  // virtual slots: text rows, then the above rows in index order
+        const int n0 = min(nA, capA);
+        uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::LPT_OFF);
+        uint16_t* ptl = pth + VCL * 16;
+        uint16_t* slot_of = reinterpret_cast<uint16_t*>(smem + GM::LSLOT_OFF);
+        uint2* lsub = reinterpret_cast<uint2*>(smem + GM::LSUB_OFF);
+        const uint32_t ubar_s = smem_u32(&xbar[3]), ubar_v = smem_u32(&xbar[4]);
+        const unsigned lt = (1u << lane) - 1u;
+        const int nch = (nvis + 31) >> 5;
+        auto cls_of = [&](uint32_t key) -> int {
+            const int dg = rel_digit(key);
+            return dg > bstar ? 2 : (dg == bstar ? 1 : 0);
+        };
+        // P row = exp2(s2 - LSE2[h]) of heads h < g as split bf16 hi + lo (zero padded to 16 heads)
+        auto write_p_row = [&](int prow, const float (&v)[16]) {
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int c2 = 0; c2 < 8; ++c2) {
+                hw[c2] = lw[c2] = 0u;
+                if (2 * c2 < NCP) {
+                    const float pa = fast_exp2(v[2 * c2] * p.scale2 - nl[2 * c2]);
+                    const float pb = fast_exp2(v[2 * c2 + 1] * p.scale2 - nl[2 * c2 + 1]);
+                    hw[c2] = pack_bf16(pa, pb);
+                    lw[c2] = pack_bf16(pa - bf16lo(hw[c2]), pb - bf16hi(hw[c2]));
+                }
+            }
+            uint4* dh = reinterpret_cast<uint4*>(pth + prow * 16);
+            uint4* dl = reinterpret_cast<uint4*>(ptl + prow * 16);
+            dh[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            dh[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+            dl[0] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            dl[1] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+        };
+        // U1: per-chunk counts (chunk c = 32 rows; warp w owns chunks 16 j + w, which lie in
+        // its TMEM lane quarter: stage c / 4, quarter c % 4 = w % 4)
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            const int c = 16 * j + warp, r = 32 * c + lane;
+            const int cl_ = (c < nch && r < nvis) ? cls_of(keys_s[r]) : 0;
+            const unsigned ba = __ballot_sync(0xffffffffu, cl_ == 2), bc = __ballot_sync(0xffffffffu, cl_ == 1);
+            if (c < nch && lane == 0) ls.ccnt[c] = (uint32_t)__popc(ba) | ((uint32_t)__popc(bc) << 16);
+        }
+        if (warp >= 8) {  // S: zero the resolve scratch (published by the barrier below)
+            const int ts = tid - 256;
+            ls.rhist[ts] = 0u;
+            if (ts == 0) ls.nsub = 0u, ls.offc = 0u;
+        }
+        cta_sync();  // chunk counts
+        SVL_TRACE(56);
+        // U2: exclusive prefixes of the chunk counts (every warp scans all 64)
+        const uint32_t e0 = (2 * lane < nch) ? ls.ccnt[2 * lane] : 0u;
+        const uint32_t e1 = (2 * lane + 1 < nch) ? ls.ccnt[2 * lane + 1] : 0u;
+        uint32_t inc = e0 + e1;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += y;
+        }
+        const uint32_t ex0 = inc - e0 - e1, ex1 = inc - e1;  // prefixes of chunks 2 lane, 2 lane + 1
+        if (tid < CS)  // this CTA's header: (rows above b*, candidates)
+            st_async_u2(mapa_shared(smem_u32(&ls.hdr[rank]), tid), make_uint2((uint32_t)na_loc, (uint32_t)nc_loc),
+                        mapa_shared(smem_u32(&xbar[2]), tid));
+        // U3: slots, prefix counts for the emission, P rows, candidate pushes, V gathers
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            const int c = 16 * j + warp;
+            if (c >= nch) break;
+            const int r = 32 * c + lane;
+            const uint32_t ck = (r < nvis) ? keys_s[r] : 0u;
+            const uint32_t pre = __shfl_sync(0xffffffffu, (c & 1) ? ex1 : ex0, c >> 1);
+            const int cl_ = (r < nvis) ? cls_of(ck) : 0;
+            const unsigned ba = __ballot_sync(0xffffffffu, cl_ == 2), bc = __ballot_sync(0xffffffffu, cl_ == 1);
+            const int preA = (int)(pre & 0xffffu), preC = (int)(pre >> 16);
+            const int ia = preA + __popc(ba & lt), jc = preC + __popc(bc & lt);  // rows above / candidates before r
+            int prow = -1;
+            uint16_t so = 0xffffu;
+            if (cl_ == 2) {
+                att[ntext + ia] = r;
+                ls.ncb[ia] = (uint16_t)jc;
+                so = (uint16_t)(ntext + ia);
+                if (ntext + ia < capA) prow = ntext + ia;
+            } else if (cl_ == 1) {
+                ls.attc[jc] = r;
+                ls.nab[jc] = (uint16_t)ia;
+                so = (uint16_t)(0x8000u | (uint32_t)jc);
+                prow = capA + jc;
+                const uint2 cv = make_uint2(ck, (uint32_t)(v0 + r));
+                const uint32_t dst = smem_u32(&ls.cand[rank][jc]), cb = smem_u32(&xbar[2]);
+                for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), cv, mapa_shared(cb, q));
+            }
+            if (r < nvis) slot_of[r] = so;
+            if (__any_sync(0xffffffffu, prow >= 0)) {  // P rows from the logits in TMEM
+                float v[16];
+                load_full(c >> 2, v);
+                if (prow >= 0) write_p_row(prow, v);
+            }
+            __syncwarp();  // this warp's att / attc entries
+            // V of this chunk's batch-0 above rows and candidates (consecutive slots)
+            const int a0 = ntext + preA, na_c = max(0, min(a0 + __popc(ba), capA) - a0), nc_c = __popc(bc);
+            for (int e = lane; e < (na_c + nc_c) * CH; e += 32) {
+                const int k2 = e / CH, cc = e % CH;
+                const int dst = k2 < na_c ? a0 + k2 : capA + preC + (k2 - na_c);
+                const int rr = k2 < na_c ? att[a0 + k2] : ls.attc[preC + (k2 - na_c)];
+                cp_async16(vst + dst * GM::VROWB + cc * 16, Vb + (int64_t)(p.vb + v0 + rr) * p.vst + cc * 8, true);
+            }
+        }
+        // text rows' P (their V has been in flight since the LSE exchange)
+        for (int i = tid; i < ntext * 16; i += FT) {
+            const int rr = i >> 4, h = i & 15;
+            float pv = 0.f;
+            if (h < g) pv = fast_exp2(txl[rr * NCP + h] - lse2[h]);
+            const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+            const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+            pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
+            ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
+        }
+        // padding rows of the two regions: P = 0 and V = 0 (0 * stale NaN would poison P.V)
+        {
+            const int npa = ((n0 + 15) & ~15) - n0, npc = candR - nc_loc;
+            for (int i = tid; i < (npa + npc) * 2; i += FT) {
+                const int rr = (i >> 1) < npa ? n0 + (i >> 1) : capA + nc_loc + ((i >> 1) - npa);
+                reinterpret_cast<uint4*>(pth + rr * 16)[i & 1] = make_uint4(0u, 0u, 0u, 0u);
+                reinterpret_cast<uint4*>(ptl + rr * 16)[i & 1] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            for (int i = tid; i < (npa + npc) * CH; i += FT) {
+                const int k2 = i / CH, rr = k2 < npa ? n0 + k2 : capA + nc_loc + (k2 - npa);
+                *reinterpret_cast<uint4*>(smem + GM::VST_OFF + rr * GM::VROWB + (i % CH) * 16) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        mbar_arrive(ubar_s);               // this thread's slots / P rows / prefix counts
+        cp_async_mbar_arrive_noinc(ubar_v);  // ... and, once landed, its V copies
         SVL_TRACE(11);
-#if SVL_EXP_RESOLVE_FIRST
-        SVL_TRACE(12);
-        sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
-        gather_rows(ntext, min(nslots, VCAP), 0);
-        v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
-#else
-        cta_sync();  // every thread's V-slot assignments (att) visible to the gathering threads
-        gather_rows(ntext, min(nslots, VCAP), 0);
-        v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
-        SVL_TRACE(12);
-        sel.resolve_and_emit(idx_out);  // state_s[i] = 2 for kept rows
-#endif
+
+        if (warp < 8) {
+            // ---------------------------------------- D: decode
+            // segments: batch 0 (prepared by U), overflow batches (a CTA keeping more rows than
+            // the staging holds), the candidates once the cut is known -- one P.V call site
+            const int nover = nA > capA ? (nA - capA + capA - 1) / capA : 0;
+            float lsum[4] = {0.f, 0.f, 0.f, 0.f};  // warp 0: l[gid] in [0], l[gid + 8] in [2]
+#pragma unroll 1
+            for (int sg = 0; sg <= nover + 1; ++sg) {
+                int row0 = 0, nr;
+                if (sg == 0) {
+                    mbar_wait(ubar_s, 0);
+                    mbar_wait(ubar_v, 0);
+                    SVL_TRACE(16);
+                    nr = (n0 + 15) & ~15;
+                } else if (!SVL_EXP_HOTONLY && sg <= nover) {
+                    const int s0 = capA * sg, n = min(capA, nA - s0);
+                    nr = (n + 15) & ~15;
+                    named_bar_sync(1, 256);  // the previous batch's P.V is done with the staging
+                    for (int e = tid; e < n * CH; e += 256) {
+                        const int sl = s0 + e / CH, cc = e % CH;
+                        cp_async16(vst + (sl - s0) * GM::VROWB + cc * 16, Vb + (int64_t)work_row(att[sl]) * p.vst + cc * 8,
+                                   true);
+                    }
+                    cp_async_commit();
+                    for (int i = warp >> 2; i < nvs; i += 2) {  // P rows from TMEM (warp quarter = warp % 4)
+                        const int row = i * STAGE_ROWS + q4 * 32 + lane;
+                        const int sl = (row < nvis) ? (int)slot_of[row] : 0xffff;
+                        const int pr = (sl < 0x8000 && sl >= s0 && sl < s0 + n) ? sl - s0 : -1;
+                        if (!__any_sync(0xffffffffu, pr >= 0)) continue;
+                        float v[16];
+                        load_full(i, v);
+                        if (pr >= 0) write_p_row(pr, v);
+                    }
+                    for (int i = tid; i < (nr - n) * 2; i += 256) {
+                        reinterpret_cast<uint4*>(pth + (n + (i >> 1)) * 16)[i & 1] = make_uint4(0u, 0u, 0u, 0u);
+                        reinterpret_cast<uint4*>(ptl + (n + (i >> 1)) * 16)[i & 1] = make_uint4(0u, 0u, 0u, 0u);
+                    }
+                    for (int i = tid; i < (nr - n) * CH; i += 256)
+                        *reinterpret_cast<uint4*>(smem + GM::VST_OFF + (n + i / CH) * GM::VROWB + (i % CH) * 16) =
+                            make_uint4(0, 0, 0, 0);
+                    cp_async_wait<0>();
+                    named_bar_sync(1, 256);
+                } else {
+                    named_bar_sync(3, 512);  // the cut (from S)
+                    SVL_TRACE(18);
+                    const uint2 cut = ls.cut;
+                    for (int jc = tid; jc < nc_loc; jc += 256) {  // the candidates the cut drops: P = 0
+                        const int r = ls.attc[jc];
+                        const uint32_t key = keys_s[r], gi = (uint32_t)(v0 + r);
+                        if (!(key > cut.x || (key == cut.x && gi <= cut.y))) {
+                            uint4* dh = reinterpret_cast<uint4*>(pth + (capA + jc) * 16);
+                            uint4* dl = reinterpret_cast<uint4*>(ptl + (capA + jc) * 16);
+                            dh[0] = dh[1] = dl[0] = dl[1] = make_uint4(0u, 0u, 0u, 0u);
+                        }
+                    }
+                    named_bar_sync(1, 256);
+                    row0 = capA;
+                    nr = candR;
+                }
+                // o += P[row0, row0 + nr) . V (warp w owns columns 16w..16w+15); warp 0 also
+                // l += P . 1.  Independent accumulator chains (hi / lo x column halves x even /
+                // odd k-tiles); the next tile's fragments are loaded before this tile's MMAs.
+                if (warp < D / 16 && nr > 0) {
+                    const int mi = lane >> 3, rin = lane & 7;
+                    const uint32_t aph = smem_u32(pth) + ((mi >> 1) * 8 + rin) * 32 + (mi & 1) * 16;
+                    const uint32_t apl = smem_u32(ptl) + ((mi >> 1) * 8 + rin) * 32 + (mi & 1) * 16;
+                    const uint32_t avv = vst + ((mi & 1) * 8 + rin) * GM::VROWB + (2 * warp + (mi >> 1)) * 16;
+                    constexpr uint32_t ONES = 0x3f803f80u;  // bf16 (1, 1)
+                    float acc[2][6][4];
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int b2 = 0; b2 < 6; ++b2) acc[a][b2][0] = acc[a][b2][1] = acc[a][b2][2] = acc[a][b2][3] = 0.f;
+                    uint32_t ph[4], pl[4], vv[4];
+                    auto ld = [&](int tb) {
+                        ldsm_x4_trans(aph + tb * 32, ph[0], ph[1], ph[2], ph[3]);
+                        ldsm_x4_trans(apl + tb * 32, pl[0], pl[1], pl[2], pl[3]);
+                        ldsm_x4_trans(avv + tb * GM::VROWB, vv[0], vv[1], vv[2], vv[3]);
+                    };
+                    auto step = [&](float (&A)[6][4], int tb) {
+                        const uint32_t hh[4] = {ph[0], ph[1], ph[2], ph[3]}, ll[4] = {pl[0], pl[1], pl[2], pl[3]};
+                        const uint32_t w0 = vv[0], w1 = vv[1], w2 = vv[2], w3 = vv[3];
+                        if (tb + 16 < row0 + nr) ld(tb + 16);
+                        mma_bf16_16816(A[0], hh, w0, w1);
+                        mma_bf16_16816(A[1], ll, w0, w1);
+                        mma_bf16_16816(A[2], hh, w2, w3);
+                        mma_bf16_16816(A[3], ll, w2, w3);
+                        if (warp == 0) {
+                            mma_bf16_16816(A[4], hh, ONES, ONES);
+                            mma_bf16_16816(A[5], ll, ONES, ONES);
+                        }
+                    };
+                    ld(row0);
+                    for (int tb = row0; tb < row0 + nr; tb += 32) {
+                        step(acc[0], tb);
+                        if (tb + 16 < row0 + nr) step(acc[1], tb + 16);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        o[0][e] += (acc[0][0][e] + acc[0][1][e]) + (acc[1][0][e] + acc[1][1][e]);
+                        o[1][e] += (acc[0][2][e] + acc[0][3][e]) + (acc[1][2][e] + acc[1][3][e]);
+                        lsum[e] += (acc[0][4][e] + acc[0][5][e]) + (acc[1][4][e] + acc[1][5][e]);
+                    }
+                }
+            }
+            SVL_TRACE(19);
+            // push the partial O (fragment pairs) and, from warp 0, the 16 denominators
+            if (warp < D / 16) {
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const int h = gid + 8 * hf;
+                        if (h < g) {
+                            const int i = h * D + warp * 16 + nt * 8 + 2 * t, q = i / per, jj = i - q * per;
+                            st_async_f2(mapa_shared(rcv_a + (uint32_t)(rank * per + jj) * 4u, q), o[nt][2 * hf],
+                                        o[nt][2 * hf + 1], mapa_shared(mrg_a, q));
+                        }
+                    }
+                if (warp == 0 && t == 0)
+                    for (int q = 0; q < CS; ++q) {
+                        st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + gid) * 4u, q), lsum[0], mapa_shared(mrg_a, q));
+                        st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + gid + 8) * 4u, q), lsum[2],
+                                     mapa_shared(mrg_a, q));
+                    }
+            }
+            fin_threads = 256;
+        } else {
+            // ---------------------------------------- S: exact cut + emit
+            const int ts = tid - 256, ws = warp - 8;
+            mbar_wait(smem_u32(&xbar[2]), 0);  // every CTA's header + candidates
+            __syncwarp();
+            if (ts == 0) tstamp(20);
+            for (int sl = ts; sl < CS * kFastCandPerCta; sl += 256) {  // one radix pass, key bits 19..12
+                const int q = sl / kFastCandPerCta, jc = sl % kFastCandPerCta;
+                if ((uint32_t)jc < ls.hdr[q].y) atomicAdd(&ls.rhist[(ls.cand[q][jc].x >> 12) & 255u], 1u);
+            }
+            named_bar_sync(2, 256);
+            warp_find_nb<256>(ls.rhist, krem, ls.sbc[ws]);  // every S warp (no barrier)
+            __syncwarp();
+            const uint32_t bA = ls.sbc[ws][0], need = krem - ls.sbc[ws][1];  // keep `need` keys of sub-bin bA
+            for (int sl = ts; sl < CS * kFastCandPerCta; sl += 256) {
+                const int q = sl / kFastCandPerCta, jc = sl % kFastCandPerCta;
+                if ((uint32_t)jc < ls.hdr[q].y) {
+                    const uint2 cv = ls.cand[q][jc];
+                    if (((cv.x >> 12) & 255u) == bA) lsub[atomicAdd(&ls.nsub, 1u)] = cv;
+                }
+            }
+            named_bar_sync(2, 256);
+            const uint32_t nsub = ls.nsub;
+            for (uint32_t m = ts; m < nsub; m += 256) {  // exact rank: (key desc, index asc)
+                const uint2 cv = lsub[m];
+                uint32_t rk = 0u;
+#pragma unroll 8
+                for (uint32_t i = 0; i < nsub; ++i) {
+                    const uint2 d2 = lsub[i];
+                    rk += d2.x > cv.x || (d2.x == cv.x && d2.y < cv.y);
+                }
+                if (rk == need - 1u) ls.cut = cv;
+            }
+            named_bar_sync(2, 256);
+            named_bar_arrive(3, 512);  // hand the cut to D
+            if (ts == 0) tstamp(21);
+            const uint2 cut = ls.cut;
+            auto kept_c = [&](uint2 cv) { return cv.x > cut.x || (cv.x == cut.x && cv.y <= cut.y); };
+            // own kept candidates (index order = candidate order) as a 64-bit mask; the
+            // output offset = lower-ranked CTAs' rows above b* + their kept candidates
+            if (ws == 0) {
+                const unsigned k0 = __ballot_sync(0xffffffffu, (uint32_t)lane < (uint32_t)nc_loc && kept_c(ls.cand[rank][lane]));
+                const unsigned k1 = __ballot_sync(0xffffffffu, (uint32_t)(lane + 32) < (uint32_t)nc_loc && kept_c(ls.cand[rank][lane + 32]));
+                if (lane == 0) ls.kmask[0] = k0, ls.kmask[1] = k1;
+            }
+            uint32_t pc = 0u;
+            for (int sl = ts; sl < rank * kFastCandPerCta; sl += 256) {
+                const int q = sl / kFastCandPerCta, jc = sl % kFastCandPerCta;
+                if ((uint32_t)jc < ls.hdr[q].y) pc += kept_c(ls.cand[q][jc]);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, off);
+            if (lane == 0 && pc) atomicAdd(&ls.offc, pc);
+            named_bar_sync(2, 256);
+            mbar_wait(ubar_s, 0);  // U's slots and prefix counts
+            uint32_t off = ls.offc;
+#pragma unroll 4
+            for (int q = 0; q < rank; ++q) off += ls.hdr[q].x;
+            const uint64_t km = (uint64_t)ls.kmask[0] | ((uint64_t)ls.kmask[1] << 32);
+            auto kept_before = [&](int n) { return (uint32_t)__popcll(n >= 64 ? km : (km & ((1ull << n) - 1ull))); };
+            for (int ia = ts; ia < na_loc; ia += 256)  // rows above b*: all kept
+                idx_out[off + ia + kept_before(ls.ncb[ia])] = v0 + att[ntext + ia];
+            for (int jc = ts; jc < nc_loc; jc += 256)  // kept candidates
+                if ((km >> jc) & 1ull) idx_out[off + ls.nab[jc] + kept_before(jc)] = v0 + ls.attc[jc];
+            if (ts == 0) tstamp(22);
+            fin_threads = 0;
+        }
     } else {
-#if SVL_EXP_FLAG_STAGE2
-        if (stage == 2 && tid == 0 && rank == 0) raise_flag(p.flags, 0x100u);
-#endif
+        float lacc = 0.f;  // thread tid sums head tid % 16
+#if !SVL_EXP_HOTONLY
+        // ============================================ stage 0 (all / none) or 2 (generic)
+        int nslots = ntext;
+        uint32_t vphase = 0;
         if (stage == 2) {
             // the generic scratch aliases the V staging: every CTA's text-row gather
             // must land before any peer pushes into it (text rows are re-gathered)
@@ -745,154 +1221,125 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         nslots = ntext + nsel;
         gather_rows(stage == 2 ? 0 : ntext, min(nslots, VCAP), 0);
         v_expect((uint32_t)(min(nslots, VCAP) * ROWB));
-    }
-    SVL_TRACE(4);
+        SVL_TRACE(4);
 
-    // ------------------------------------------------ 4. decode over the kept rows
-    // p = exp2(s2 - LSE2[h]): the same reference in every CTA -> plain-sum merge.
-    float lacc = 0.f;  // thread tid sums head tid % 16 (FT % 16 == 0)
-    float o[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::PT_OFF);
-    uint16_t* ptl = pth + VCAP * 16;
-    cta_sync();  // top-k scratch (aliased by the P table and slot_of) is dead
-    for (int sl = ntext + tid; sl < nslots; sl += FT) slot_of[att[sl]] = (uint16_t)sl;
-    for (int s0 = 0; s0 < nslots; s0 += VCAP) {
-        const int n = min(VCAP, nslots - s0);
-        const int nr = (n + 15) & ~15;
-        if (s0 > 0) {  // overflow batches (rare): after the previous PV
-            gather_rows(s0, s0 + n, s0);
-            v_expect((uint32_t)(n * ROWB));
-        }
-        // P table rows [0, nr): zero, then the text rows and the kept visual rows
-        for (int i = tid; i < nr * 2; i += FT) {  // 16 heads x 2 B = 32 B = 2 uint4 per row and table
-            reinterpret_cast<uint4*>(pth)[i] = make_uint4(0, 0, 0, 0);
-            reinterpret_cast<uint4*>(ptl)[i] = make_uint4(0, 0, 0, 0);
-        }
-        cta_sync();
-        for (int i = tid; i < (min(ntext, s0 + n) - s0) * 16; i += FT) {
-            const int rr = i >> 4, h = i & 15;
-            if (h < g) {
-                const float pv = fast_exp2(txl[(att[s0 + rr] - nvis) * NCP + h] - lse2[h]);
-                const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
-                const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
-                pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
-                ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
+        // p = exp2(s2 - LSE2[h]): the same reference in every CTA -> plain-sum merge.
+        uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::PT_OFF);
+        uint16_t* ptl = pth + VCAP * 16;
+        cta_sync();  // top-k scratch (aliased by the P table and slot_of) is dead
+        for (int sl = ntext + tid; sl < nslots; sl += FT) slot_of[att[sl]] = (uint16_t)sl;
+        for (int s0 = 0; s0 < nslots; s0 += VCAP) {
+            const int n = min(VCAP, nslots - s0);
+            const int nr = (n + 15) & ~15;
+            if (s0 > 0) {  // overflow batches (rare): after the previous PV
+                gather_rows(s0, s0 + n, s0);
+                v_expect((uint32_t)(n * ROWB));
             }
-        }
-        for (int i = warp >> 2; i < nvs; i += FT / 128) {
-            const int row = i * STAGE_ROWS + q4 * 32 + lane;
-            const bool kept = row < nvis && state_s[row] == kKeySel;
-            if (!__any_sync(0xffffffffu, kept)) continue;
-            float v[16];
-            load_full(i, v);
-            const int rr = kept ? (int)slot_of[row] - s0 : -1;
-#if SVL_PTMEM
-            if (!ptmem_ready) goto compute_p;
-            if (rr >= 0 && rr < n) {  // hi + lo pairs written by the key pass
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
-                uint4* dh = reinterpret_cast<uint4*>(pth + rr * 16);
-                uint4* dl = reinterpret_cast<uint4*>(ptl + rr * 16);
-                dh[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                dh[1] = make_uint4(w[4], w[5], w[6], w[7]);
-                dl[0] = make_uint4(w[8], w[9], w[10], w[11]);
-                dl[1] = make_uint4(w[12], w[13], w[14], w[15]);
+            // P table rows [0, nr): zero, then the text rows and the kept visual rows
+            for (int i = tid; i < nr * 2; i += FT) {  // 16 heads x 2 B = 32 B = 2 uint4 per row and table
+                reinterpret_cast<uint4*>(pth)[i] = make_uint4(0, 0, 0, 0);
+                reinterpret_cast<uint4*>(ptl)[i] = make_uint4(0, 0, 0, 0);
             }
-            continue;
-        compute_p:
-#endif
-            if (rr >= 0 && rr < n) {
-                uint32_t hw[8], lw[8];
-#pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2) {
-                    float pv2[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int c = 2 * c2 + e;
-                        pv2[e] = (c < NCP) ? fast_exp2(v[c] * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
-                    }
-                    hw[c2] = pack_bf16(pv2[0], pv2[1]);
-                    lw[c2] = pack_bf16(pv2[0] - bf16lo(hw[c2]), pv2[1] - bf16hi(hw[c2]));
+            cta_sync();
+            for (int i = tid; i < (min(ntext, s0 + n) - s0) * 16; i += FT) {
+                const int rr = i >> 4, h = i & 15;
+                if (h < g) {
+                    const float pv = fast_exp2(txl[(att[s0 + rr] - nvis) * NCP + h] - lse2[h]);
+                    const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+                    const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+                    pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
+                    ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
                 }
-                uint4* dh = reinterpret_cast<uint4*>(pth + rr * 16);
-                uint4* dl = reinterpret_cast<uint4*>(ptl + rr * 16);
-                dh[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                dh[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
-                dl[0] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-                dl[1] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
             }
-        }
-        // rows [n, nr) of the staging buffer: zero V (the P rows are zero, avoid NaN * 0)
-        for (int i = n * CH + tid; i < nr * CH; i += FT) {
-            const int rr = i / CH, c = i % CH;
-            *reinterpret_cast<uint4*>(smem + GM::VST_OFF + rr * GM::VROWB + c * 16) = make_uint4(0, 0, 0, 0);
-        }
-        v_wait(vphase);
-        vphase ^= 1u;
-        cta_sync();
-        // denominators from the table itself (hi + lo: the weights the PV uses)
-        for (int i = tid; i < nr * 16; i += FT) {
-            const uint32_t hv = pth[i], lv = ptl[i];
-            lacc += __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
-        }
-        SVL_TRACE(5);
-        if (warp < D / 16) {
-            const int mi = lane >> 3, rin = lane & 7;
-            const uint32_t aph = smem_u32(pth), apl = smem_u32(ptl);
-            for (int tb = 0; tb < nr; tb += 16) {
-                // P fragment (m = heads, k = rows): matrices (h0-7,k0-7) (h8-15,k0-7) (h0-7,k8-15) (h8-15,k8-15)
-                const int prow = tb + (mi >> 1) * 8 + rin;
-                uint32_t ph[4], pl[4];
-                ldsm_x4_trans(aph + prow * 32 + (mi & 1) * 16, ph[0], ph[1], ph[2], ph[3]);
-                ldsm_x4_trans(apl + prow * 32 + (mi & 1) * 16, pl[0], pl[1], pl[2], pl[3]);
-                const int vrow = tb + (mi & 1) * 8 + rin;
-                const int c = 2 * warp + (mi >> 1);
-                uint32_t v0r, v1r, v2r, v3r;
-                ldsm_x4_trans(vst + vrow * GM::VROWB + c * 16, v0r, v1r, v2r, v3r);
-                mma_bf16_16816(o[0], ph, v0r, v1r);
-                mma_bf16_16816(o[0], pl, v0r, v1r);
-                mma_bf16_16816(o[1], ph, v2r, v3r);
-                mma_bf16_16816(o[1], pl, v2r, v3r);
-            }
-        }
-        cta_sync();  // staging + P table free for the next batch
-    }
-    SVL_TRACE(6);
-    float* lred = reinterpret_cast<float*>(smem + GM::LRED_OFF);
-    float* octa = reinterpret_cast<float*>(smem + GM::OCTA_OFF);  // [16][D]
-    lred[tid] = lacc;
-    if (warp < D / 16) {
+            for (int i = warp >> 2; i < nvs; i += FT / 128) {
+                const int row = i * STAGE_ROWS + q4 * 32 + lane;
+                const bool kept = row < nvis && state_s[row] == kKeySel;
+                if (!__any_sync(0xffffffffu, kept)) continue;
+                float v[16];
+                load_full(i, v);
+                const int rr = kept ? (int)slot_of[row] - s0 : -1;
+                if (rr >= 0 && rr < n) {
+                    uint32_t hw[8], lw[8];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            const int col = warp * 16 + nt * 8 + 2 * t;
-            if (gid < g) *reinterpret_cast<float2*>(octa + gid * D + col) = make_float2(o[nt][0], o[nt][1]);
-            if (gid + 8 < g) *reinterpret_cast<float2*>(octa + (gid + 8) * D + col) = make_float2(o[nt][2], o[nt][3]);
+                    for (int c2 = 0; c2 < 8; ++c2) {
+                        float pv2[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int c = 2 * c2 + e;
+                            pv2[e] = (c < NCP) ? fast_exp2(v[c] * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
+                        }
+                        hw[c2] = pack_bf16(pv2[0], pv2[1]);
+                        lw[c2] = pack_bf16(pv2[0] - bf16lo(hw[c2]), pv2[1] - bf16hi(hw[c2]));
+                    }
+                    uint4* dh = reinterpret_cast<uint4*>(pth + rr * 16);
+                    uint4* dl = reinterpret_cast<uint4*>(ptl + rr * 16);
+                    dh[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    dh[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+                    dl[0] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                    dl[1] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+                }
+            }
+            // rows [n, nr) of the staging buffer: zero V (the P rows are zero, avoid NaN * 0)
+            for (int i = n * CH + tid; i < nr * CH; i += FT) {
+                const int rr = i / CH, c = i % CH;
+                *reinterpret_cast<uint4*>(smem + GM::VST_OFF + rr * GM::VROWB + c * 16) = make_uint4(0, 0, 0, 0);
+            }
+            v_wait(vphase);
+            vphase ^= 1u;
+            cta_sync();
+            // denominators from the table itself (hi + lo: the weights the PV uses)
+            for (int i = tid; i < nr * 16; i += FT) {
+                const uint32_t hv = pth[i], lv = ptl[i];
+                lacc += __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
+            }
+            SVL_TRACE(5);
+            if (warp < D / 16) {
+                const int mi = lane >> 3, rin = lane & 7;
+                const uint32_t aph = smem_u32(pth), apl = smem_u32(ptl);
+                for (int tb = 0; tb < nr; tb += 16) {
+                    // P fragment (m = heads, k = rows): matrices (h0-7,k0-7) (h8-15,k0-7) (h0-7,k8-15) (h8-15,k8-15)
+                    const int prow = tb + (mi >> 1) * 8 + rin;
+                    uint32_t ph[4], pl[4];
+                    ldsm_x4_trans(aph + prow * 32 + (mi & 1) * 16, ph[0], ph[1], ph[2], ph[3]);
+                    ldsm_x4_trans(apl + prow * 32 + (mi & 1) * 16, pl[0], pl[1], pl[2], pl[3]);
+                    const int vrow = tb + (mi & 1) * 8 + rin;
+                    const int c = 2 * warp + (mi >> 1);
+                    uint32_t v0r, v1r, v2r, v3r;
+                    ldsm_x4_trans(vst + vrow * GM::VROWB + c * 16, v0r, v1r, v2r, v3r);
+                    mma_bf16_16816(o[0], ph, v0r, v1r);
+                    mma_bf16_16816(o[0], pl, v0r, v1r);
+                    mma_bf16_16816(o[1], ph, v2r, v3r);
+                    mma_bf16_16816(o[1], pl, v2r, v3r);
+                }
+            }
+            cta_sync();  // staging + P table free for the next batch
         }
-    }
-    cta_sync();
-    if (tid < 16) {
-        float acc = 0.f;
-        for (int j = 0; j < FT / 16; ++j) acc += lred[j * 16 + tid];
-        lh[tid] = acc;
-    }
-    cta_sync();  // lh complete before it is pushed
-    // ------------------------------------------------ 5. cluster merge (plain sums)
-    // Push style: CTA q owns output items [q*per, (q+1)*per) of the unit's g x D
-    // block; every CTA stores its partial of those items (and its 16 l sums)
-    // straight into the owner's receive buffer with st.async, which counts the
-    // bytes on the owner's mbarrier.  The owner waits for the bytes it expects and
-    // sums in sender order; no CTA reads a peer's shared memory, so a CTA whose
-    // inbound pushes have landed may exit at once (no closing cluster barrier).
-    const int items = g * D;
-    const int per = (items + CS - 1) / CS;
-    float* rcv = reinterpret_cast<float*>(smem + GM::RCV_OFF);   // [CS][per]
-    float* lrcv = rcv + GM::RCV_FLOATS;                           // [16][16]
-    SVL_TRACE(7);
-    {
-        const uint32_t rcv_a = smem_u32(rcv), lrcv_a = smem_u32(lrcv), mrg_a = smem_u32(mrg);
+#endif
+        float* octa = reinterpret_cast<float*>(smem + GM::OCTA_OFF);  // [16][D]
+        float* lred = reinterpret_cast<float*>(smem + GM::LRED_OFF);
+        cta_sync();  // P.V done everywhere
+        SVL_TRACE(6);
+        lred[tid] = lacc;
+        if (warp < D / 16) {
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int col = warp * 16 + nt * 8 + 2 * t;
+                if (gid < g) *reinterpret_cast<float2*>(octa + gid * D + col) = make_float2(o[nt][0], o[nt][1]);
+                if (gid + 8 < g) *reinterpret_cast<float2*>(octa + (gid + 8) * D + col) = make_float2(o[nt][2], o[nt][3]);
+            }
+        }
+        cta_sync();
+        if (tid < 16) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < FT / 16; ++j) acc += lred[j * 16 + tid];
+            lh[tid] = acc;
+        }
+        cta_sync();  // lh complete before it is pushed
+        SVL_TRACE(7);
         for (int i = tid; i < items; i += FT) {
             const int q = i / per, j = i - q * per;
-            st_async_f32(mapa_shared(rcv_a + (uint32_t)(rank * per + j) * 4u, q), octa[(i / D) * D + (i % D)],
-                         mapa_shared(mrg_a, q));
+            st_async_f32(mapa_shared(rcv_a + (uint32_t)(rank * per + j) * 4u, q), octa[i], mapa_shared(mrg_a, q));
         }
         if (tid < 16 * CS)
             st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + (tid & 15)) * 4u, tid >> 4), lh[tid & 15],
@@ -900,15 +1347,18 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     }
     tc_fence_before();  // every TMEM read of this CTA precedes the dealloc below
     SVL_TRACE(8);
-    mbar_wait(smem_u32(mrg), 0);
-    for (int j = tid; j < per; j += FT) {
+    if (tid < fin_threads) mbar_wait(mrg_a, 0);
+    for (int j = tid; j < per && tid < fin_threads; j += fin_threads) {
         const int i = rank * per + j;
         if (i >= items) break;
         const int h = i / D, dd = i % D;
         float num = 0.f, den = 0.f;
-        for (int q = 0; q < CS; ++q) {
-            num += rcv[q * per + j];
-            den += lrcv[q * 16 + h];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {  // (sender order; the loads are independent)
+            if (q < CS) {
+                num += rcv[q * per + j];
+                den += lrcv[q * 16 + h];
+            }
         }
         const int hh = G * g + h;
         p.out[((int64_t)b * p.H + hh) * D + dd] = (den > 0.f) ? num / den : 0.f;
@@ -919,12 +1369,19 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     SVL_TRACE(9);
     tc_fence_before();
     SVL_TRACE(10);
-    if (p.trace && tid == 0) trs[31] = clock64();
+    if (trace_out && tid == 0) {
+        uint64_t c1;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1)::"memory");
+        trs[31] = c1;
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tbase, TMEM_COLS);
     }
-    if (p.trace && tid < 64) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + tid] = trs[tid];
+    if (trace_out) {
+        cta_sync();  // (trace builds) every warp's stamps
+        if (tid < 64) trace_out[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + tid] = trs[tid];
+    }
 #undef SVL_TRACE
 }
 

@@ -6,7 +6,7 @@ from paper_2510_17777_b200 import inputs as gen, svl
 tag = sys.argv[1] if len(sys.argv) > 1 else ""
 _a = torch.empty(1 << 28, dtype=torch.uint8, device="cuda"); _b = torch.empty_like(_a)
 for _ in range(1000): _b.copy_(_a)
-for name, nl in (("long-video", 28), ("nvila-4k", 77)):
+for name, nl in [c for c in (("long-video", 28), ("nvila-4k", 77)) if c[0] in os.environ.get("CFGS", "long-video,nvila-4k")]:
     wl = gen.CONFIGS[name]
     xs = [gen.make_decode_inputs(wl, seed=s, device="cuda") for s in range(nl)]
     ws = svl.Workspace()

@@ -29,6 +29,17 @@ for rep in range(2):
 torch.cuda.synchronize()
 tr = ws.buf[1024:1024 + (1 << 20)].view(torch.int64)[: 2048 * 64].view(-1, 64).cpu()
 tr = tr[tr[:, 0] > 0]
+# slots 0 / 10: global timer (ns); 30 / 31: SM cycles at those points; every other slot: SM
+# cycles -> ns on the global timeline at the CTA's measured clock
+ratio = (tr[:, 10] - tr[:, 0]).double() / (tr[:, 31] - tr[:, 30]).double()
+conv = tr.clone()
+for j in range(64):
+    if j in (0, 10, 30, 31):
+        continue
+    nz = tr[:, j] != 0
+    conv[nz, j] = (tr[nz, 0].double() + (tr[nz, j] - tr[nz, 30]).double() * ratio[nz]).round().long()
+cyc_ratio = ratio
+tr, raw = conv, tr
 t0 = tr[:, 0].min()
 names = {0: "start", 1: "stream+textV", 2: "lse", 3: "hist+thr", 4: "select", 5: "Ptab+Vwait", 6: "PV", 7: "O+l",
          8: "merge-sync", 9: "merge", 10: "end", 11: "assign+push", 12: "gather-issue"}
@@ -48,9 +59,20 @@ for j, nm in post.items():
         continue
     print(f"   {nm:24s} {((col - tr[:, 0]).double() / 1e3).median().item():8.2f}")
 
+lean = {26: "keys done", 27: "B1", 28: "w0: hists landed", 12: "U: B3+slots", 11: "U: V issued", 16: "D: V landed", 17: "D: PV above", 18: "D: cut recv", 19: "D: PV cands",
+        20: "S: cands landed", 21: "S: cut", 22: "S: emitted", 6: "final sync", 23: "lred/octa",
+        24: "sync", 25: "lh", 56: "U1 (counts) + B3", 57: "U2 (scan)", 58: "U3 (slots, P, push)", 59: "U text P",
+        60: "S: cut seen (emit start)", 61: "S: peers' kept", 62: "S: own counts", 63: "S: offsets"}
+print("split pipeline (us from the threshold stamp, median / max over CTAs):")
+for j, nm in lean.items():
+    col = tr[:, j]
+    if (col == 0).any():
+        continue
+    v = (col - tr[:, 3]).double() / 1e3
+    print(f"   {nm:22s} {v.median().item():8.2f} {v.max().item():8.2f}")
 sub = ["cand-hist", "find", "flags", "mine", "scan", "off", "-", "-", "-", "-", "-", "-", "-"]
 print("resolve internals (us from gather-issue, median):")
-for j, nm in enumerate(sub):
+for j, nm in (enumerate(sub) if not (tr[:, 12] == 0).any() and (tr[:, 11] > tr[:, 12]).all() else []):
     col = tr[:, 16 + j]
     if (col == 0).any():
         continue
@@ -65,11 +87,11 @@ for j, nm in hsub.items():
     print(f"   {nm:10s} {((col - tr[:, 2]).double() / 1e3).median().item():8.2f}")
 
 print("stage arrivals (us from start, median):", " ".join(
-    f"{((tr[:, 32 + i] - tr[:, 0]).double() / 1e3).median().item():.2f}" for i in range(32) if not (tr[:, 32 + i] == 0).any()))
+    f"{((tr[:, 32 + i] - tr[:, 0]).double() / 1e3).median().item():.2f}" for i in range(24) if not (tr[:, 32 + i] == 0).any()))
 
-cyc = (tr[:, 31] - tr[:, 30]).double()
-ns = (tr[:, 10] - tr[:, 0]).double()
+cyc = (raw[:, 31] - raw[:, 30]).double()
+ns = (raw[:, 10] - raw[:, 0]).double()
 print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {(cyc / ns).median().item() * 1e3:.0f} MHz")
 
 print("LDS-warp stage done (us from start, median):", " ".join(
-    f"{((tr[:, 48 + i] - tr[:, 0]).double() / 1e3).median().item():.2f}" for i in range(16) if not (tr[:, 48 + i] == 0).any()))
+    f"{((tr[:, 48 + i] - tr[:, 0]).double() / 1e3).median().item():.2f}" for i in range(8) if not (tr[:, 48 + i] == 0).any()))
