@@ -122,22 +122,21 @@ struct FGeom {
     static_assert(LRED_OFF + FT * 4 <= KEYS_OFF, "P table / O / l scratch below keys, state, slot_of");
     static_assert(RING % 1024 == 0 && QT_OFF % 1024 == 0, "128-B swizzle atoms are 1024-B aligned");
     // split pipeline (stage 1): P table [VCL][16] hi + lo, then LeanSmem, below the keys;
-    // slot_of (uint16) over the per-row state; the gathered histograms and the resolve's
-    // sub-bin list in parts of the V staging / private histograms that are dead by then
+    // the gathered histograms and the resolve's sub-bin list in parts of the V staging /
+    // private histograms that are dead by then
     static constexpr int LS_BYTES = (int)sizeof(LeanSmem);
     static constexpr int VCL0 = (KEYS_OFF - LS_BYTES) / 64 / 16 * 16;
     static constexpr int VCL1 = (WHIST_OFF - VST_OFF) / VROWB / 16 * 16;
     static constexpr int VCL = VCL0 < VCL1 ? (VCL0 < 512 ? VCL0 : 512) : (VCL1 < 512 ? VCL1 : 512);
     static constexpr int LPT_OFF = 0;
     static constexpr int LS_OFF = VCL * 64;
-    static constexpr int LSLOT_OFF = STATE_OFF;
     static constexpr int LHIST_OFF = (VST_OFF + TMAX * VROWB + 1023) / 1024 * 1024;
     static constexpr int LSUB_OFF = WHIST_OFF;
     static_assert(LS_OFF + LS_BYTES <= KEYS_OFF, "P table + LeanSmem below the keys");
     static_assert(STATE_OFF + 2 * SMAX <= VST_OFF, "slot_of below the V staging");
     static_assert(LHIST_OFF + 16 * 1024 <= WHIST_OFF, "gathered histograms above the text rows' V");
     static_assert(VST_OFF + VCL * VROWB <= WHIST_OFF, "split-pipeline V staging below the sub-bin list");
-    static_assert(LSUB_OFF + 16 * kFastCandPerCta * 8 <= RING, "sub-bin list inside the ring");
+    static_assert(LSUB_OFF + 2 * 16 * kFastCandPerCta * 8 <= RING, "the two cut-select member lists inside the ring");
     static_assert(16 * D * 4 + FT * 4 <= VCL * 64, "O + l scratch over the dead P table");
     static_assert(SMAX <= 2048 && VCL >= kFusedTextMax + kFastCandPerCta + 16, "chunk counts / batch sizes");
 };
@@ -334,8 +333,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             // every exchange barrier: one local arrival + the bytes the peers will store
             mbar_init(smem_u32(&xbar[0]), 1);
             mbar_arrive_expect_tx(smem_u32(&xbar[0]), (uint32_t)(CS * NCP * 8));
-            mbar_init(smem_u32(&xbar[1]), 1);  // top-k histograms: CS x 256 words
-            mbar_arrive_expect_tx(smem_u32(&xbar[1]), (uint32_t)(CS * 1024));
+            mbar_init(smem_u32(&xbar[1]), 1);  // top-k histograms: CS x 512 B
+            mbar_arrive_expect_tx(smem_u32(&xbar[1]), (uint32_t)(CS * 512));
             mbar_init(smem_u32(&xbar[2]), 1);  // top-k candidates (armed once their count is known)
             mbar_init(smem_u32(&xbar[3]), FT);  // split pipeline: every thread's slots / P rows
             mbar_init(smem_u32(&xbar[4]), FT);  // ... and its V copies (cp.async arrivals)
@@ -727,7 +726,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     FastSelect<FT> sel(cl, fs, nvis, v0, slice, p.nv, p.k, keys_s, state_s, p.flags, whist);
     if (trace_out) sel.tr = trs + 16;
     LeanSmem& ls = *reinterpret_cast<LeanSmem*>(smem + GM::LS_OFF);
-    uint32_t* lhist = reinterpret_cast<uint32_t*>(smem + GM::LHIST_OFF);  // [CS][256] gathered histograms
+    uint32_t* lhist = reinterpret_cast<uint32_t*>(smem + GM::LHIST_OFF);  // [CS][128] gathered histograms (16-bit bin pairs)
     int stage = 0;
     if (!sel.trivial()) {
         if (!zero_early) {  // (the text rows' K buffer reached the private histograms)
@@ -769,32 +768,43 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         cta_sync();  // private histograms complete
         tc_fence_after();
         if (tid == 0) tstamp(27);
-        // threads 0..63 fold 4 bins of the 16 private histograms and push them to every peer
-        if (tid < 64) {
-            uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+        // threads 0..31 fold 8 bins of the 16 private histograms into 16-bit counts (a slice
+        // has <= 2048 rows, a unit <= 32768) and push them to every peer: 512 B per histogram
+        // (the all-gather's shared-memory port traffic, 2 x CS x 512 B, is on the chain)
+        if (tid < 32) {
+            uint32_t acc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
             for (int w = 0; w < FT / 32; ++w) {
-                const uint4 h = *reinterpret_cast<const uint4*>(whist + w * 256 + 4 * tid);
-                acc.x += h.x, acc.y += h.y, acc.z += h.z, acc.w += h.w;
+                const uint4 h0 = *reinterpret_cast<const uint4*>(whist + w * 256 + 8 * tid);
+                const uint4 h1 = *reinterpret_cast<const uint4*>(whist + w * 256 + 8 * tid + 4);
+                acc[0] += h0.x, acc[1] += h0.y, acc[2] += h0.z, acc[3] += h0.w;
+                acc[4] += h1.x, acc[5] += h1.y, acc[6] += h1.z, acc[7] += h1.w;
             }
-            const uint32_t dst = smem_u32(lhist + rank * 256 + 4 * tid), hb = smem_u32(&xbar[1]);
-            for (int q = 0; q < CS; ++q) st_async_u4(mapa_shared(dst, q), acc, mapa_shared(hb, q));
+            const uint4 pk = make_uint4(acc[0] | (acc[1] << 16), acc[2] | (acc[3] << 16), acc[4] | (acc[5] << 16),
+                                        acc[6] | (acc[7] << 16));
+            const uint32_t dst = smem_u32(lhist + rank * 128 + 4 * tid), hb = smem_u32(&xbar[1]);
+            for (int q = 0; q < CS; ++q) st_async_u4(mapa_shared(dst, q), pk, mapa_shared(hb, q));
         }
         if (warp == 0) {
-            // the threshold: bins 8 lane .. 8 lane + 7 summed over the CS histograms
+            // the threshold: bins 8 lane .. 8 lane + 7 summed over the CS histograms (16-bit
+            // halves summed in place: a unit's count fits)
             mbar_wait(smem_u32(&xbar[1]), 0);
             __syncwarp();
             if (lane == 0) tstamp(28);
-            uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, grp = 0u, own = 0u;
+            uint4 sm = make_uint4(0u, 0u, 0u, 0u), mine = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {  // 2 x 16 B per histogram, all loads independent
+            for (int q = 0; q < 16; ++q) {  // one 16-B load per histogram, all independent
                 if (q < CS) {
-                    const uint4 a = *reinterpret_cast<const uint4*>(lhist + q * 256 + 8 * lane);
-                    const uint4 b2 = *reinterpret_cast<const uint4*>(lhist + q * 256 + 8 * lane + 4);
-                    c[0] += a.x, c[1] += a.y, c[2] += a.z, c[3] += a.w;
-                    c[4] += b2.x, c[5] += b2.y, c[6] += b2.z, c[7] += b2.w;
+                    const uint4 a = *reinterpret_cast<const uint4*>(lhist + q * 128 + 4 * lane);
+                    sm.x += a.x, sm.y += a.y, sm.z += a.z, sm.w += a.w;
+                    if (q == rank) mine = a;
                 }
             }
+            uint32_t c[8] = {sm.x & 0xffffu, sm.x >> 16, sm.y & 0xffffu, sm.y >> 16,
+                             sm.z & 0xffffu, sm.z >> 16, sm.w & 0xffffu, sm.w >> 16};
+            const uint32_t cm[8] = {mine.x & 0xffffu, mine.x >> 16, mine.y & 0xffffu, mine.y >> 16,
+                                    mine.z & 0xffffu, mine.z >> 16, mine.w & 0xffffu, mine.w >> 16};
+            uint32_t grp = 0u, own = 0u;
 #pragma unroll
             for (int i = 0; i < 8; ++i) grp += c[i];
             uint32_t suf = grp;  // keys in bins >= 8 lane
@@ -818,10 +828,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             const int bstar = __shfl_sync(0xffffffffu, bl, lstar);
             above = __shfl_sync(0xffffffffu, above, lstar);
             // per-CTA counts of b*, and this CTA's rows above it
-            const uint32_t cq = (lane < CS) ? lhist[lane * 256 + bstar] : 0u;
+            const uint32_t cq = (lane < CS) ? ((lhist[lane * 128 + (bstar >> 1)] >> (16 * (bstar & 1))) & 0xffffu) : 0u;
             uint32_t maxc = cq, totc = cq;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) own += (8 * lane + i > bstar) ? lhist[rank * 256 + 8 * lane + i] : 0u;
+            for (int i = 0; i < 8; ++i) own += (8 * lane + i > bstar) ? cm[i] : 0u;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, off));
@@ -834,7 +844,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 ls.bc[1] = (uint32_t)p.k - above;  // keys still to keep inside b*
                 ls.bc[2] = (uint32_t)st;
                 ls.bc[3] = own;
-                ls.bc[4] = lhist[rank * 256 + bstar];
+                ls.bc[4] = (lhist[rank * 128 + (bstar >> 1)] >> (16 * (bstar & 1))) & 0xffffu;
                 // every CTA's (above, count) header + its candidates
                 if (st == 1) mbar_arrive_expect_tx(smem_u32(&xbar[2]), totc * 8u + (uint32_t)CS * 8u);
             }
@@ -879,7 +889,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         const int n0 = min(nA, capA);
         uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::LPT_OFF);
         uint16_t* ptl = pth + VCL * 16;
-        uint16_t* slot_of = reinterpret_cast<uint16_t*>(smem + GM::LSLOT_OFF);
         uint2* lsub = reinterpret_cast<uint2*>(smem + GM::LSUB_OFF);
         const uint32_t ubar_s = smem_u32(&xbar[3]), ubar_v = smem_u32(&xbar[4]);
         const unsigned lt = (1u << lane) - 1u;
@@ -889,6 +898,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             return dg > bstar ? 2 : (dg == bstar ? 1 : 0);
         };
         // P row = exp2(s2 - LSE2[h]) of heads h < g as split bf16 hi + lo (zero padded to 16 heads)
+        auto vaddr = [&](int r, int cc) -> uint32_t { return vst + (uint32_t)(r * GM::VROWB + cc * 16); };  // staging chunk
+        auto zero16 = [](uint32_t a) { asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(0u) : "memory"); };
         auto write_p_row = [&](int prow, const float (&v)[16]) {
             uint32_t hw[8], lw[8];
 #pragma unroll
@@ -937,50 +948,77 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         if (tid < CS)  // this CTA's header: (rows above b*, candidates)
             st_async_u2(mapa_shared(smem_u32(&ls.hdr[rank]), tid), make_uint2((uint32_t)na_loc, (uint32_t)nc_loc),
                         mapa_shared(smem_u32(&xbar[2]), tid));
-        // U3: slots, prefix counts for the emission, P rows, candidate pushes, V gathers
-#pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
-            const int c = 16 * j + warp;
-            if (c >= nch) break;
+        // U3: slots, prefix counts for the emission, P rows, candidate pushes, then the V
+        // gathers.  A warp's chunks are its TMEM stages (lane quarter warp % 4): their logits
+        // are loaded at once, one wait.
+        constexpr int CPW = 32 / NCP;  // chunks per warp (4 for g <= 8, 2 for g <= 16)
+        uint32_t lv[32];
+#pragma unroll
+        for (int m = 0; m < CPW; ++m) {
+            const int c = 16 * m + warp;
+            if (c < nch) {
+                const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (c >> 2) * UMMA_N;
+                if constexpr (NCP == 8) tmem_ld8_nowait(ta, lv + m * NCP);
+                else tmem_ld16_nowait_p(ta, lv + m * NCP);
+            }
+        }
+        tmem_wait_ld_tie(lv);
+        if (tid == 0) tstamp(57);
+        int gpre[CPW], gba[CPW], gbc[CPW];
+#pragma unroll
+        for (int m = 0; m < CPW; ++m) {
+            const int c = 16 * m + warp;
+            gba[m] = gbc[m] = 0;
+            gpre[m] = 0;
+            if (c >= nch) continue;
             const int r = 32 * c + lane;
             const uint32_t ck = (r < nvis) ? keys_s[r] : 0u;
             const uint32_t pre = __shfl_sync(0xffffffffu, (c & 1) ? ex1 : ex0, c >> 1);
             const int cl_ = (r < nvis) ? cls_of(ck) : 0;
             const unsigned ba = __ballot_sync(0xffffffffu, cl_ == 2), bc = __ballot_sync(0xffffffffu, cl_ == 1);
             const int preA = (int)(pre & 0xffffu), preC = (int)(pre >> 16);
+            gpre[m] = (int)pre, gba[m] = (int)ba, gbc[m] = (int)bc;
+            if ((ba | bc) == 0u) continue;  // (most chunks: nothing kept; U is issue-bound, 4 warps per SMSP)
             const int ia = preA + __popc(ba & lt), jc = preC + __popc(bc & lt);  // rows above / candidates before r
             int prow = -1;
-            uint16_t so = 0xffffu;
             if (cl_ == 2) {
                 att[ntext + ia] = r;
                 ls.ncb[ia] = (uint16_t)jc;
-                so = (uint16_t)(ntext + ia);
                 if (ntext + ia < capA) prow = ntext + ia;
             } else if (cl_ == 1) {
                 ls.attc[jc] = r;
                 ls.nab[jc] = (uint16_t)ia;
-                so = (uint16_t)(0x8000u | (uint32_t)jc);
                 prow = capA + jc;
                 const uint2 cv = make_uint2(ck, (uint32_t)(v0 + r));
                 const uint32_t dst = smem_u32(&ls.cand[rank][jc]), cb = smem_u32(&xbar[2]);
                 for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), cv, mapa_shared(cb, q));
             }
-            if (r < nvis) slot_of[r] = so;
-            if (__any_sync(0xffffffffu, prow >= 0)) {  // P rows from the logits in TMEM
+            if (prow >= 0) {  // P row from the logits
                 float v[16];
-                load_full(c >> 2, v);
-                if (prow >= 0) write_p_row(prow, v);
+#pragma unroll
+                for (int k2 = 0; k2 < 16; ++k2) v[k2] = (k2 < NCP) ? __uint_as_float(lv[m * NCP + (k2 < NCP ? k2 : 0)]) : 0.f;
+                write_p_row(prow, v);
             }
-            __syncwarp();  // this warp's att / attc entries
-            // V of this chunk's batch-0 above rows and candidates (consecutive slots)
-            const int a0 = ntext + preA, na_c = max(0, min(a0 + __popc(ba), capA) - a0), nc_c = __popc(bc);
+        }
+        __syncwarp();  // this warp's att / attc entries
+        if (tid == 0) tstamp(58);
+#pragma unroll
+        for (int m = 0; m < CPW; ++m) {  // V of each chunk's batch-0 above rows and candidates
+            const int preA = gpre[m] & 0xffff, preC = (int)((uint32_t)gpre[m] >> 16);
+            const int a0 = ntext + preA, na_c = max(0, min(a0 + __popc((unsigned)gba[m]), capA) - a0);
+            const int nc_c = __popc((unsigned)gbc[m]);
+#pragma unroll 2
             for (int e = lane; e < (na_c + nc_c) * CH; e += 32) {
                 const int k2 = e / CH, cc = e % CH;
                 const int dst = k2 < na_c ? a0 + k2 : capA + preC + (k2 - na_c);
                 const int rr = k2 < na_c ? att[a0 + k2] : ls.attc[preC + (k2 - na_c)];
-                cp_async16(vst + dst * GM::VROWB + cc * 16, Vb + (int64_t)(p.vb + v0 + rr) * p.vst + cc * 8, true);
+#if SVL_DEBUG_TRAP  // debug builds: a gathered row must be one of this CTA's visual rows, a slot inside the staging
+                if (rr < 0 || rr >= nvis || dst < 0 || dst >= VCL) __trap();
+#endif
+                cp_async16(vaddr(dst, cc), Vb + (int64_t)(p.vb + v0 + rr) * p.vst + cc * 8, true);
             }
         }
+        if (tid == 0) tstamp(59);
         // text rows' P (their V has been in flight since the LSE exchange)
         for (int i = tid; i < ntext * 16; i += FT) {
             const int rr = i >> 4, h = i & 15;
@@ -1001,9 +1039,10 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             }
             for (int i = tid; i < (npa + npc) * CH; i += FT) {
                 const int k2 = i / CH, rr = k2 < npa ? n0 + k2 : capA + nc_loc + (k2 - npa);
-                *reinterpret_cast<uint4*>(smem + GM::VST_OFF + rr * GM::VROWB + (i % CH) * 16) = make_uint4(0, 0, 0, 0);
+                zero16(vaddr(rr, i % CH));
             }
         }
+        if (tid == 0) tstamp(60);
         mbar_arrive(ubar_s);               // this thread's slots / P rows / prefix counts
         cp_async_mbar_arrive_noinc(ubar_v);  // ... and, once landed, its V copies
         SVL_TRACE(11);
@@ -1013,7 +1052,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             // segments: batch 0 (prepared by U), overflow batches (a CTA keeping more rows than
             // the staging holds), the candidates once the cut is known -- one P.V call site
             const int nover = nA > capA ? (nA - capA + capA - 1) / capA : 0;
-            float lsum[4] = {0.f, 0.f, 0.f, 0.f};  // warp 0: l[gid] in [0], l[gid + 8] in [2]
+            float ot[NT][4], lt_[NT][4];  // O^T fragments (d x heads) and, warp 0, l (every row)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) ot[nt][0] = ot[nt][1] = ot[nt][2] = ot[nt][3] = lt_[nt][0] = lt_[nt][1] = lt_[nt][2] = lt_[nt][3] = 0.f;
 #pragma unroll 1
             for (int sg = 0; sg <= nover + 1; ++sg) {
                 int row0 = 0, nr;
@@ -1028,14 +1069,20 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                     named_bar_sync(1, 256);  // the previous batch's P.V is done with the staging
                     for (int e = tid; e < n * CH; e += 256) {
                         const int sl = s0 + e / CH, cc = e % CH;
-                        cp_async16(vst + (sl - s0) * GM::VROWB + cc * 16, Vb + (int64_t)work_row(att[sl]) * p.vst + cc * 8,
-                                   true);
+#if SVL_DEBUG_TRAP
+                        if (att[sl] < 0 || att[sl] >= nvis) __trap();
+#endif
+                        cp_async16(vaddr(sl - s0, cc), Vb + (int64_t)work_row(att[sl]) * p.vst + cc * 8, true);
                     }
                     cp_async_commit();
                     for (int i = warp >> 2; i < nvs; i += 2) {  // P rows from TMEM (warp quarter = warp % 4)
-                        const int row = i * STAGE_ROWS + q4 * 32 + lane;
-                        const int sl = (row < nvis) ? (int)slot_of[row] : 0xffff;
-                        const int pr = (sl < 0x8000 && sl >= s0 && sl < s0 + n) ? sl - s0 : -1;
+                        // the row's virtual slot, recomputed as U assigned it (chunk prefix + ballot)
+                        const int row = i * STAGE_ROWS + q4 * 32 + lane, c = row >> 5;
+                        const uint32_t pre = __shfl_sync(0xffffffffu, (c & 1) ? ex1 : ex0, c >> 1);
+                        const bool above = row < nvis && cls_of(keys_s[row]) == 2;
+                        const unsigned ba = __ballot_sync(0xffffffffu, above);
+                        const int sl = ntext + (int)(pre & 0xffffu) + __popc(ba & lt);
+                        const int pr = (above && sl >= s0 && sl < s0 + n) ? sl - s0 : -1;
                         if (!__any_sync(0xffffffffu, pr >= 0)) continue;
                         float v[16];
                         load_full(i, v);
@@ -1045,9 +1092,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                         reinterpret_cast<uint4*>(pth + (n + (i >> 1)) * 16)[i & 1] = make_uint4(0u, 0u, 0u, 0u);
                         reinterpret_cast<uint4*>(ptl + (n + (i >> 1)) * 16)[i & 1] = make_uint4(0u, 0u, 0u, 0u);
                     }
-                    for (int i = tid; i < (nr - n) * CH; i += 256)
-                        *reinterpret_cast<uint4*>(smem + GM::VST_OFF + (n + i / CH) * GM::VROWB + (i % CH) * 16) =
-                            make_uint4(0, 0, 0, 0);
+                    for (int i = tid; i < (nr - n) * CH; i += 256) zero16(vaddr(n + i / CH, i % CH));
                     cp_async_wait<0>();
                     named_bar_sync(1, 256);
                 } else {
@@ -1067,37 +1112,48 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                     row0 = capA;
                     nr = candR;
                 }
-                // o += P[row0, row0 + nr) . V (warp w owns columns 16w..16w+15); warp 0 also
-                // l += P . 1.  Independent accumulator chains (hi / lo x column halves x even /
-                // odd k-tiles); the next tile's fragments are loaded before this tile's MMAs.
                 if (warp < D / 16 && nr > 0) {
+                    // O^T[d][h] += V^T . P, swap-AB: warp w owns d rows [16w, 16w + 16) as the MMA's M,
+                    // heads are N (8 per tile), so every MMA does useful work (heads as M would be half
+                    // zero rows for g <= 8).  Per 16-row k-tile: one ldmatrix.x4.trans of V (A = V^T)
+                    // and one of P (hi and lo B fragments), hi / lo x even / odd tiles in separate
+                    // accumulator chains, the next tile's fragments loaded before this tile's MMAs
+                    // (legacy mma.sync: 8 cycles per m16n8k16 per SMSP); warp 0 also l += ones . P.
                     const int mi = lane >> 3, rin = lane & 7;
-                    const uint32_t aph = smem_u32(pth) + ((mi >> 1) * 8 + rin) * 32 + (mi & 1) * 16;
-                    const uint32_t apl = smem_u32(ptl) + ((mi >> 1) * 8 + rin) * 32 + (mi & 1) * 16;
-                    const uint32_t avv = vst + ((mi & 1) * 8 + rin) * GM::VROWB + (2 * warp + (mi >> 1)) * 16;
+                    const uint32_t avv = vst + ((mi >> 1) * 8 + rin) * GM::VROWB + (2 * warp + (mi & 1)) * 16;
+                    const uint32_t apb = smem_u32((mi >> 1) ? ptl : pth) + ((mi & 1) * 8 + rin) * 32;
                     constexpr uint32_t ONES = 0x3f803f80u;  // bf16 (1, 1)
-                    float acc[2][6][4];
-#pragma unroll
-                    for (int a = 0; a < 2; ++a)
-#pragma unroll
-                        for (int b2 = 0; b2 < 6; ++b2) acc[a][b2][0] = acc[a][b2][1] = acc[a][b2][2] = acc[a][b2][3] = 0.f;
-                    uint32_t ph[4], pl[4], vv[4];
+                    const uint32_t ones4[4] = {ONES, ONES, ONES, ONES};
+                    uint32_t va[4], pb[NT][4];
                     auto ld = [&](int tb) {
-                        ldsm_x4_trans(aph + tb * 32, ph[0], ph[1], ph[2], ph[3]);
-                        ldsm_x4_trans(apl + tb * 32, pl[0], pl[1], pl[2], pl[3]);
-                        ldsm_x4_trans(avv + tb * GM::VROWB, vv[0], vv[1], vv[2], vv[3]);
+                        ldsm_x4_trans(avv + tb * GM::VROWB, va[0], va[1], va[2], va[3]);
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+                            ldsm_x4_trans(apb + tb * 32 + nt * 16, pb[nt][0], pb[nt][1], pb[nt][2], pb[nt][3]);
                     };
-                    auto step = [&](float (&A)[6][4], int tb) {
-                        const uint32_t hh[4] = {ph[0], ph[1], ph[2], ph[3]}, ll[4] = {pl[0], pl[1], pl[2], pl[3]};
-                        const uint32_t w0 = vv[0], w1 = vv[1], w2 = vv[2], w3 = vv[3];
+                    float acc[2][NT][4][4];  // [tile parity][nt][hi, lo, l hi, l lo]
+#pragma unroll
+                    for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) acc[a2][nt][c][0] = acc[a2][nt][c][1] = acc[a2][nt][c][2] = acc[a2][nt][c][3] = 0.f;
+                    auto step = [&](float (&A)[NT][4][4], int tb) {
+                        const uint32_t aa[4] = {va[0], va[1], va[2], va[3]};
+                        uint32_t bb[NT][4];
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) bb[nt][c] = pb[nt][c];
                         if (tb + 16 < row0 + nr) ld(tb + 16);
-                        mma_bf16_16816(A[0], hh, w0, w1);
-                        mma_bf16_16816(A[1], ll, w0, w1);
-                        mma_bf16_16816(A[2], hh, w2, w3);
-                        mma_bf16_16816(A[3], ll, w2, w3);
-                        if (warp == 0) {
-                            mma_bf16_16816(A[4], hh, ONES, ONES);
-                            mma_bf16_16816(A[5], ll, ONES, ONES);
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            mma_bf16_16816(A[nt][0], aa, bb[nt][0], bb[nt][1]);
+                            mma_bf16_16816(A[nt][1], aa, bb[nt][2], bb[nt][3]);
+                            if (warp == 0) {
+                                mma_bf16_16816(A[nt][2], ones4, bb[nt][0], bb[nt][1]);
+                                mma_bf16_16816(A[nt][3], ones4, bb[nt][2], bb[nt][3]);
+                            }
                         }
                     };
                     ld(row0);
@@ -1106,33 +1162,40 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                         if (tb + 16 < row0 + nr) step(acc[1], tb + 16);
                     }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        o[0][e] += (acc[0][0][e] + acc[0][1][e]) + (acc[1][0][e] + acc[1][1][e]);
-                        o[1][e] += (acc[0][2][e] + acc[0][3][e]) + (acc[1][2][e] + acc[1][3][e]);
-                        lsum[e] += (acc[0][4][e] + acc[0][5][e]) + (acc[1][4][e] + acc[1][5][e]);
-                    }
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            ot[nt][e] += (acc[0][nt][0][e] + acc[0][nt][1][e]) + (acc[1][nt][0][e] + acc[1][nt][1][e]);
+                            lt_[nt][e] += (acc[0][nt][2][e] + acc[0][nt][3][e]) + (acc[1][nt][2][e] + acc[1][nt][3][e]);
+                        }
                 }
             }
             SVL_TRACE(19);
-            // push the partial O (fragment pairs) and, from warp 0, the 16 denominators
+            // push O^T fragments: thread (gid, t) of warp w holds d = 16w + gid (+ 8), heads
+            // 8 nt + 2t (+ 1); the d-neighbour (gid + 1) is 4 lanes up -> float2 pairs along d.
+            // l: warp 0, lanes with gid == 0 hold l[8 nt + 2t], l[8 nt + 2t + 1].
             if (warp < D / 16) {
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
+                for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
-                        const int h = gid + 8 * hf;
-                        if (h < g) {
-                            const int i = h * D + warp * 16 + nt * 8 + 2 * t, q = i / per, jj = i - q * per;
-                            st_async_f2(mapa_shared(rcv_a + (uint32_t)(rank * per + jj) * 4u, q), o[nt][2 * hf],
-                                        o[nt][2 * hf + 1], mapa_shared(mrg_a, q));
+                    for (int e = 0; e < 4; ++e) {
+                        const float a0 = ot[nt][e], a1 = __shfl_down_sync(0xffffffffu, a0, 4);
+                        const int h = 8 * nt + 2 * t + (e & 1), d = 16 * warp + gid + 8 * (e >> 1);
+                        if ((gid & 1) == 0 && h < g) {
+                            const int i = h * D + d, q = i / per, jj = i - q * per;
+                            st_async_f2(mapa_shared(rcv_a + (uint32_t)(rank * per + jj) * 4u, q), a0, a1, mapa_shared(mrg_a, q));
                         }
                     }
-                if (warp == 0 && t == 0)
-                    for (int q = 0; q < CS; ++q) {
-                        st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + gid) * 4u, q), lsum[0], mapa_shared(mrg_a, q));
-                        st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + gid + 8) * 4u, q), lsum[2],
-                                     mapa_shared(mrg_a, q));
-                    }
+                if (warp == 0 && gid == 0)
+                    for (int q = 0; q < CS; ++q)
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {  // heads 8 hh + 2t + e (zero past the NT tiles)
+                                const float lv = (hh < NT) ? lt_[hh < NT ? hh : 0][e] : 0.f;
+                                st_async_f32(mapa_shared(lrcv_a + (uint32_t)(rank * 16 + 8 * hh + 2 * t + e) * 4u, q), lv,
+                                             mapa_shared(mrg_a, q));
+                            }
             }
             fin_threads = 256;
         } else {
@@ -1141,20 +1204,17 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             mbar_wait(smem_u32(&xbar[2]), 0);  // every CTA's header + candidates
             __syncwarp();
             if (ts == 0) tstamp(20);
-            for (int sl = ts; sl < CS * kFastCandPerCta; sl += 256) {  // one radix pass, key bits 19..12
-                const int q = sl / kFastCandPerCta, jc = sl % kFastCandPerCta;
-                if ((uint32_t)jc < ls.hdr[q].y) atomicAdd(&ls.rhist[(ls.cand[q][jc].x >> 12) & 255u], 1u);
-            }
+            const int cq_ = ts >> 4;  // 16 threads per peer's candidate list
+            const uint32_t ncq = (cq_ < CS) ? ls.hdr[cq_].y : 0u;
+            for (uint32_t jc = ts & 15; jc < ncq; jc += 16)  // one radix pass, key bits 19..12
+                atomicAdd(&ls.rhist[(ls.cand[cq_][jc].x >> 12) & 255u], 1u);
             named_bar_sync(2, 256);
             warp_find_nb<256>(ls.rhist, krem, ls.sbc[ws]);  // every S warp (no barrier)
             __syncwarp();
             const uint32_t bA = ls.sbc[ws][0], need = krem - ls.sbc[ws][1];  // keep `need` keys of sub-bin bA
-            for (int sl = ts; sl < CS * kFastCandPerCta; sl += 256) {
-                const int q = sl / kFastCandPerCta, jc = sl % kFastCandPerCta;
-                if ((uint32_t)jc < ls.hdr[q].y) {
-                    const uint2 cv = ls.cand[q][jc];
-                    if (((cv.x >> 12) & 255u) == bA) lsub[atomicAdd(&ls.nsub, 1u)] = cv;
-                }
+            for (uint32_t jc = ts & 15; jc < ncq; jc += 16) {
+                const uint2 cv = ls.cand[cq_][jc];
+                if (((cv.x >> 12) & 255u) == bA) lsub[atomicAdd(&ls.nsub, 1u)] = cv;
             }
             named_bar_sync(2, 256);
             const uint32_t nsub = ls.nsub;
@@ -1181,10 +1241,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 if (lane == 0) ls.kmask[0] = k0, ls.kmask[1] = k1;
             }
             uint32_t pc = 0u;
-            for (int sl = ts; sl < rank * kFastCandPerCta; sl += 256) {
-                const int q = sl / kFastCandPerCta, jc = sl % kFastCandPerCta;
-                if ((uint32_t)jc < ls.hdr[q].y) pc += kept_c(ls.cand[q][jc]);
-            }
+            if (cq_ < rank)
+                for (uint32_t jc = ts & 15; jc < ncq; jc += 16) pc += kept_c(ls.cand[cq_][jc]);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, off);
             if (lane == 0 && pc) atomicAdd(&ls.offc, pc);

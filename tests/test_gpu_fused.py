@@ -64,6 +64,24 @@ def test_fresh_step_gapped_bitexact(svl, orc):
     assert np.array_equal(idx.cpu().numpy(), oi)
 
 
+@pytest.mark.parametrize("k", [12288, 20000])
+def test_fresh_step_overflow_batches(svl, orc, k):
+    """Stage-1 split pipeline with more kept rows per CTA than its V staging holds (3/8 and
+    ~5/8 of 32k visual rows kept, gapped so the threshold bin stays small): the decode warps
+    run overflow batches (P rows re-read from TMEM) before the candidates; indices exact,
+    attention within tolerance."""
+    base = gen.CONFIGS["long-video"]
+    for gamma in (6.0, 10.0, 16.0):
+        wl = gen.DecodeWorkload(**{**base.__dict__, "name": "ovf", "k": k, "gap_gamma": gamma, "sinks": 0,
+                                   "needles": 0})
+        x = gen.make_decode_inputs(wl, seed=71, device="cpu")
+        oi, osc, gap = orc.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, k, nthreads=NTH)
+        if gap.min() > 1e-3:
+            break
+    frac, mx, rel, idx, oi2 = _run(svl, orc, wl, seed=71)
+    assert np.array_equal(idx, oi)
+
+
 @pytest.mark.parametrize("k", [0, 1, 2000])
 def test_fresh_step_k_edges_ragged(svl, orc, k):
     wl = gen.DecodeWorkload("fe", 3, 28, 4, 128, 19, 2000, 77, k, 1, 256)

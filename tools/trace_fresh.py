@@ -37,7 +37,8 @@ for j in range(64):
     if j in (0, 10, 30, 31):
         continue
     nz = tr[:, j] != 0
-    conv[nz, j] = (tr[nz, 0].double() + (tr[nz, j] - tr[nz, 30]).double() * ratio[nz]).round().long()
+    # (int64 offset first: ~1.8e18 ns does not survive a double addition below 256 ns)
+    conv[nz, j] = tr[nz, 0] + ((tr[nz, j] - tr[nz, 30]).double() * ratio[nz]).round().long()
 cyc_ratio = ratio
 tr, raw = conv, tr
 t0 = tr[:, 0].min()
@@ -61,8 +62,8 @@ for j, nm in post.items():
 
 lean = {26: "keys done", 27: "B1", 28: "w0: hists landed", 12: "U: B3+slots", 11: "U: V issued", 16: "D: V landed", 17: "D: PV above", 18: "D: cut recv", 19: "D: PV cands",
         20: "S: cands landed", 21: "S: cut", 22: "S: emitted", 6: "final sync", 23: "lred/octa",
-        24: "sync", 25: "lh", 56: "U1 (counts) + B3", 57: "U2 (scan)", 58: "U3 (slots, P, push)", 59: "U text P",
-        60: "S: cut seen (emit start)", 61: "S: peers' kept", 62: "S: own counts", 63: "S: offsets"}
+        24: "sync", 25: "lh", 56: "U1 (counts) + B3", 57: "U TMEM loads", 58: "U slots/P/push", 59: "U gathers",
+        60: "U text P + pads"}
 print("split pipeline (us from the threshold stamp, median / max over CTAs):")
 for j, nm in lean.items():
     col = tr[:, j]
