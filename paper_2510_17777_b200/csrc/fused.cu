@@ -44,6 +44,9 @@
 #ifndef SVL_TRACE_BUILD
 #define SVL_TRACE_BUILD 0
 #endif
+#ifndef SVL_EXP_NOPROW
+#define SVL_EXP_NOPROW 0  // timing experiment: U writes no P rows (wrong results)
+#endif
 #ifndef SVL_EXP_HOTONLY
 #define SVL_EXP_HOTONLY 0  // timing experiment: the stage-0/2 and overflow paths compiled out
 #endif
@@ -750,17 +753,27 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 }
             }
             tmem_wait_ld_tie(lv);
+            // the exponentials p = exp2(s2 - LSE2[h]) replace the logits in TMEM: they are the
+            // decode weights of the rows that get kept (U and the stage-0/2 path read them back)
 #pragma unroll
             for (int m = 0; m < NI; ++m) {
                 const int i = (warp >> 2) + 4 * m;
                 const int row = i * STAGE_ROWS + q4 * 32 + lane;
-                if (i < nvs && row < nvis) {
-                    float sc = 0.f;
+                float sc = 0.f;
 #pragma unroll
-                    for (int c = 0; c < NCP; ++c) sc += fast_exp2(__uint_as_float(lv[m * NCP + c]) * p.scale2 - nl[c]);
-                    sel.add_key(row, sc);
+                for (int c = 0; c < NCP; ++c) {
+                    const float pc = fast_exp2(__uint_as_float(lv[m * NCP + c]) * p.scale2 - nl[c]);
+                    lv[m * NCP + c] = __float_as_uint(pc);
+                    sc += pc;
+                }
+                if (i < nvs) {
+                    const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + i * UMMA_N;
+                    if constexpr (NCP == 8) tmem_st8_nowait(ta, lv + m * NCP);
+                    else tmem_st16_nowait(ta, lv + m * NCP);
+                    if (row < nvis) sel.add_key(row, sc);
                 }
             }
+            tmem_wait_st();
         }
         if (sel.nan_seen) raise_flag(p.flags, 2u /*NONFINITE*/);
         if (tid == 0) tstamp(26);
@@ -897,7 +910,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             const int dg = rel_digit(key);
             return dg > bstar ? 2 : (dg == bstar ? 1 : 0);
         };
-        // P row = exp2(s2 - LSE2[h]) of heads h < g as split bf16 hi + lo (zero padded to 16 heads)
+        // P row = exp2(s2 - LSE2[h]) of heads h < g (from TMEM) as split bf16 hi + lo, zero padded to 16 heads
         auto vaddr = [&](int r, int cc) -> uint32_t { return vst + (uint32_t)(r * GM::VROWB + cc * 16); };  // staging chunk
         auto zero16 = [](uint32_t a) { asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(0u) : "memory"); };
         auto write_p_row = [&](int prow, const float (&v)[16]) {
@@ -905,9 +918,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
 #pragma unroll
             for (int c2 = 0; c2 < 8; ++c2) {
                 hw[c2] = lw[c2] = 0u;
-                if (2 * c2 < NCP) {
-                    const float pa = fast_exp2(v[2 * c2] * p.scale2 - nl[2 * c2]);
-                    const float pb = fast_exp2(v[2 * c2 + 1] * p.scale2 - nl[2 * c2 + 1]);
+                if (2 * c2 < NCP) {  // (v = the exponentials the key pass left in TMEM)
+                    const float pa = v[2 * c2], pb = v[2 * c2 + 1];
                     hw[c2] = pack_bf16(pa, pb);
                     lw[c2] = pack_bf16(pa - bf16lo(hw[c2]), pb - bf16hi(hw[c2]));
                 }
@@ -964,12 +976,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         }
         tmem_wait_ld_tie(lv);
         if (tid == 0) tstamp(57);
-        int gpre[CPW], gba[CPW], gbc[CPW];
 #pragma unroll
         for (int m = 0; m < CPW; ++m) {
             const int c = 16 * m + warp;
-            gba[m] = gbc[m] = 0;
-            gpre[m] = 0;
             if (c >= nch) continue;
             const int r = 32 * c + lane;
             const uint32_t ck = (r < nvis) ? keys_s[r] : 0u;
@@ -977,7 +986,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             const int cl_ = (r < nvis) ? cls_of(ck) : 0;
             const unsigned ba = __ballot_sync(0xffffffffu, cl_ == 2), bc = __ballot_sync(0xffffffffu, cl_ == 1);
             const int preA = (int)(pre & 0xffffu), preC = (int)(pre >> 16);
-            gpre[m] = (int)pre, gba[m] = (int)ba, gbc[m] = (int)bc;
             if ((ba | bc) == 0u) continue;  // (most chunks: nothing kept; U is issue-bound, 4 warps per SMSP)
             const int ia = preA + __popc(ba & lt), jc = preC + __popc(bc & lt);  // rows above / candidates before r
             int prow = -1;
@@ -993,7 +1001,12 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 const uint32_t dst = smem_u32(&ls.cand[rank][jc]), cb = smem_u32(&xbar[2]);
                 for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), cv, mapa_shared(cb, q));
             }
-            if (prow >= 0) {  // P row from the logits
+            if (prow >= 0) {  // the row's V: its own lane issues the 16-B copies (no slot lookups)
+#pragma unroll
+                for (int cc = 0; cc < CH; ++cc)
+                    cp_async16(vaddr(prow, cc), Vb + (int64_t)(p.vb + v0 + r) * p.vst + cc * 8, true);
+            }
+            if (!SVL_EXP_NOPROW && prow >= 0) {  // P row from the exponentials in TMEM
                 float v[16];
 #pragma unroll
                 for (int k2 = 0; k2 < 16; ++k2) v[k2] = (k2 < NCP) ? __uint_as_float(lv[m * NCP + (k2 < NCP ? k2 : 0)]) : 0.f;
@@ -1002,22 +1015,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         }
         __syncwarp();  // this warp's att / attc entries
         if (tid == 0) tstamp(58);
-#pragma unroll
-        for (int m = 0; m < CPW; ++m) {  // V of each chunk's batch-0 above rows and candidates
-            const int preA = gpre[m] & 0xffff, preC = (int)((uint32_t)gpre[m] >> 16);
-            const int a0 = ntext + preA, na_c = max(0, min(a0 + __popc((unsigned)gba[m]), capA) - a0);
-            const int nc_c = __popc((unsigned)gbc[m]);
-#pragma unroll 2
-            for (int e = lane; e < (na_c + nc_c) * CH; e += 32) {
-                const int k2 = e / CH, cc = e % CH;
-                const int dst = k2 < na_c ? a0 + k2 : capA + preC + (k2 - na_c);
-                const int rr = k2 < na_c ? att[a0 + k2] : ls.attc[preC + (k2 - na_c)];
-#if SVL_DEBUG_TRAP  // debug builds: a gathered row must be one of this CTA's visual rows, a slot inside the staging
-                if (rr < 0 || rr >= nvis || dst < 0 || dst >= VCL) __trap();
-#endif
-                cp_async16(vaddr(dst, cc), Vb + (int64_t)(p.vb + v0 + rr) * p.vst + cc * 8, true);
-            }
-        }
         if (tid == 0) tstamp(59);
         // text rows' P (their V has been in flight since the LSE exchange)
         for (int i = tid; i < ntext * 16; i += FT) {
@@ -1324,7 +1321,8 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int c = 2 * c2 + e;
-                            pv2[e] = (c < NCP) ? fast_exp2(v[c] * p.scale2 - nl[c < NCP ? c : 0]) : 0.f;
+                            // (stage 2: the key pass left the exponentials in TMEM; stage 0: logits)
+                            pv2[e] = (c < NCP) ? (stage == 2 ? v[c] : fast_exp2(v[c] * p.scale2 - nl[c < NCP ? c : 0])) : 0.f;
                         }
                         hw[c2] = pack_bf16(pv2[0], pv2[1]);
                         lw[c2] = pack_bf16(pv2[0] - bf16lo(hw[c2]), pv2[1] - bf16hi(hw[c2]));
