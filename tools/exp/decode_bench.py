@@ -58,7 +58,13 @@ for _ in range(2000):  # ~1 s of copies: the SM clock ramps up from idle (a GEMM
     _b.copy_(_a)
 torch.cuda.synchronize()
 print("lib", svl.LIB_PATH, tag)
-run("long-video", [0, 16, -16, 8, 4])
-run("nvila-4k", [0, 16, 8])
-run("multi-turn", [0, -4, 4, 2])
-run("sweep", [0, -2, 2, 1])
+_cf = os.environ.get("DCFGS")
+if _cf is None:
+    run("long-video", [0, 16, -16, 8, 4])
+    run("nvila-4k", [0, 16, 8])
+    run("multi-turn", [0, -4, 4, 2])
+    run("sweep", [0, -2, 2, 1])
+else:  # e.g. DCFGS="long-video:0,16;nvila-4k:0"
+    for item in _cf.split(";"):
+        nm, pins = item.split(":")
+        run(nm, [int(v) for v in pins.split(",")])
