@@ -711,7 +711,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     // racecheck)
     cta_sync();
     gather_rows(0, ntext, 0);
-    cta_sync();
     SVL_TRACE(2);
     // per-thread copies of the normalisers (+inf pads: exp2(x - inf) = 0)
     float nl[NCP];
@@ -862,6 +861,21 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 if (st == 1) mbar_arrive_expect_tx(smem_u32(&xbar[2]), totc * 8u + (uint32_t)CS * 8u);
             }
         }
+        else {
+            // meanwhile (split pipeline) the text rows' P rows, exp2(s2 - LSE2[h]) as bf16 hi + lo
+            // -- they do not depend on the threshold (the stage-2 path rebuilds its own table)
+            uint16_t* pth = reinterpret_cast<uint16_t*>(smem + GM::LPT_OFF);
+            uint16_t* ptl = pth + GM::VCL * 16;
+            for (int i = tid - 32; i < ntext * 16; i += FT - 32) {
+                const int rr = i >> 4, h = i & 15;
+                float pv = 0.f;
+                if (h < g) pv = fast_exp2(txl[rr * NCP + h] - lse2[h]);
+                const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+                const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+                pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
+                ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
+            }
+        }
         cta_sync();  // threshold published
         stage = (int)ls.bc[2];
     }
@@ -933,12 +947,14 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         };
         // U1: per-chunk counts (chunk c = 32 rows; warp w owns chunks 16 j + w, which lie in
         // its TMEM lane quarter: stage c / 4, quarter c % 4 = w % 4)
-#pragma unroll 1
+        unsigned cba[4], cbc[4];  // this warp's chunks: rows above b*, candidates (reused by U3)
+#pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int c = 16 * j + warp, r = 32 * c + lane;
             const int cl_ = (c < nch && r < nvis) ? cls_of(keys_s[r]) : 0;
-            const unsigned ba = __ballot_sync(0xffffffffu, cl_ == 2), bc = __ballot_sync(0xffffffffu, cl_ == 1);
-            if (c < nch && lane == 0) ls.ccnt[c] = (uint32_t)__popc(ba) | ((uint32_t)__popc(bc) << 16);
+            cba[j] = __ballot_sync(0xffffffffu, cl_ == 2);
+            cbc[j] = __ballot_sync(0xffffffffu, cl_ == 1);
+            if (c < nch && lane == 0) ls.ccnt[c] = (uint32_t)__popc(cba[j]) | ((uint32_t)__popc(cbc[j]) << 16);
         }
         if (warp >= 8) {  // S: zero the resolve scratch (published by the barrier below)
             const int ts = tid - 256;
@@ -981,12 +997,12 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             const int c = 16 * m + warp;
             if (c >= nch) continue;
             const int r = 32 * c + lane;
-            const uint32_t ck = (r < nvis) ? keys_s[r] : 0u;
-            const uint32_t pre = __shfl_sync(0xffffffffu, (c & 1) ? ex1 : ex0, c >> 1);
-            const int cl_ = (r < nvis) ? cls_of(ck) : 0;
-            const unsigned ba = __ballot_sync(0xffffffffu, cl_ == 2), bc = __ballot_sync(0xffffffffu, cl_ == 1);
-            const int preA = (int)(pre & 0xffffu), preC = (int)(pre >> 16);
+            const unsigned ba = cba[m], bc = cbc[m];
             if ((ba | bc) == 0u) continue;  // (most chunks: nothing kept; U is issue-bound, 4 warps per SMSP)
+            const uint32_t pre = __shfl_sync(0xffffffffu, (c & 1) ? ex1 : ex0, c >> 1);
+            const int cl_ = ((ba >> lane) & 1u) ? 2 : (((bc >> lane) & 1u) ? 1 : 0);
+            const uint32_t ck = (cl_ == 1) ? keys_s[r] : 0u;
+            const int preA = (int)(pre & 0xffffu), preC = (int)(pre >> 16);
             const int ia = preA + __popc(ba & lt), jc = preC + __popc(bc & lt);  // rows above / candidates before r
             int prow = -1;
             if (cl_ == 2) {
@@ -1016,16 +1032,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         __syncwarp();  // this warp's att / attc entries
         if (tid == 0) tstamp(58);
         if (tid == 0) tstamp(59);
-        // text rows' P (their V has been in flight since the LSE exchange)
-        for (int i = tid; i < ntext * 16; i += FT) {
-            const int rr = i >> 4, h = i & 15;
-            float pv = 0.f;
-            if (h < g) pv = fast_exp2(txl[rr * NCP + h] - lse2[h]);
-            const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
-            const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
-            pth[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&hi);
-            ptl[rr * 16 + h] = *reinterpret_cast<const uint16_t*>(&lo);
-        }
+        // (the text rows' P rows were written while warp 0 found the threshold)
         // padding rows of the two regions: P = 0 and V = 0 (0 * stale NaN would poison P.V)
         {
             const int npa = ((n0 + 15) & ~15) - n0, npc = candR - nc_loc;
