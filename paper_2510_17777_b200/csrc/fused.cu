@@ -1213,9 +1213,35 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             for (uint32_t jc = ts & 15; jc < ncq; jc += 16)  // one radix pass, key bits 19..12
                 atomicAdd(&ls.rhist[(ls.cand[cq_][jc].x >> 12) & 255u], 1u);
             named_bar_sync(2, 256);
-            warp_find_nb<256>(ls.rhist, krem, ls.sbc[ws]);  // every S warp (no barrier)
-            __syncwarp();
-            const uint32_t bA = ls.sbc[ws][0], need = krem - ls.sbc[ws][1];  // keep `need` keys of sub-bin bA
+            // every S warp finds the sub-bin holding the krem-th key (registers only, no barrier):
+            // lane l holds bins 8l .. 8l + 7
+            uint32_t bA, need;
+            {
+                const uint4 h0 = *reinterpret_cast<const uint4*>(ls.rhist + 8 * lane);
+                const uint4 h1 = *reinterpret_cast<const uint4*>(ls.rhist + 8 * lane + 4);
+                const uint32_t cb[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                uint32_t grp = 0u;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) grp += cb[i];
+                uint32_t suf = grp;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t y = __shfl_down_sync(0xffffffffu, suf, off);
+                    if (lane + off < 32) suf += y;
+                }
+                const unsigned ball = __ballot_sync(0xffffffffu, suf >= krem);
+                const int lstar = ball ? 31 - __clz(ball) : 0;
+                uint32_t above = suf - grp, bl = 8u * lane;
+#pragma unroll
+                for (int i = 7; i >= 0; --i) {
+                    const bool hit = above + cb[i] >= krem;
+                    bl = hit ? 8u * lane + i : bl;
+                    above = hit ? above : above + cb[i];
+                    if (hit) break;
+                }
+                bA = __shfl_sync(0xffffffffu, bl, lstar);
+                need = krem - __shfl_sync(0xffffffffu, above, lstar);  // keep `need` keys of sub-bin bA
+            }
             for (uint32_t jc = ts & 15; jc < ncq; jc += 16) {
                 const uint2 cv = ls.cand[cq_][jc];
                 if (((cv.x >> 12) & 255u) == bA) lsub[atomicAdd(&ls.nsub, 1u)] = cv;
