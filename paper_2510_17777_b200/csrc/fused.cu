@@ -44,6 +44,12 @@
 #ifndef SVL_TRACE_BUILD
 #define SVL_TRACE_BUILD 0
 #endif
+#ifndef SVL_UGATHER_BULK
+#define SVL_UGATHER_BULK 1  // U's V rows as one bulk copy each (A/B: 0 = 16-B cp.async per chunk)
+#endif
+#ifndef SVL_EXP_NOVG
+#define SVL_EXP_NOVG 0  // timing experiment: U issues no V copies (wrong results)
+#endif
 #ifndef SVL_EXP_NOPROW
 #define SVL_EXP_NOPROW 0  // timing experiment: U writes no P rows (wrong results)
 #endif
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
             mbar_arrive_expect_tx(smem_u32(&xbar[1]), (uint32_t)(CS * 512));
             mbar_init(smem_u32(&xbar[2]), 1);  // top-k candidates (armed once their count is known)
             mbar_init(smem_u32(&xbar[3]), FT);  // split pipeline: every thread's slots / P rows
-            mbar_init(smem_u32(&xbar[4]), FT);  // ... and its V copies (cp.async arrivals)
+            mbar_init(smem_u32(&xbar[4]), SVL_UGATHER_BULK ? 2 * FT : FT);  // ... and its V copies
             {
                 const int items = g * D, per = (((items + CS - 1) / CS) + 1) & ~1;  // (as the merge)
                 const int mine = max(0, min(per, items - rank * per));
@@ -980,6 +986,7 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         // gathers.  A warp's chunks are its TMEM stages (lane quarter warp % 4): their logits
         // are loaded at once, one wait.
         constexpr int CPW = 32 / NCP;  // chunks per warp (4 for g <= 8, 2 for g <= 16)
+        uint32_t vbytes = 0u;          // (bulk-copy variant) this thread's V bytes in flight
         uint32_t lv[32];
 #pragma unroll
         for (int m = 0; m < CPW; ++m) {
@@ -1017,10 +1024,18 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 const uint32_t dst = smem_u32(&ls.cand[rank][jc]), cb = smem_u32(&xbar[2]);
                 for (int q = 0; q < CS; ++q) st_async_u2(mapa_shared(dst, q), cv, mapa_shared(cb, q));
             }
-            if (prow >= 0) {  // the row's V: its own lane issues the 16-B copies (no slot lookups)
+            if (!SVL_EXP_NOVG && prow >= 0) {
+#if SVL_UGATHER_BULK
+                // the row's V as one bulk copy (one L2 request stream per row instead of 16
+                // single-row 16-B requests per warp instruction), counted on ubar_v
+                bulk_g2s(vaddr(prow, 0), Vb + (int64_t)(p.vb + v0 + r) * p.vst, (uint32_t)ROWB, ubar_v);
+                vbytes += (uint32_t)ROWB;
+#else
+                // the row's V: its own lane issues the 16-B copies (no slot lookups)
 #pragma unroll
                 for (int cc = 0; cc < CH; ++cc)
                     cp_async16(vaddr(prow, cc), Vb + (int64_t)(p.vb + v0 + r) * p.vst + cc * 8, true);
+#endif
             }
             if (!SVL_EXP_NOPROW && prow >= 0) {  // P row from the exponentials in TMEM
                 float v[16];
@@ -1049,6 +1064,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         if (tid == 0) tstamp(60);
         mbar_arrive(ubar_s);               // this thread's slots / P rows / prefix counts
         cp_async_mbar_arrive_noinc(ubar_v);  // ... and, once landed, its V copies
+#if SVL_UGATHER_BULK
+        mbar_arrive_expect_tx(ubar_v, vbytes);  // (its bulk row copies: bytes counted on ubar_v)
+#endif
         SVL_TRACE(11);
 
         if (warp < 8) {
