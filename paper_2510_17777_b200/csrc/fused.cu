@@ -1276,8 +1276,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
                 }
                 if (rk == need - 1u) ls.cut = cv;
             }
+            // hand the cut to D at once (the writer arrives after its store), then S's own barrier
+            named_bar_arrive(3, 512);
             named_bar_sync(2, 256);
-            named_bar_arrive(3, 512);  // hand the cut to D
             if (ts == 0) tstamp(21);
             const uint2 cut = ls.cut;
             auto kept_c = [&](uint2 cv) { return cv.x > cut.x || (cv.x == cut.x && cv.y <= cut.y); };
