@@ -736,6 +736,9 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
     LeanSmem& ls = *reinterpret_cast<LeanSmem*>(smem + GM::LS_OFF);
     uint32_t* lhist = reinterpret_cast<uint32_t*>(smem + GM::LHIST_OFF);  // [CS][128] gathered histograms (16-bit bin pairs)
     int stage = 0;
+    // the key pass's exponentials of this warp's stages (= U3's chunks 16 m + warp), kept in
+    // registers for the split pipeline's P rows
+    uint32_t lv[32];
     if (!sel.trivial()) {
         if (!zero_early) {  // (the text rows' K buffer reached the private histograms)
             sel.zero_hist();
@@ -747,7 +750,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         {
             constexpr int NI = kFusedSliceMax / NT / STAGE_ROWS / (FT / 128);  // stages per warp
             static_assert(NI * NCP == 32, "32 logit registers per thread");
-            uint32_t lv[32];
 #pragma unroll
             for (int m = 0; m < NI; ++m) {
                 const int i = (warp >> 2) + 4 * m;
@@ -987,17 +989,6 @@ __global__ void __launch_bounds__(FT, 1) fresh_kernel(const __grid_constant__ Fr
         // are loaded at once, one wait.
         constexpr int CPW = 32 / NCP;  // chunks per warp (4 for g <= 8, 2 for g <= 16)
         uint32_t vbytes = 0u;          // (bulk-copy variant) this thread's V bytes in flight
-        uint32_t lv[32];
-#pragma unroll
-        for (int m = 0; m < CPW; ++m) {
-            const int c = 16 * m + warp;
-            if (c < nch) {
-                const uint32_t ta = tbase + ((uint32_t)(q4 * 32) << 16) + (c >> 2) * UMMA_N;
-                if constexpr (NCP == 8) tmem_ld8_nowait(ta, lv + m * NCP);
-                else tmem_ld16_nowait_p(ta, lv + m * NCP);
-            }
-        }
-        tmem_wait_ld_tie(lv);
         if (tid == 0) tstamp(57);
 #pragma unroll
         for (int m = 0; m < CPW; ++m) {
