@@ -34,6 +34,13 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef SVL_OWNER_T
+#define SVL_OWNER_T 1  // cluster merge: threads per owned item (measured: 1 -> 9.49 to 8.53 us at long-video)
+#endif
+#ifndef SVL_EXP_NOOWNER
+#define SVL_EXP_NOOWNER 0  // timing experiment: the cluster merge's owner loop skipped (no output)
+#endif
+
 namespace svl {
 
 namespace {
@@ -456,9 +463,9 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         __syncwarp();
         stamp(8);
         const int i0 = split * per, ni = max(0, min(per, items - i0));
-        int T = 32;
-        while (T > 1 && T * ni > 2 * NTH) T >>= 1;
-        for (int jb = 0; jb < ni; jb += NTH / T) {
+        int T = SVL_OWNER_T;  // threads per owned item (measured: 1 pass over the items with few
+        while (T > 1 && T * ni > NTH) T >>= 1;  // threads each beats wide xor trees)
+        for (int jb = 0; jb < (SVL_EXP_NOOWNER ? 0 : ni); jb += NTH / T) {
             const int j = jb + tid / T, sub = tid & (T - 1);
             const int h = (j < ni) ? (i0 + j) / D : 0;
             float M = -INFINITY;
