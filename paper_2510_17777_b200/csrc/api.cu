@@ -937,13 +937,20 @@ static bool fresh_plan(int B, int Hkv, int g, int nv, int capacity, int& CS, int
     if (const int v = (int)(flags >> 24)) {  // SVL_PIN_SPLITS(8 or 16)
         if ((v == 8 || v == 16) && v >= c) CS = v, pinned = true;
     }
-    // The fused kernel only while every unit's cluster is co-resident (one wave).  Beyond
-    // that the two-call kernels, which spread over every SM, are faster (measured, us/layer
-    // fused vs two-call: 32k B=2 56.8 vs 50.7, 16k B=4 67.2 vs 52.4, 4k B=8 55.9 vs 38.9;
-    // B=1: 32k 28.1 vs 34.2, 4k 17.3 vs 23.6)
+    // The fused kernel while every unit's cluster is co-resident (one wave), or -- 16-CTA
+    // clusters over long slices -- up to three waves; beyond that the two-call kernels, which
+    // spread over every SM, are faster (round 1, us/layer fused vs two-call: 16k B=4 67.2 vs
+    // 52.4, 4k B=8 55.9 vs 38.9; B=1: 32k 28.1 vs 34.2, 4k 17.3 vs 23.6; round 3 below)
     if (!pinned) {
         const int mac = fresh_max_active_clusters(d, g, CS);
-        if (mac <= 0 || units > mac) return false;
+        if (mac <= 0) return false;
+        if (units > mac) {
+            // several waves of clusters: still ahead of the two calls while a unit's slice is long
+            // (round 3, us/layer fused vs two-call: 32k visual B = 3 / 4 / 5: 49.4 / 71.8 / 74.7 vs
+            // 56.2 / 76.8 / 91.0; 24k B = 4: 63.8 vs 66.0; 16k B = 4 / 6: 55.6 / 74.5 vs 49.0 / 58.1)
+            const int waves = (units + mac - 1) / mac;
+            if (!(CS == 16 && (nv + CS - 1) / CS >= 1536 && waves <= 3)) return false;
+        }
     }
     slice = (nv + CS - 1) / CS;
     if (slice > smax) return false;

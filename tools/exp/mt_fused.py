@@ -28,11 +28,12 @@ def run(wl, nl, flags):
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / 100 / nl
 base = gen.CONFIGS["long-video"]
-for name, wl, nl in [("multi-turn", gen.CONFIGS["multi-turn"], 28),
-                     ("lv B2", gen.DecodeWorkload(**{**base.__dict__, "name": "b2", "B": 2, "seq_lens": None}), 14),
-                     ("lv B4", gen.DecodeWorkload(**{**base.__dict__, "name": "b4", "B": 4, "seq_lens": None}), 7)]:
+def mk(B, nv):
+    return gen.DecodeWorkload(**{**base.__dict__, "name": f"b{B}n{nv}", "B": B, "nv": nv, "k": nv // 10, "seq_lens": None})
+for name, wl, nl in [("lv B3", mk(3, 32768), 10), ("lv B4", mk(4, 32768), 7), ("24k B4", mk(4, 24576), 9),
+                     ("16k B4", mk(4, 16384), 14), ("16k B6", mk(6, 16384), 10), ("32k B5", mk(5, 32768), 6)]:
     res = {}
-    for tag, fl in [("planner", 0), ("fused16", svl.SVL_PIN_SPLITS(16)), ("fused8", svl.SVL_PIN_SPLITS(8)), ("unfused", svl.SVL_FRESH_UNFUSED)]:
+    for tag, fl in [("planner", 0), ("fused16", svl.SVL_PIN_SPLITS(16)), ("unfused", svl.SVL_FRESH_UNFUSED)]:
         try:
             res[tag] = round(run(wl, nl, fl), 2)
         except Exception as e:
