@@ -247,3 +247,18 @@ def test_pack_host_validation(svl, case, status):
         args["Vp"] = _kv(cap=61)
     rc = L.svl_pack_kv(*args.values())
     assert rc == status, (rc, L.svl_last_error_message())
+
+
+@pytest.mark.gpu
+def test_fresh_plan_multi_wave_rule():
+    """The fresh-step planner (svl_fresh_decode_plan, host only): one wave of 16-CTA clusters,
+    or up to three over slices >= 1536 rows; two calls beyond (or over short slices).  Needs
+    the device's co-resident cluster count, so it is skipped without a GPU."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs the device's cluster occupancy")
+    from paper_2510_17777_b200 import svl
+    lib = svl.lib()
+    plan = lambda B, nv: lib.svl_fresh_decode_plan(B, 28, 4, 128, nv, nv + 1024, 0)
+    assert plan(1, 32768) == 1 and plan(3, 32768) == 1 and plan(5, 32768) == 1
+    assert plan(8, 16384) == 0 and plan(16, 65536) == 0

@@ -159,11 +159,12 @@ def test_fresh_step_deterministic(svl):
 
 
 @pytest.mark.parametrize("pin", [None, "16"])
-@pytest.mark.parametrize("B,nv", [(2, 32768), (8, 32768), (8, 24576)])
+@pytest.mark.parametrize("B,nv", [(2, 32768), (3, 32768), (5, 24576), (8, 32768), (8, 24576)])
 def test_fresh_step_many_units(svl, orc, B, nv, pin):
     """More clusters than fit at once (later clusters start on SMs vacated by earlier
     ones): this exposed the text-row / ring-slot parity race fixed in fused.cu (the
-    text rows now have their own buffer and barrier); run twice back to back."""
+    text rows now have their own buffer and barrier); run twice back to back.  B = 3 at 32k
+    and B = 5 at 24k take the fused kernel unpinned (the planner's up-to-three-wave rule)."""
     # pin: force the fused kernel into a multi-wave launch (the planner would take two calls)
     xf = svl.SVL_PIN_SPLITS(int(pin)) if pin else 0
     base = gen.CONFIGS["long-video"]
