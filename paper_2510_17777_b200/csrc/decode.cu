@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         }
     }
     cta_sync();
+    stamp(10);
     if (tid < 16) {  // CTA max, warp scales and sum of head tid (fixed warp order)
         float M = -INFINITY;
 #pragma unroll
@@ -447,7 +448,9 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         const int items = p.g * D, per = (items + S - 1) / S;
         float* rcv = reinterpret_cast<float*>(smem + SM::RCV_OFF);  // [S][per]
         float* rml = reinterpret_cast<float*>(smem + SM::RML_OFF);  // [S][33]: M[16], l[16], pad
+        stamp(11);
         cluster_wait();  // every peer has armed its barrier
+        stamp(12);
         const uint32_t rcv_a = smem_u32(rcv), rml_a = smem_u32(rml);
         for (int i = tid; i < items; i += NTH) {
             const int q = i / per;

@@ -47,6 +47,7 @@ tr = tr[tr[:, 0] > 0]
 f_ghz = ((tr[:, 7] - tr[:, 0]).double() / (tr[:, 15] - tr[:, 14]).double())
 print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {f_ghz.median() * 1e3:.0f} MHz")
 names = {1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 4: "compute done",
+         10: "O staged (cross-warp)", 11: "CTA M / l", 12: "cluster_wait",
          5: "partial stored/pushed", 8: "partials landed", 9: "merged", 7: "end"}
 print(f"{name} decode pin={pin}: {tr.shape[0]} CTAs; per-CTA cycles from its start -> us at its clock "
       f"(min / median / max); kernel span {((tr[:, 15].max() - tr[:, 14].min()) / 1e3).item():.2f} us")
