@@ -10,30 +10,34 @@
 //
 // One thread-block cluster (CS <= 16 CTAs, distributed shared memory) per
 // unit (b, KV group G); CTA r owns visual rows [r*slice, (r+1)*slice) and a
-// 1/CS share of the text rows.  Per CTA: 1 TMA producer warp, 8 consumer
-// warps, 7 helper warps (512 threads), 216 KB of shared memory.
-//   1. stream: the TMA warp streams the CTA's K rows (visual slice, then text
-//      share) with cp.async.bulk into a 4 x 32 KB mbarrier ring; the consumer
-//      warps turn every 16-row tile into the base-2 logits of all g heads with
-//      mma.sync (swap-AB, permuted contraction) kept in shared memory, plus a
-//      running (max, sum) per head.  The text rows' V gather starts as soon as
-//      the ring drains.
-//   2. LSE: (max, sum) partials pushed to every peer over DSMEM; one cluster
-//      barrier; every CTA folds the same 16 partials -> identical LSE2[h].
-//   3. top-k (two cluster barriers): relevance keys + a 256-bin value-adaptive
-//      histogram, all-gathered; the threshold bin b*; the V gather of every row
-//      at or above b* is issued right away (a superset of the kept rows); the
-//      keys of b* are all-gathered in index order and resolved locally (one
-//      8-bit radix pass + exact ranking inside the last bin, ties to the lower
-//      index).  A generic exact radix (select_push.cuh) handles massive ties.
-//   4. decode: weights p = exp2(s2 - LSE2[h]) relative to the GLOBAL
-//      normaliser (identical in every CTA, so the merge needs no rescaling),
-//      tabulated once as split bf16 hi + lo; warp w owns output columns
-//      [16w, 16w+16) (ldmatrix.trans P and V fragments, mma.sync) -- no
-//      cross-warp reduction.
-//   5. merge: plain sums of (O, l) over the cluster -> out fp32, lse.
-// HBM traffic per unit: visual K + text K once + kept V + text V (+ the V of
-// the few non-kept keys of the threshold bin).
+// 1/CS share of the text rows.  512 threads, 226 KB of shared memory, 512 TMEM
+// columns per CTA.
+//   1. stream: one thread issues 128-row TMA stages (128-B swizzle) into a ring;
+//      d is split between tcgen05.mma (logits in TMEM) and mma.sync on warps
+//      8-15; warps 4-7 fold a running (max, sum) per head.
+//   2. LSE: (max, sum) partials pushed to every peer over DSMEM (st.async);
+//      every CTA folds the same partials -> identical LSE2[h].
+//   3. key pass: relevance = sum over the g heads of exp2(s2 - LSE2[h]) (the
+//      exponentials are written back over the logits: they are the decode
+//      weights), per-warp 256-bin value-adaptive histograms folded into 16-bit
+//      counts and all-gathered; warp 0 finds the threshold bin b*.
+//   4. split pipeline (stage 1: no CTA holds more than 64 keys of b*):
+//      U, all warps: slots in index order for the rows above b* and the keys of
+//        b* (candidates), P rows (bf16 hi + lo), one bulk V copy per row,
+//        candidates pushed to every peer;
+//      D, warps 0-7: swap-AB mma.sync P.V over the text + above rows as their V
+//        lands (overflow batches if a CTA keeps more rows than its staging),
+//        then over the candidates the cut keeps; O and l pushed from registers
+//        to the owning peers;
+//      S, warps 8-15: exact cut among the gathered candidates (one radix pass on
+//        key bits 19..12, exact rank inside the cut sub-bin, ties to the lower
+//        index) handed to D, then this CTA's kept indices, ascending.
+//      Stage 2 (massive ties) / stage 0 (k <= 0 or k >= N_v): the generic exact
+//      cluster radix (select_push.cuh) and the batched decode.
+//   5. merge: every owner sums its items over the cluster -> out fp32, lse.
+// The weights are relative to the GLOBAL normaliser (identical in every CTA),
+// so the merge is a plain sum.  HBM traffic per unit: visual K + text K once +
+// kept V + text V (+ the V of the cut-bin keys the cut drops).
 #include <cooperative_groups.h>
 #include <stdlib.h>
 
