@@ -82,6 +82,16 @@ def test_fresh_step_overflow_batches(svl, orc, k):
     assert np.array_equal(idx, oi)
 
 
+@pytest.mark.parametrize("kfrac", [0.5, 0.97, "nv-1"])
+def test_fresh_step_large_k(svl, orc, kfrac):
+    """Most of the visual rows kept (the threshold bin near the bottom of the value range;
+    above-b* rows overflow the staging): indices by the gap rule, attention within tolerance."""
+    base = gen.CONFIGS["nvila-4k"]
+    k = base.nv - 1 if kfrac == "nv-1" else int(base.nv * kfrac)
+    wl = gen.DecodeWorkload(**{**base.__dict__, "name": "lk", "k": k})
+    _run(svl, orc, wl, seed=81, k=k)
+
+
 @pytest.mark.parametrize("k", [0, 1, 2000])
 def test_fresh_step_k_edges_ragged(svl, orc, k):
     wl = gen.DecodeWorkload("fe", 3, 28, 4, 128, 19, 2000, 77, k, 1, 256)
