@@ -37,6 +37,9 @@
 #ifndef SVL_OWNER_T
 #define SVL_OWNER_T 1  // cluster merge: threads per owned item (measured: 1 -> 9.49 to 8.53 us at long-video)
 #endif
+#ifndef SVL_L2OWNER_T
+#define SVL_L2OWNER_T 4  // L2 merge (S > 16): threads per owned item (at most; measured S = 37: 32 -> 10.35, 4 -> 9.59 us)
+#endif
 #ifndef SVL_EXP_NOOWNER
 #define SVL_EXP_NOOWNER 0  // timing experiment: the cluster merge's owner loop skipped (no output)
 #endif
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             stamp(8);
             // per item: T threads (a power of two <= 32) stride over the splits -- max, then the
             // weighted sums of o and l -- with fixed xor trees inside the T-lane group
-            int T = 32;
+            int T = SVL_L2OWNER_T;
             while (T > 1 && T * ni > 2 * NTH) T >>= 1;
             for (int jb = 0; jb < ni; jb += NTH / T) {
                 const int j = jb + tid / T, sub = tid & (T - 1);
