@@ -124,16 +124,27 @@ static RetrieveTcLayout retrieve_tc_layout(int B, int n_q, int H, int Hkv, int d
 // Splits per unit.  The grid (units x S CTAs) never exceeds the co-resident CTA
 // count (the split merge is a grid-wide barrier), so S = floor(SMs * occ / units)
 // for occ in {1, 2} CTAs per SM, at least kDecodeMinRows attended rows per CTA;
-// of the two the one with the smaller per-SM row load (ties: more CTAs); <= 16 splits run
-// as one thread-block cluster per unit (DSMEM merge), more as a co-resident grid (L2 merge).
+// of the two the one with the smaller per-SM row load (ties: more CTAs); see plan_decode for
+// the merge path (cluster over DSMEM or co-resident grid over L2).
 constexpr int kDecodeMinRows = 32;
 #ifndef SVL_DECODE_OCC
 #define SVL_DECODE_OCC 2  // (the kernel's shared memory allows one CTA per SM today)
 #endif
 static int decode_slots(int d) { return device_sm_count() * std::max(1, decode_ctas_per_sm(d)); }
 
-static int plan_splits(int units, int n_att_max, int d, uint32_t flags) {
-    if (const int pin = (int)(flags >> 24)) return pin;
+// Split count S and merge path of the steady decode.  S <= 16 splits may run as one
+// S-CTA cluster per unit merging over DSMEM, but only while every unit's cluster is
+// co-resident: clusters that do not fit run as a second wave (measured long-video, us/layer:
+// B = 3 as 12-CTA clusters 19.5 vs grid merge 13.5; B = 4 as 8-CTA clusters 22.5 vs grid
+// merge at S = 9 15.0).  Past the co-resident cluster count the same S merges through L2.
+struct DecodePlan {
+    int S;
+    int cluster;
+};
+
+static DecodePlan plan_decode(int units, int n_att_max, int d, uint32_t flags) {
+    const bool grid_only = (flags & SVL_DECODE_GRID_MERGE) != 0;
+    if (const int pin = (int)(flags >> 24)) return {pin, (pin > 1 && pin <= 16 && !grid_only) ? 1 : 0};
     const int sms = device_sm_count();
     const int occ_max = std::min(SVL_DECODE_OCC, std::max(1, decode_ctas_per_sm(d)));
     const int smax = std::max(1, n_att_max / kDecodeMinRows);
@@ -150,11 +161,18 @@ static int plan_splits(int units, int n_att_max, int d, uint32_t flags) {
             bestS = S;
         }
     }
-    // few units (<= 7 co-resident clusters of 16): one 16-CTA cluster per unit merging over
-    // DSMEM beats spreading the unit over more SMs with the L2 merge (measured, us/layer:
+    if (bestS <= 1) return {1, 0};
+    if (grid_only) return {bestS, 0};
+    // few units: one 16-CTA cluster per unit merging over DSMEM beats spreading the unit over
+    // more SMs with the L2 merge while the clusters are co-resident (measured, us/layer:
     // long-video 9.65 vs 10.37 at S = 37, nvila-4k 7.32 vs 8.69)
-    if (bestS > 16 && units * 16 <= 7 * 16 && !(flags & SVL_DECODE_GRID_MERGE)) bestS = std::min(16, smax);
-    return bestS;
+    if (bestS > 16) return units <= decode_max_active_clusters(d, 16) ? DecodePlan{16, 1} : DecodePlan{bestS, 0};
+    if (units <= decode_max_active_clusters(d, bestS)) return {bestS, 1};
+    // a slightly narrower cluster that fits in one wave still beats the L2 merge (B = 3:
+    // 8-CTA clusters 12.0 vs grid merge at S = 12 13.5)
+    for (int S2 = bestS - 1; 3 * S2 >= 2 * bestS && S2 > 1; --S2)
+        if (units <= decode_max_active_clusters(d, S2)) return {S2, 1};
+    return {bestS, 0};
 }
 
 static size_t decode_ws_bytes(int units, int S, int d) {
@@ -629,7 +647,7 @@ size_t svl_sparse_decode_workspace_size(int32_t B, int32_t H, int32_t Hkv, int32
     if (B < 1 || Hkv < 1 || H % Hkv || capacity < 1 || k < 0 || visual_len < 0) return 0;
     const int n_att_max = std::max(1, k + std::max(0, capacity - visual_len));
     const int units = B * Hkv;
-    return decode_ws_bytes(units, plan_splits(units, n_att_max, d, flags), d);
+    return decode_ws_bytes(units, plan_decode(units, n_att_max, d, flags).S, d);
 }
 
 struct PushArgs {
@@ -671,10 +689,10 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
 
     const int units = B * Hkv;
     const int n_att_max = std::max(1, k + std::max(0, K.capacity - span.visual_len));
-    const int S = plan_splits(units, n_att_max, d, flags);
-    // <= 16 splits: the unit's CTAs form one cluster and merge over DSMEM (no co-residency
-    // requirement across units); more: the grid merge through L2 (co-resident grid)
-    const int cluster = (S > 1 && S <= 16 && !(flags & SVL_DECODE_GRID_MERGE)) ? 1 : 0;
+    const DecodePlan plan = plan_decode(units, n_att_max, d, flags);
+    const int S = plan.S;
+    // cluster: the unit's S CTAs merge over DSMEM; else the grid merge through L2 (co-resident grid)
+    const int cluster = plan.cluster;
     if (S > 1 && !cluster && ((long)units * S > decode_slots(d) || units > kWsEpochs))
         return fail(SVL_ERR_UNSUPPORTED, "pinned split count: B*Hkv*n exceeds the co-resident CTA count%s");
     if (ws_bytes < decode_ws_bytes(units, S, d)) return fail(SVL_ERR_WORKSPACE, "workspace too small%s");

@@ -702,7 +702,42 @@ int decode_ctas_per_sm_t() {
     return n;
 }
 
+template <int D>
+int decode_max_active_clusters_t(int S) {
+    using SM = DecodeSmem<D, 3>;
+    if (prepare_decode_t<D, 3>() != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(S, 1, 1);
+    cfg.blockDim = dim3(NTH, 1, 1);
+    cfg.dynamicSmemBytes = SM::BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, decode_kernel<D, 3>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 }  // namespace
+
+int decode_max_active_clusters(int d, int S) {
+    static int cache[64][2][17] = {};
+    int dev = 0;
+    if (S < 1 || S > 16 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    int& c = cache[dev][d == 128][S];
+    if (c == 0) {
+        c = (d == 128) ? decode_max_active_clusters_t<128>(S) : decode_max_active_clusters_t<64>(S);
+        if (c <= 0) c = -1;
+    }
+    return c;
+}
 
 cudaError_t launch_wait_flags(const uint32_t* flags, int P, uint32_t epoch, uint32_t* ws_flags, cudaStream_t s) {
     wait_flags_kernel<<<1, 32, 0, s>>>(flags, P, epoch, ws_flags);

@@ -89,6 +89,7 @@ template <int D>
 constexpr int kDecodePartStride = 16 * D + 32;  // o [16][D], M [16], l [16] (64-bit tagged fp32)
 constexpr int kDecodeMaxSplits = 256;           // splits per unit (merge staging: S * slice <= g D + S)
 int decode_ctas_per_sm(int d);                  // co-resident decode CTAs per SM
+int decode_max_active_clusters(int d, int S);   // co-resident S-CTA decode clusters (<= 0: none)
 cudaError_t launch_wait_flags(const uint32_t* flags, int P, uint32_t epoch, uint32_t* ws_flags, cudaStream_t s);
 
 struct FreshParams {

@@ -98,3 +98,31 @@ def test_decode_pin_too_many_splits_rejected(svl):
         svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, 2048, idx,
                                flags=svl.SVL_PIN_SPLITS(255))
     assert e.value.status == 5  # SVL_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("B", [2, 3, 4, 6])
+def test_decode_planner_batch_sweep_matches_oracle(svl, orc, B):
+    """Planner defaults at B*Hkv = 8..24 units: where the S-CTA clusters are not all
+    co-resident the planner narrows the cluster or switches to the L2 merge (api.cu
+    plan_decode); whichever path runs must match the oracle and rerun bitwise."""
+    base = gen.CONFIGS["long-video"]
+    wl = gen.DecodeWorkload(**{**base.__dict__, "name": f"lvB{B}", "B": B, "nv": 4096, "k": 1024,
+                               "seq_lens": None})
+    cpu = gen.make_decode_inputs(wl, seed=90 + B)
+    g = torch.Generator().manual_seed(B)
+    oi = torch.stack([torch.stack([torch.sort(torch.randperm(wl.nv, generator=g)[:wl.k])[0]
+                                   for _ in range(wl.Hkv)]) for _ in range(B)]).to(torch.int32).numpy()
+    oo, ol = orc.sparse_decode(cpu["q_dec"], cpu["K"], cpu["V"], cpu["seq_len"], wl.vb, wl.nv, oi, nthreads=NTH)
+    dev = {kk: v.cuda() for kk, v in cpu.items()}
+    idx = torch.as_tensor(oi).cuda()
+    ws = svl.Workspace()
+    lse = torch.empty(wl.B, wl.H, device="cuda")
+    a, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                  lse_out=lse, ws=ws)
+    a, lse_a = a.clone(), lse.clone()
+    b, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
+                                  lse_out=lse, ws=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(lse_a, lse)
+    parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)
+    assert ws.flags() == 0

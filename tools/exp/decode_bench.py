@@ -7,7 +7,11 @@ from paper_2510_17777_b200 import inputs as gen, svl
 import bench
 
 def run(name, pins, layers=28, steps=200):
-    wl = gen.CONFIGS[name]
+    if name.startswith("lvB"):  # long-video at batch B (e.g. lvB2)
+        base = gen.CONFIGS["long-video"]
+        wl = gen.DecodeWorkload(**{**base.__dict__, "name": name, "B": int(name[3:]), "seq_lens": None})
+    else:
+        wl = gen.CONFIGS[name]
     nl = layers if name != "sweep" else 3
     xs = [gen.make_decode_inputs(wl, seed=500 + l, device="cuda") for l in range(nl)]
     idx = [torch.sort(torch.stack([torch.stack([torch.randperm(wl.nv, device="cuda")[:wl.k] for _ in range(wl.Hkv)])
