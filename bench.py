@@ -248,8 +248,10 @@ def config_rows(graph_of, timed):
         wsd.get(svl.sparse_decode_workspace_size(wl.B, wl.H, wl.Hkv, wl.d, wl.k, wl.nv, wl.capacity))
         g_f = graph_of(lambda: [svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k,
                                                       idx_out=i, out=o, ws=wsf) for x, i, o in zip(xs, idx, outs)])
+        # steady decode: the selection of the round's fresh step (another graph) -- static
         g_d = graph_of(lambda: [svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, i,
-                                                       out=o, ws=wsd) for x, i, o in zip(xs, idx, outs)])
+                                                       flags=svl.SVL_DECODE_STATIC_PREFIX, out=o, ws=wsd)
+                                for x, i, o in zip(xs, idx, outs)])
         f_us = timed(g_f, 100, 10) * 1e3 / nrot
         d_us = timed(g_d, 100, 10) * 1e3 / nrot
         b = step_bytes(wl)
@@ -884,8 +886,8 @@ def run_headline(args):
     def layer_retrieve(l, flags=0):
         svl.retrieve(qs[l], Ks[l], seq, wl.vb, wl.nv, wl.k, flags=flags, idx_out=idxs[l], ws=ws_r)
 
-    def layer_decode(l):
-        svl.sparse_decode_attn(qds[l], Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l], out=outs[l],
+    def layer_decode(l, flags=0):
+        svl.sparse_decode_attn(qds[l], Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l], flags=flags, out=outs[l],
                                ws=ws_d)
 
     ws_f = svl.Workspace(dev)
@@ -919,7 +921,11 @@ def run_headline(args):
     g_unfused = graph_of(unfused_step)
     g_score = graph_of(lambda: [layer_retrieve(l, svl.SVL_RETRIEVE_SCORE_ONLY) for l in range(LAYERS)])
     g_select = graph_of(lambda: [layer_retrieve(l, svl.SVL_RETRIEVE_SELECT_ONLY) for l in range(LAYERS)])
-    g_decode = graph_of(lambda: [layer_decode(l) for l in range(LAYERS)])
+    # steady decode: idxs are the last fresh step's selection, the rows below the current
+    # token's were written by earlier steps -- SVL_DECODE_STATIC_PREFIX (their gathers start
+    # before the PDL wait); the unfused graph above writes idxs[l] right before
+    # layer_decode(l), so it runs without
+    g_decode = graph_of(lambda: [layer_decode(l, svl.SVL_DECODE_STATIC_PREFIX) for l in range(LAYERS)])
 
     if args.profile:
         for _ in range(max(args.warmup, 1)):
@@ -982,7 +988,8 @@ def run_headline(args):
     g_pack = graph_of(lambda: [svl.pack_kv(Ks[l], Vs[l], seq, wl.vb, wl.nv, idxs[l], Kp=packed[l][0],
                                            Vp=packed[l][1], ws=ws_p) for l in range(LAYERS)])
     g_decode_packed = graph_of(lambda: [svl.sparse_decode_attn(qds[l], packed[l][0], packed[l][1], packed[l][2],
-                                                               wl.vb, wl.k, ident, out=outs[l], ws=ws_d)
+                                                               wl.vb, wl.k, ident, out=outs[l], ws=ws_d,
+                                                               flags=svl.SVL_DECODE_STATIC_PREFIX)
                                         for l in range(LAYERS)])
     ms_pack = timed(g_pack, sub, 10)
     ms_decode_packed = timed(g_decode_packed, sub, 10)

@@ -84,6 +84,18 @@ typedef enum {
  * partials, co-resident grid) even when the split count would allow a
  * thread-block cluster per unit merged over DSMEM (A/B measurements, tests). */
 #define SVL_DECODE_GRID_MERGE 0x2000u
+/* svl_sparse_decode_attn(_push): the caller guarantees that vis_idx and every
+ * K/V row below seq_len[b] - 1 (all rows but the current token's) are not
+ * written by the work enqueued immediately before this call on the stream
+ * (steady decode: vis_idx is the last fresh step's selection; the prompt and
+ * the earlier tokens' rows were written by earlier steps).  The kernel then
+ * loads vis_idx and starts gathering those rows before its programmatic-
+ * dependent-launch wait, overlapping the upstream kernel's tail; their text
+ * share is laid out from a speculative read of seq_len[b] that is checked after
+ * the wait (a changed seq_len re-gathers the text rows).  q, seq_len and the
+ * current token's row are read only after the wait.  Results are bitwise
+ * identical with and without the flag. */
+#define SVL_DECODE_STATIC_PREFIX 0x4000u
 /* Split-count pin, flags bits 24..31 (0 = the planner's choice).
  * svl_sparse_decode_attn(_push): exactly n CTAs per (b, KV group) unit
  * (B*Hkv*n must not exceed the co-resident CTA count when n > 1, else

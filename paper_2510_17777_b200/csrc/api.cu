@@ -664,7 +664,7 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
                                      const PushArgs& push, const char* name) {
     if (!q || (!out && push.P == 0) || !span.seq_len || (k > 0 && !vis_idx))
         return fail(SVL_ERR_INVALID_ARGUMENT, "NULL pointer argument%s");
-    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK | SVL_IDX_PADDED | SVL_DECODE_GRID_MERGE))
+    if (flags & ~(SVL_SELECT_SHARED | SVL_PIN_SPLITS_MASK | SVL_IDX_PADDED | SVL_DECODE_GRID_MERGE | SVL_DECODE_STATIC_PREFIX))
         return fail(SVL_ERR_INVALID_ARGUMENT, "unknown flag bits%s");
     if (B < 1 || H < 1 || Hkv < 1) return fail(SVL_ERR_SHAPE, "B, H, Hkv must be >= 1%s");
     if (H % Hkv) return fail(SVL_ERR_SHAPE, "H %% Hkv != 0%s");
@@ -710,6 +710,7 @@ static svl_status sparse_decode_impl(const void* q, int32_t B, int32_t H, int32_
     p.shared = (flags & SVL_SELECT_SHARED) ? 1 : 0;
     p.padded = (flags & SVL_IDX_PADDED) ? 1 : 0;
     p.cluster = cluster;
+    p.static_vis = (flags & SVL_DECODE_STATIC_PREFIX) ? 1 : 0;
     p.capacity = K.capacity;
     p.S = S;
     // rows of one split <= ceil(vb / S) + ceil(k / S) + ceil(T_max / S) (three segments)

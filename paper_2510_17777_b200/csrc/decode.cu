@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     }
 #endif
     // programmatic dependent launch: nothing an upstream kernel may write (seq_len,
-    // idx, q, the appended K/V row) is read before the wait
+    // idx, q, the appended K/V row) is read before the wait -- but see SVL_DECODE_STATIC_PREFIX
     // cluster merge: one local arrival + the bytes every peer will push (its share of this
     // CTA's items and its 32 M, l values); peers push only after their cluster_wait
     const uint32_t mbar = smem_u32(smem + SM::MB_OFF);
@@ -151,100 +151,17 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         cluster_arrive_relaxed();
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // SVL_DECODE_STATIC_PREFIX: vis_idx and every K, V row below seq_len - 1 (all but the
+    // current token's) are not written by the upstream kernel, so the idx loads and the first
+    // batches' gathers of those rows go out before the wait (overlapping the upstream kernel's
+    // tail), their text share laid out by a speculative seq_len read that is checked after it;
+    // q, seq_len, the current token's row and the workspace counters are read only after it
+    const bool early = p.static_vis != 0;
     const int b = u / p.Hkv, G = u % p.Hkv;
-    const int U = p.shared ? 1 : p.Hkv;
-    const int uG = p.shared ? 0 : G;
-    // this call's epoch of the unit (advanced by split 0 at the end of the previous call)
-    const uint32_t tag_epoch = (S > 1 && !p.cluster) ? ld_relaxed_u32(p.epochs + u) : 0u;
-    // tag = hash(epoch, unit, S): a slot left by another call -- another epoch, or another
-    // split layout of the same workspace -- does not match (zero-filled slots never do)
-    const uint32_t tag = partial_tag(tag_epoch, (uint32_t)u, (uint32_t)S);
-    const int32_t* idx = p.idx + ((int64_t)b * U + uG) * p.k;
-    const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
-    const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
-
-    // this split's share of the segments: system rows [s0, s0 + ns), kept visual m in
-    // [m0, m0 + nm), later text rows t in [t0, t0 + na) (the last needs seq_len)
-    const int s0 = (int)((int64_t)split * p.vb / S), ns = (int)((int64_t)(split + 1) * p.vb / S) - s0;
-    const int m0 = (int)((int64_t)split * p.k / S), nm = (int)((int64_t)(split + 1) * p.k / S) - m0;
-    struct Pending {
-        int x, xp;
-    };
-    auto fetch = [&](int i) -> Pending {  // list item i: issue its idx loads (visual items only)
-        Pending r{0, -1};
-        const int m = m0 + (i - ns);
-        if (i >= ns && i < ns + nm) {
-            r.x = __ldg(idx + m);
-            r.xp = m > 0 ? __ldg(idx + m - 1) : -1;
-        }
-        return r;
-    };
-    // the first NBUF - 1 batches' idx loads go out together with seq_len's
-    Pending pre = fetch(tid);
-    int L = __ldg(p.seq_len + b);
-    if (L < p.vb + p.nv || L > p.capacity) {
-        if (tid == 0 && split == 0) raise_flag(p.flags, 4u /*SPAN*/);
-        L = min(max(L, p.vb + p.nv), p.capacity);
-    }
-    const int T = L - p.vb - p.nv;
-    const int t0 = (int)((int64_t)split * T / S), na = (int)((int64_t)(split + 1) * T / S) - t0;
-    const int n = ns + nm + na;  // this CTA's attended rows
-    const int nb = (n + RB - 1) / RB;
-    stamp(1);
-    // row id of list item i (-1: past the list, or a bad index -> device flag)
-    auto resolve = [&](int i, const Pending& r) -> int {
-        if (i < 0 || i >= n) return -1;
-        if (i < ns) return s0 + i;
-        if (i < ns + nm) {
-            if (r.x >= 0 && r.x < p.nv && r.xp < r.x) return p.vb + r.x;
-            if (p.padded && r.x == -1) return -1;  // trailing padding (SVL_IDX_PADDED)
-            raise_flag(p.flags, 1u /*SVL_DEVFLAG_INDEX*/);
-            return -1;
-        }
-        return p.vb + p.nv + t0 + (i - ns - nm);
-    };
-    auto issue = [&](int j) {  // gather batch j (row ids in rows_s[j % NBUF]) -- one commit group
-        if (j < nb) {
-            const int* rows = rows_s + (j % NBUF) * RB;
-            const uint32_t sK = smem_u32(smem + (j % NBUF) * SM::BUF_BYTES);
-            const uint32_t sV = sK + RB * SM::ROW_BYTES;
-            const int nj = min(RB, n - j * RB);
-            const int nr = (nj + 15) & ~15;
-            // thread -> chunk c of rows r0, r0 + NTH/CH, ...: every row id read first, then
-            // all the copies back to back (no shared-memory load between two copies)
-            constexpr int RPP = NTH / CH, PASSES = RB / RPP;
-            const int c = tid % CH, r0 = tid / CH;
-            int rw[PASSES];
-#pragma unroll
-            for (int k = 0; k < PASSES; ++k) rw[k] = (r0 + k * RPP < nr) ? rows[r0 + k * RPP] : -2;
-#pragma unroll
-            for (int k = 0; k < PASSES; ++k) {
-                const int r = r0 + k * RPP;
-                if (rw[k] == -2) continue;
-                const bool valid = rw[k] >= 0;
-                const int rr = valid ? rw[k] : 0;
-#if SVL_DEBUG_TRAP  // debug builds: every gathered row lies inside the cache
-                if (rr >= p.capacity) __trap();
-#endif
-                cp_async16(sK + r * SM::ROW_BYTES + swz_k(r, c) * 16, Kb + (int64_t)rr * p.kst + c * 8, valid);
-                cp_async16(sV + r * SM::ROW_BYTES + swz_v(r, c) * 16, Vb + (int64_t)rr * p.vst + c * 8, valid);
-            }
-        }
-        cp_async_commit();  // (empty groups keep the wait_group arithmetic uniform)
-    };
-
-    // ---- prologue: row ids of batches [0, NBUF - 1) (one per thread), their gathers, and
-    // the idx loads of batch NBUF - 1 (consumed at the top of iteration 0)
-    if (tid < (NBUF - 1) * RB) rows_s[tid] = resolve(tid, pre);
-    Pending pend = tid < RB ? (NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid)) : Pending{0, -1};
-    cta_sync();
-    stamp(2);
-    for (int j = 0; j < NBUF - 1; ++j) issue(j);
-
-    // q A-fragments (heads gid, gid + 8 of the group; zero beyond g)
+    // q A-fragments (heads gid, gid + 8 of the group; zero beyond g); an early call loads
+    // them right after the wait
     uint4 qa[NCH], qb[NCH];
-    {
+    auto load_q = [&]() {
         const int ha = gid, hb = gid + 8;
 #pragma unroll
         for (int i = 0; i < NCH; ++i) qa[i] = qb[i] = make_uint4(0, 0, 0, 0);
@@ -258,6 +175,161 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
 #pragma unroll
             for (int i = 0; i < NCH; ++i) qb[i] = qr[t + 4 * i];
         }
+    };
+    if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int U = p.shared ? 1 : p.Hkv;
+    const int uG = p.shared ? 0 : G;
+    const int32_t* idx = p.idx + ((int64_t)b * U + uG) * p.k;
+    const uint16_t* Kb = p.K + (int64_t)b * p.ksb + (int64_t)G * p.ksh;
+    const uint16_t* Vb = p.V + (int64_t)b * p.vsb + (int64_t)G * p.vsh;
+
+    // this split's share of the segments: system rows [s0, s0 + ns), kept visual m in
+    // [m0, m0 + nm), later text rows t in [t0, t0 + na) (the last needs seq_len)
+    const int s0 = (int)((int64_t)split * p.vb / S), ns = (int)((int64_t)(split + 1) * p.vb / S) - s0;
+    const int m0 = (int)((int64_t)split * p.k / S), nm = (int)((int64_t)(split + 1) * p.k / S) - m0;
+    const int nst = ns + nm;  // list items [0, nst) need no seq_len (system + visual rows)
+    struct Pending {
+        int x, xp;
+    };
+    auto fetch = [&](int i) -> Pending {  // list item i: issue its idx loads (visual items only)
+        Pending r{0, -1};
+        const int m = m0 + (i - ns);
+        if (i >= ns && i < ns + nm) {
+            r.x = __ldg(idx + m);
+            r.xp = m > 0 ? __ldg(idx + m - 1) : -1;
+        }
+        return r;
+    };
+    // row id of a system or visual list item i < nst (-1: a bad index -> device flag)
+    auto resolve_st = [&](int i, const Pending& r) -> int {
+        if (i < ns) return s0 + i;
+        if (r.x >= 0 && r.x < p.nv && r.xp < r.x) return p.vb + r.x;
+        if (p.padded && r.x == -1) return -1;  // trailing padding (SVL_IDX_PADDED)
+        raise_flag(p.flags, 1u /*SVL_DEVFLAG_INDEX*/);
+        return -1;
+    };
+    // batches [0, JE) of an early call had their system / visual rows gathered before the wait
+    constexpr int JE = NBUF > 1 ? NBUF - 1 : 1;
+    // gather list items [lo, hi) of batch j (row ids in rows_s[j % NBUF]; n_lim bounds the
+    // batch's rows, padded to the 16-row tile with zero-filled copies) -- no commit
+    auto issue_rows = [&](int j, auto take, int n_lim) {  // take(i): gather list item i
+        const int* rows = rows_s + (j % NBUF) * RB;
+        const uint32_t sK = smem_u32(smem + (j % NBUF) * SM::BUF_BYTES);
+        const uint32_t sV = sK + RB * SM::ROW_BYTES;
+        const int nj = min(RB, n_lim - j * RB);
+        const int nr = (nj + 15) & ~15;
+        // thread -> chunk c of rows r0, r0 + NTH/CH, ...: every row id read first, then
+        // all the copies back to back (no shared-memory load between two copies)
+        constexpr int RPP = NTH / CH, PASSES = RB / RPP;
+        const int c = tid % CH, r0 = tid / CH;
+        int rw[PASSES];
+#pragma unroll
+        for (int k = 0; k < PASSES; ++k) {
+            const int r = r0 + k * RPP;
+            rw[k] = (r < nr && take(j * RB + r)) ? rows[r] : -2;
+        }
+#pragma unroll
+        for (int k = 0; k < PASSES; ++k) {
+            const int r = r0 + k * RPP;
+            if (rw[k] == -2) continue;
+            const bool valid = rw[k] >= 0;
+            const int rr = valid ? rw[k] : 0;
+#if SVL_DEBUG_TRAP  // debug builds: every gathered row lies inside the cache
+            if (rr >= p.capacity) __trap();
+#endif
+            cp_async16(sK + r * SM::ROW_BYTES + swz_k(r, c) * 16, Kb + (int64_t)rr * p.kst + c * 8, valid);
+            cp_async16(sV + r * SM::ROW_BYTES + swz_v(r, c) * 16, Vb + (int64_t)rr * p.vst + c * 8, valid);
+        }
+    };
+    // text share of this split for a seq_len value (clamped to the span; the device flag is
+    // raised for the checked read only)
+    auto clamp_len = [&](int Lv) { return min(max(Lv, p.vb + p.nv), p.capacity); };
+    auto text_share = [&](int Lv, int& t0o, int& nao) {
+        const int Tv = Lv - p.vb - p.nv;
+        t0o = (int)((int64_t)split * Tv / S);
+        nao = (int)((int64_t)(split + 1) * Tv / S) - t0o;
+    };
+    // the first NBUF - 1 batches' idx loads (one item per thread) go out first
+    Pending pre = fetch(tid);
+    int Ls = 0, t0s = 0, nas = 0;  // early: the speculative seq_len (clamped) and text share
+    Pending pend{0, -1};            // idx loads of batch NBUF - 1 (consumed at the top of iteration 0)
+    if (early) {
+        if (tid < RB) pend = NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid);
+        Ls = clamp_len((int)ld_relaxed_u32(reinterpret_cast<const uint32_t*>(p.seq_len + b)));
+#if SVL_EXP_SPEC_MISS  // test build: the speculation always misses (the re-gather path)
+        Ls = clamp_len(Ls - 1 - (int)(split & 3));
+#endif
+        text_share(Ls, t0s, nas);
+        const int n_s = nst + nas;
+        // every item of batches [0, JE) under the speculation; all gathered now but the
+        // current token's row (Ls - 1), which goes out right after the wait
+        if (tid < JE * RB)
+            rows_s[tid] = tid < nst ? resolve_st(tid, pre) : (tid < n_s ? p.vb + p.nv + t0s + (tid - nst) : -1);
+        cta_sync();
+        const int i_cur = (nas > 0 && t0s + nas == Ls - p.vb - p.nv) ? n_s - 1 : -1;  // the current row's item
+#if SVL_EXP_CURPRE  // timing experiment: the current row gathered before the wait too
+        const_cast<int&>(i_cur) = -1;
+#endif
+        for (int j = 0; j < JE; ++j) issue_rows(j, [&](int i) { return i != i_cur; }, n_s);
+        cp_async_commit();  // (one group, older than every group below)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        load_q();
+        // one group per early batch, the current row's copies in its batch's group (batch 0's
+        // compute does not wait for a later batch's row); these stand in for the prologue's
+        // groups in the wait_group arithmetic (JE = NBUF - 1 when NBUF > 1)
+        for (int j = 0; j < JE; ++j) {
+            if (i_cur >= 0 && i_cur / RB == j) issue_rows(j, [&](int i) { return i == i_cur; }, n_s);
+            cp_async_commit();
+        }
+    }
+    // this call's epoch of the unit (advanced by split 0 at the end of the previous call)
+    const uint32_t tag_epoch = (S > 1 && !p.cluster) ? ld_relaxed_u32(p.epochs + u) : 0u;
+    // tag = hash(epoch, unit, S): a slot left by another call -- another epoch, or another
+    // split layout of the same workspace -- does not match (zero-filled slots never do)
+    const uint32_t tag = partial_tag(tag_epoch, (uint32_t)u, (uint32_t)S);
+    int L = __ldg(p.seq_len + b);
+    if (L < p.vb + p.nv || L > p.capacity) {
+        if (tid == 0 && split == 0) raise_flag(p.flags, 4u /*SPAN*/);
+        L = clamp_len(L);
+    }
+    int t0, na;
+    text_share(L, t0, na);
+    const int n = nst + na;  // this CTA's attended rows
+    const int nb = (n + RB - 1) / RB;
+    stamp(1);
+    // row id of list item i (-1: past the list, or a bad index -> device flag)
+    auto resolve = [&](int i, const Pending& r) -> int {
+        if (i < 0 || i >= n) return -1;
+        if (i < nst) return resolve_st(i, r);
+        return p.vb + p.nv + t0 + (i - nst);
+    };
+    // an early call published (and gathered) every item of batches [0, JE)
+    auto published = [&](int i) { return early && i < JE * RB; };
+    auto issue = [&](int j) {  // gather batch j -- one commit group (+ the tile's zero-filled padding)
+        if (j < nb) issue_rows(j, [&](int i) { return !published(i); }, n);
+        cp_async_commit();  // (empty groups keep the wait_group arithmetic uniform)
+    };
+    if (early && L != Ls) {
+        // the speculation missed (seq_len changed upstream): every early copy lands, then the
+        // text items of batches [0, JE) are laid out and gathered again, and land too
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        cta_sync();
+        if (tid < JE * RB && tid >= nst) rows_s[tid] = resolve(tid, pre);
+        cta_sync();
+        for (int j = 0; j < JE; ++j) issue_rows(j, [&](int i) { return i >= nst; }, n);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        cta_sync();
+    }
+
+    // ---- prologue: row ids of batches [0, NBUF - 1) (one per thread), their gathers, and
+    // the idx loads of batch NBUF - 1 (consumed at the top of iteration 0)
+    if (tid < (NBUF - 1) * RB && !published(tid)) rows_s[tid] = resolve(tid, pre);
+    if (!early && tid < RB) pend = NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid);
+    cta_sync();
+    stamp(2);
+    if (!early) {
+        for (int j = 0; j < NBUF - 1; ++j) issue(j);
+        load_q();
     }
 
     // FlashAttention-2 style per warp: warp w owns rows [16 w, 16 w + 16) of every batch,
@@ -274,7 +346,8 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     for (int j = 0; j < nb; ++j) {
         // row ids of batch j + NBUF - 1 (loads issued one iteration ago), then the loads of
         // batch j + NBUF's; the barrier publishes the ids and frees buffer (j - 1) % NBUF
-        if (tid < RB) rows_s[((j + NBUF - 1) % NBUF) * RB + tid] = resolve((j + NBUF - 1) * RB + tid, pend);
+        if (tid < RB && !published((j + NBUF - 1) * RB + tid))
+            rows_s[((j + NBUF - 1) % NBUF) * RB + tid] = resolve((j + NBUF - 1) * RB + tid, pend);
         if (tid < RB) pend = fetch((j + NBUF) * RB + tid);
         cta_sync();
         issue(j + NBUF - 1);

@@ -69,6 +69,7 @@ struct DecodeParams {
     int single_batch;  // every split has <= kDecodeRowsMax rows (host bound): one gather buffer
     int padded;        // SVL_IDX_PADDED: trailing -1 entries of vis_idx are skipped silently
     int cluster;       // 1: the S CTAs of a unit are one thread-block cluster, merged over DSMEM
+    int static_vis;    // SVL_DECODE_STATIC_PREFIX: idx and rows < seq_len - 1 gathered before the PDL wait
     float scale2;  // scale * log2(e)
     float* out;    // [B][H][d]
     float* lse_out;

@@ -27,6 +27,7 @@ WORKSPACE_HEADER_BYTES = 1024  # SVL_WORKSPACE_HEADER_BYTES
 SVL_IDX_PADDED = 0x800
 SVL_SHARD_VIEW = 0x1000
 SVL_DECODE_GRID_MERGE = 0x2000
+SVL_DECODE_STATIC_PREFIX = 0x4000
 SVL_PIN_SPLITS_MASK = 0xff000000
 
 

@@ -49,8 +49,9 @@ def test_decode_any_split_count_matches_oracle(svl, orc, name, splits):
             a, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
                                           flags=fl, lse_out=lse, ws=ws)
             a, lse_a = a.clone(), lse.clone()
+            # the rerun with SVL_DECODE_STATIC_PREFIX (prompt rows gathered before the PDL wait)
             b, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
-                                          flags=fl, lse_out=lse, ws=ws)
+                                          flags=fl | svl.SVL_DECODE_STATIC_PREFIX, lse_out=lse, ws=ws)
             torch.cuda.synchronize()
             assert torch.equal(a, b) and torch.equal(lse_a, lse), f"S={S} not bitwise repeatable"
             mx, rel = parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)
@@ -70,10 +71,10 @@ def test_decode_planner_default_and_graph_replay(svl, orc):
     parity.check_attention(ref.cpu().numpy(), None, oo, ol)
     outs = [torch.empty_like(ref) for _ in range(6)]
 
-    def body():
-        for o in outs:
+    def body():  # alternating with / without SVL_DECODE_STATIC_PREFIX (idx is not written here)
+        for i, o in enumerate(outs):
             svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
-                                   out=o, ws=ws)
+                                   flags=svl.SVL_DECODE_STATIC_PREFIX if i % 2 else 0, out=o, ws=ws)
     body()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -121,7 +122,7 @@ def test_decode_planner_batch_sweep_matches_oracle(svl, orc, B):
                                   lse_out=lse, ws=ws)
     a, lse_a = a.clone(), lse.clone()
     b, _ = svl.sparse_decode_attn(dev["q_dec"], dev["K"], dev["V"], dev["seq_len"], wl.vb, wl.nv, idx,
-                                  lse_out=lse, ws=ws)
+                                  flags=svl.SVL_DECODE_STATIC_PREFIX, lse_out=lse, ws=ws)
     torch.cuda.synchronize()
     assert torch.equal(a, b) and torch.equal(lse_a, lse)
     parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)

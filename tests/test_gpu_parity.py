@@ -229,14 +229,16 @@ def test_decode_shared_selection(svl, orc):
     parity.check_attention(out, lse, oo, ol)
 
 
-def test_decode_bad_indices_flagged(svl):
+@pytest.mark.parametrize("early", [0, 1])
+def test_decode_bad_indices_flagged(svl, early):
     wl = gen.DecodeWorkload("bad", 1, 8, 2, 64, 4, 300, 10, 20, 1, 64)
     x = gen.make_decode_inputs(wl, seed=14, device="cuda")
     idx = torch.arange(20, dtype=torch.int32, device="cuda").flip(0).expand(1, 2, 20).contiguous()
     ws = svl.Workspace()
     ws.get(1 << 20)
     ws.reset_flags()
-    out, _ = svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx, ws=ws)
+    fl = svl.SVL_DECODE_STATIC_PREFIX if early else 0  # (the early gathers resolve the same rows)
+    out, _ = svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx, flags=fl, ws=ws)
     assert ws.flags() & svl.SVL_DEVFLAG_INDEX
     assert torch.isfinite(out).all()
 

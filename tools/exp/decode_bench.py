@@ -21,6 +21,7 @@ def run(name, pins, layers=28, steps=200):
     for pin in pins:
         ws = svl.Workspace()
         fl = (svl.SVL_PIN_SPLITS(abs(pin)) if pin else 0) | (svl.SVL_DECODE_GRID_MERGE if pin < 0 else 0)
+        fl |= svl.SVL_DECODE_STATIC_PREFIX if os.environ.get("DSTATIC") == "1" else 0
         def body():
             for l in range(nl):
                 svl.sparse_decode_attn(xs[l]["q_dec"], xs[l]["K"], xs[l]["V"], xs[l]["seq_len"], wl.vb, wl.nv,
