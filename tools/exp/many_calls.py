@@ -19,9 +19,12 @@ for it in range(N):
     o, i = svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k, ws=ws)
     d, _ = svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, i0, ws=ws)
     r = svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k, ws=ws)
+    # (i0 and the cache are not written by the retrieve before it: the early-gather path)
+    ds, _ = svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, i0,
+                                   flags=svl.SVL_DECODE_STATIC_PREFIX, ws=ws)
     if it % 100 == 99 or it == N - 1:
         torch.cuda.synchronize()
-    bad += int(not (torch.equal(o, o0) and torch.equal(i, i0) and torch.equal(d, d0) and torch.equal(r, r0)))
+    bad += int(not (torch.equal(o, o0) and torch.equal(i, i0) and torch.equal(d, d0) and torch.equal(ds, d0) and torch.equal(r, r0)))
 torch.cuda.synchronize()
-print(f"{name}: {N} x (fresh step + steady decode + retrieve): {bad} calls differ from the first; "
+print(f"{name}: {N} x (fresh step + steady decode + retrieve + early-gather decode): {bad} calls differ from the first; "
       f"device flags {ws.flags()}")
