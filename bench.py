@@ -926,6 +926,7 @@ def run_headline(args):
     # before the PDL wait); the unfused graph above writes idxs[l] right before
     # layer_decode(l), so it runs without
     g_decode = graph_of(lambda: [layer_decode(l, svl.SVL_DECODE_STATIC_PREFIX) for l in range(LAYERS)])
+    g_decode_plain = graph_of(lambda: [layer_decode(l) for l in range(LAYERS)])  # (no early gathers)
 
     if args.profile:
         for _ in range(max(args.warmup, 1)):
@@ -978,6 +979,7 @@ def run_headline(args):
     ms_score = timed(g_score, sub, 10)
     ms_select = timed(g_select, sub, 10)
     ms_decode = timed(g_decode, sub, 10)
+    ms_decode_plain = timed(g_decode_plain, sub, 10)
 
     # ---- pack-once: once per round, then the steady
     # steps attend the dense packed cache instead of gathering the kept rows
@@ -1250,11 +1252,14 @@ def run_headline(args):
             "hbm_frac_of_measured": value / world / peak,
             "unfused_us_per_layer": {"retrieve+decode (2 calls)": ms_unfused * 1e3 / LAYERS,
                                      "score": score_us, "select": ms_select * 1e3 / LAYERS,
-                                     "decode+merge": ms_decode * 1e3 / LAYERS},
+                                     "decode+merge": ms_decode_plain * 1e3 / LAYERS},
             "bytes_per_layer": nbytes["total"],
             "steady": {"us_per_layer": steady_us, "GB_s": steady_bytes / (steady_us * 1e-6) / 1e9,
                        "bytes_per_layer": steady_bytes,
-                       "what": "svl_sparse_decode_attn alone (selected + text K/V), indices reused"},
+                       "what": "svl_sparse_decode_attn alone (selected + text K/V), indices reused, "
+                               "SVL_DECODE_STATIC_PREFIX (rows below the current token's gathered before "
+                               "the PDL wait, overlapping the previous layer's tail)",
+                       "us_per_layer_without_early_gathers": ms_decode_plain * 1e3 / LAYERS},
             "amortized_us_per_layer": amort_us,
             "amortized_what": f"(1 fresh step + {ROUND_STEPS - 1} steady steps) / {ROUND_STEPS} per round",
             "pack_once": {"what": "svl_pack_kv once per round (kept visual + text K/V -> dense cache), then "
