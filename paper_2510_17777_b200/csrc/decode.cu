@@ -176,7 +176,10 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             for (int i = 0; i < NCH; ++i) qb[i] = qr[t + 4 * i];
         }
     };
-    if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!early) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        stamp(6);
+    }
     const int U = p.shared ? 1 : p.Hkv;
     const int uG = p.shared ? 0 : G;
     const int32_t* idx = p.idx + ((int64_t)b * U + uG) * p.k;
@@ -273,6 +276,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         for (int j = 0; j < JE; ++j) issue_rows(j, [&](int i) { return i != i_cur; }, n_s);
         cp_async_commit();  // (one group, older than every group below)
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        stamp(6);
         load_q();
         // one group per early batch, the current row's copies in its batch's group (batch 0's
         // compute does not wait for a later batch's row); these stand in for the prologue's
@@ -287,15 +291,21 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     // tag = hash(epoch, unit, S): a slot left by another call -- another epoch, or another
     // split layout of the same workspace -- does not match (zero-filled slots never do)
     const uint32_t tag = partial_tag(tag_epoch, (uint32_t)u, (uint32_t)S);
-    int L = __ldg(p.seq_len + b);
-    if (L < p.vb + p.nv || L > p.capacity) {
-        if (tid == 0 && split == 0) raise_flag(p.flags, 4u /*SPAN*/);
-        L = clamp_len(L);
-    }
+    // seq_len: an early call runs on its speculative value and checks this read after the
+    // batch loop (its latency overlaps the compute); a miss reruns the pipeline on it
+    const int L_raw = __ldg(p.seq_len + b);
+    auto checked_len = [&]() {
+        if (L_raw < p.vb + p.nv || L_raw > p.capacity) {
+            if (tid == 0 && split == 0) raise_flag(p.flags, 4u /*SPAN*/);
+            return clamp_len(L_raw);
+        }
+        return L_raw;
+    };
+    int L = early ? Ls : checked_len();
     int t0, na;
     text_share(L, t0, na);
-    const int n = nst + na;  // this CTA's attended rows
-    const int nb = (n + RB - 1) / RB;
+    int n = nst + na;  // this CTA's attended rows
+    int nb = (n + RB - 1) / RB;
     stamp(1);
     // row id of list item i (-1: past the list, or a bad index -> device flag)
     auto resolve = [&](int i, const Pending& r) -> int {
@@ -303,45 +313,37 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         if (i < nst) return resolve_st(i, r);
         return p.vb + p.nv + t0 + (i - nst);
     };
-    // an early call published (and gathered) every item of batches [0, JE)
-    auto published = [&](int i) { return early && i < JE * RB; };
+    // an early call published (and gathered) every item of batches [0, JE) -- until a rerun
+    bool pub_early = early;
+    auto published = [&](int i) { return pub_early && i < JE * RB; };
     auto issue = [&](int j) {  // gather batch j -- one commit group (+ the tile's zero-filled padding)
         if (j < nb) issue_rows(j, [&](int i) { return !published(i); }, n);
         cp_async_commit();  // (empty groups keep the wait_group arithmetic uniform)
     };
-    if (early && L != Ls) {
-        // the speculation missed (seq_len changed upstream): every early copy lands, then the
-        // text items of batches [0, JE) are laid out and gathered again, and land too
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        cta_sync();
-        if (tid < JE * RB && tid >= nst) rows_s[tid] = resolve(tid, pre);
-        cta_sync();
-        for (int j = 0; j < JE; ++j) issue_rows(j, [&](int i) { return i >= nst; }, n);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        cta_sync();
-    }
 
+    constexpr int NTO = D / 8;  // output n-tiles
+    float o[NTO][4];
+    float m_a, m_b;  // running max of heads gid, gid + 8 (quad-uniform)
+    float l_a, l_b;  // this thread's share of the running sums
+    for (;;) {  // one pass; an early call whose seq_len speculation missed takes a second
     // ---- prologue: row ids of batches [0, NBUF - 1) (one per thread), their gathers, and
     // the idx loads of batch NBUF - 1 (consumed at the top of iteration 0)
     if (tid < (NBUF - 1) * RB && !published(tid)) rows_s[tid] = resolve(tid, pre);
-    if (!early && tid < RB) pend = NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid);
+    if (!pub_early && tid < RB) pend = NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid);
     cta_sync();
     stamp(2);
-    if (!early) {
+    if (!pub_early)
         for (int j = 0; j < NBUF - 1; ++j) issue(j);
-        load_q();
-    }
+    if (!early) load_q();
 
     // FlashAttention-2 style per warp: warp w owns rows [16 w, 16 w + 16) of every batch,
     // scores them, keeps a running max per head, and multiplies P (still in registers: the
     // two n-tiles of the score accumulator ARE the A fragment of a k16 MMA) into its own
     // O[16 heads][D] -- no per-batch CTA barrier beyond the buffer hand-over.
-    constexpr int NTO = D / 8;  // output n-tiles
-    float o[NTO][4];
 #pragma unroll
     for (int i = 0; i < NTO; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m_a = -INFINITY, m_b = -INFINITY;  // running max of heads gid, gid + 8 (quad-uniform)
-    float l_a = 0.f, l_b = 0.f;              // this thread's share of the running sums
+    m_a = m_b = -INFINITY;
+    l_a = l_b = 0.f;
 
     for (int j = 0; j < nb; ++j) {
         // row ids of batch j + NBUF - 1 (loads issued one iteration ago), then the loads of
@@ -443,6 +445,17 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     }
     cp_async_wait<0>();
     cta_sync();  // every warp's batches done; the gather buffers are free
+    if (!early || !pub_early) break;
+    const int L_chk = checked_len();
+    if (L_chk == Ls) break;
+    // the speculation missed (seq_len changed upstream): rerun on the checked value with every
+    // row gathered after the wait (the pipeline's buffers are idle: the barrier above)
+    pub_early = false;
+    L = L_chk;
+    text_share(L, t0, na);
+    n = nst + na;
+    nb = (n + RB - 1) / RB;
+    }
     stamp(4);
 
     // ---- cross-warp merge inside the CTA (shared memory, the gather buffers): each warp's

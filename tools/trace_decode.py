@@ -19,7 +19,7 @@ from paper_2510_17777_b200 import inputs as gen, svl  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "long-video"
 pin = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-flags = svl.SVL_PIN_SPLITS(pin) if pin else 0
+flags = (svl.SVL_PIN_SPLITS(pin) if pin else 0) | int(os.environ.get("DFLAGS", "0"), 0)
 wl = gen.CONFIGS[name]
 NL = 28 if wl.B * wl.nv <= 65536 else 3
 xs = [gen.make_decode_inputs(wl, seed=s, device="cuda") for s in range(NL)]
@@ -46,7 +46,7 @@ tr = tr[tr[:, 0] > 0]
 # stamps 0..13: SM cycles (clock64) of the CTA; 14 / 15: globaltimer at start / end
 f_ghz = ((tr[:, 7] - tr[:, 0]).double() / (tr[:, 15] - tr[:, 14]).double())
 print(f"SM clock during the kernel (clock64 / globaltimer, median over CTAs): {f_ghz.median() * 1e3:.0f} MHz")
-names = {1: "PDL wait + seq_len", 2: "row ids", 3: "batch0 landed", 4: "compute done",
+names = {6: "PDL wait released", 1: "seq_len read", 2: "row ids", 3: "batch0 landed", 4: "compute done",
          10: "O staged (cross-warp)", 11: "CTA M / l", 12: "cluster_wait",
          5: "partial stored/pushed", 8: "partials landed", 9: "merged", 7: "end"}
 print(f"{name} decode pin={pin}: {tr.shape[0]} CTAs; per-CTA cycles from its start -> us at its clock "
@@ -57,3 +57,13 @@ for ph, nm in names.items():
         continue
     v = (tr[ok, ph] - tr[ok, 0]).double() / f_ghz[ok] / 1e3
     print(f"  {ph:2d} {nm:22s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
+# the same phases from the CTA's own PDL release (stamp 6): the critical path after the wait
+ok6 = tr[:, 6] > 0
+if ok6.any():
+    print("  from the PDL release (min / median / max):")
+    for ph, nm in names.items():
+        ok = ok6 & (tr[:, ph] > 0)
+        if ph == 6 or not ok.any():
+            continue
+        v = (tr[ok, ph] - tr[ok, 6]).double() / f_ghz[ok] / 1e3
+        print(f"  {ph:2d} {nm:22s} {v.min():8.2f} {v.median():8.2f} {v.max():8.2f}")
