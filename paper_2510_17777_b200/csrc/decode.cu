@@ -66,9 +66,10 @@ struct DecodeSmem {
     static constexpr int RUN_OFF = WML_OFF + 2 * NW * 16 * 4;       // CTA M[16], l[16]
     static constexpr int SC_OFF = RUN_OFF + 32 * 4;                 // warp scales [NW][16]
     // cluster merge (DSMEM): every peer's share of this CTA's items [S][per] and its M, l
-    // [S][32]; per = ceil(g D / S) -> S * per <= 16 D + 16; mbarrier counting the bytes
+    // [S][32]; per = ceil(g D / S) rounded up to 4 (16-byte pushes) -> S * per <= 16 D + 4 S
+    // <= 16 D + 64; mbarrier counting the bytes
     static constexpr int RCV_OFF = SC_OFF + NW * 16 * 4;
-    static constexpr int RML_OFF = RCV_OFF + (16 * D + 16) * 4;
+    static constexpr int RML_OFF = RCV_OFF + (16 * D + 64) * 4;
     static constexpr int MB_OFF = RML_OFF + 16 * 33 * 4;  // rml rows padded to 33 (bank-conflict free)
     static constexpr int BYTES = MB_OFF + 16;
 };
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     const uint32_t mbar = smem_u32(smem + SM::MB_OFF);
     if (p.cluster) {
         if (tid == 0) {
-            const int items = p.g * D, per = (items + S - 1) / S;
+            const int items = p.g * D, per = (((items + S - 1) / S) + 3) & ~3;  // (16-B pushes)
             const int mine = max(0, min(per, items - split * per));
             mbar_init(mbar, 1);
             mbar_arrive_expect_tx(mbar, (uint32_t)(S * (mine + 32) * 4));
@@ -534,17 +535,28 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
         // the S CTAs of the unit form one cluster: every CTA pushes each item of the unit's
         // g x D block to its owner q = i / per (st.async into q's receive buffer, counted on
         // q's mbarrier) and its 32 (M, l) to every peer; owners merge in rank order
-        const int items = p.g * D, per = (items + S - 1) / S;
+        const int items = p.g * D, per = (((items + S - 1) / S) + 3) & ~3;  // (16-B pushes)
         float* rcv = reinterpret_cast<float*>(smem + SM::RCV_OFF);  // [S][per]
         float* rml = reinterpret_cast<float*>(smem + SM::RML_OFF);  // [S][33]: M[16], l[16], pad
         stamp(11);
         cluster_wait();  // every peer has armed its barrier
         stamp(12);
         const uint32_t rcv_a = smem_u32(rcv), rml_a = smem_u32(rml);
-        for (int i = tid; i < items; i += NTH) {
-            const int q = i / per;
-            st_async_f32(mapa_shared(rcv_a + (uint32_t)(split * per + (i - q * per)) * 4u, q),
-                         cta_o(i / D, i % D), mapa_shared(mbar, q));
+        // four consecutive items per thread (one head: D % 4 == 0; one owner: per % 4 == 0):
+        // 128-bit loads of the warps' staged O, one 16-byte push
+        for (int i = 4 * tid; i < items; i += 4 * NTH) {
+            const int q = i / per, h = i / D, c = (i % D) ^ ((h & 3) << 3);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const float sc = wsc[w * 16 + h];
+                const float4 v = *reinterpret_cast<const float4*>(wo + (w * 16 + h) * D + c);
+                acc.x += sc * v.x; acc.y += sc * v.y; acc.z += sc * v.z; acc.w += sc * v.w;
+            }
+            st_async_u4(mapa_shared(rcv_a + (uint32_t)(split * per + (i - q * per)) * 4u, q),
+                        make_uint4(__float_as_uint(acc.x), __float_as_uint(acc.y), __float_as_uint(acc.z),
+                                   __float_as_uint(acc.w)),
+                        mapa_shared(mbar, q));
         }
         for (int i = tid; i < 32 * S; i += NTH) {
             const int q = i >> 5, h = i & 31;
