@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     // the idx loads of batch NBUF - 1 (consumed at the top of iteration 0)
     if (tid < (NBUF - 1) * RB && !published(tid)) rows_s[tid] = resolve(tid, pre);
     if (!pub_early && tid < RB) pend = NBUF == 1 ? pre : fetch((NBUF - 1) * RB + tid);
-    cta_sync();
+    if (!pub_early) cta_sync();  // (an early pass wrote its prologue row ids before the wait)
     stamp(2);
     if (!pub_early)
         for (int j = 0; j < NBUF - 1; ++j) issue(j);
@@ -349,10 +349,12 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     for (int j = 0; j < nb; ++j) {
         // row ids of batch j + NBUF - 1 (loads issued one iteration ago), then the loads of
         // batch j + NBUF's; the barrier publishes the ids and frees buffer (j - 1) % NBUF
-        if (tid < RB && !published((j + NBUF - 1) * RB + tid))
-            rows_s[((j + NBUF - 1) % NBUF) * RB + tid] = resolve((j + NBUF - 1) * RB + tid, pend);
-        if (tid < RB) pend = fetch((j + NBUF) * RB + tid);
-        cta_sync();
+        if (j + NBUF - 1 < nb) {  // (past the last batch: nothing to publish, no buffer to free)
+            if (tid < RB && !published((j + NBUF - 1) * RB + tid))
+                rows_s[((j + NBUF - 1) % NBUF) * RB + tid] = resolve((j + NBUF - 1) * RB + tid, pend);
+            if (tid < RB) pend = fetch((j + NBUF) * RB + tid);
+            cta_sync();
+        }
         issue(j + NBUF - 1);
         cp_async_wait<NBUF - 1>();  // batch j landed (this thread's copies)
         cta_sync();                 // ... and everyone's
