@@ -6,29 +6,34 @@
 // remain cached but inactive"; SPEC.md:315-323 pack_active order).  For each
 // unit (b, KV group G) the attended rows
 //     [0, vb)  U  {vb + idx[m] : m < k}  U  [vb + N_v, seq_len)
-// are cut into S splits, one CTA each, the grid (S x units) sized to the
-// co-resident CTA count (B = 1: 4 units x 37 splits = all 148 SMs).  Split s
-// takes the s-th S-th of each of the three segments (system rows, kept visual
-// rows, later text rows), so its visual share -- the idx loads and the K/V
-// gathers -- does not wait for seq_len.  Per CTA (256 threads, one per SM):
+// are cut into S splits, one CTA each (api.cu plan_decode: S from the co-resident
+// CTA count; B = 1: 4 units x 16 splits).  Split s takes the s-th S-th of each of
+// the three segments (system rows, kept visual rows, later text rows), so its
+// visual share -- the idx loads and the K/V gathers -- does not wait for seq_len.
+// Per CTA (256 threads, one per SM):
 //   1. software pipeline over 128-row batches: row ids of batch j + NBUF are
 //      loaded (idx validated: in range, strictly ascending) while batch j is
 //      computed; K and V rows of batch j + NBUF - 1 are gathered with cp.async
-//      (16-byte, L1-bypassing) into XOR-swizzled shared memory;
+//      (16-byte, L1-bypassing) into XOR-swizzled shared memory.  With
+//      SVL_DECODE_STATIC_PREFIX the first batches' rows (all but the current
+//      token's) are gathered before the PDL wait, laid out by a speculative
+//      seq_len read that is checked after the batch loop (a miss reruns it);
 //   2. per warp and 16-row tile: S = q K^T with mma.sync m16n8k16 (heads are M,
 //      rows are N, the contraction permuted so K chunks are read with
 //      conflict-free 128-bit LDS), online softmax in base 2, O += P V with P
 //      split into bf16 hi + lo (two MMAs: ~2^-17 relative error instead of
-//      bf16's 2^-9) and V B-fragments from ldmatrix.trans;
-//   3. S > 1: the CTA's partial (o, m, l) is stored (coalesced) to the
-//      workspace; a barrier over the unit's CTAs (release add / acquire spin
-//      on a counter in the workspace header; every CTA is co-resident: the
-//      grid is sized for it and launched cooperatively); then CTA s merges a
-//      1/S slice of its unit's (head, column) items over the S partials,
-//      staged in shared memory with one round of coalesced loads:
+//      bf16's 2^-9) and V B-fragments from ldmatrix.trans; one cross-warp merge
+//      per CTA gives its partial (o, M, l);
+//   3. S > 1, the S CTAs of a unit one thread-block cluster (every cluster
+//      co-resident): each CTA owns a 1/S share of the unit's (head, column)
+//      items (a multiple of 4); every CTA pushes its partial's items to their
+//      owners and its (M, l) to every peer with st.async (16-byte pushes,
+//      mbarrier byte counts), each owner merges over the S partials in rank
+//      order.  Otherwise a co-resident grid (cooperative launch): partials are
+//      stored as 64-bit (value, tag) pairs tagged with the unit's call epoch
+//      and each CTA merges its share once the tags it needs are this call's.
 //      M = max m_i, out = sum e^{m_i-M} o_i / sum e^{m_i-M} l_i,
 //      lse = M + log sum e^{m_i-M} l_i (north star step 3), in a fixed order.
-//      The counters reset themselves (the unit's last CTA out zeroes them).
 #include <stdlib.h>
 
 #include "common.cuh"
