@@ -276,9 +276,6 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
             rows_s[tid] = tid < nst ? resolve_st(tid, pre) : (tid < n_s ? p.vb + p.nv + t0s + (tid - nst) : -1);
         cta_sync();
         const int i_cur = (nas > 0 && t0s + nas == Ls - p.vb - p.nv) ? n_s - 1 : -1;  // the current row's item
-#if SVL_EXP_CURPRE  // timing experiment: the current row gathered before the wait too
-        const_cast<int&>(i_cur) = -1;
-#endif
         for (int j = 0; j < JE; ++j) issue_rows(j, [&](int i) { return i != i_cur; }, n_s);
         cp_async_commit();  // (one group, older than every group below)
         asm volatile("griddepcontrol.wait;" ::: "memory");
