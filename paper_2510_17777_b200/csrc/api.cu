@@ -219,9 +219,10 @@ bool encode_kv_tensor_map(CUtensorMap* map, const void* data, int d, int capacit
 extern "C" {
 
 const char* svl_version(void) {
-    return "libsparsevila 0.4 sm_100a (fused fresh step: TMA + tcgen05 K stream, cluster top-k over DSMEM, split "
+    return "libsparsevila 0.5 sm_100a (fused fresh step: TMA + tcgen05 K stream, cluster top-k over DSMEM, split "
            "decode / selection warp groups after the threshold bin; "
-           "steady decode: split-K gather, cluster DSMEM merge (<= 16 splits) or epoch-tagged L2 merge; "
+           "steady decode: split-K gather (optionally started before the PDL wait), co-resident cluster DSMEM "
+           "merge or epoch-tagged L2 merge; "
            "question chunk: tcgen05 row LSE, column mass and attention output (P from TMEM))";
 }
 
