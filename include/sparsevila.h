@@ -221,15 +221,19 @@ size_t svl_question_attention_workspace_size(int32_t B, int32_t n_q, int32_t H, 
  * token's K/V before the call (reading A9).
  *   out[b,h,:] = sum_j softmax(scale * q.K_j)_j V_j   (fp32, reading A18)
  *   lse[b,h]   = natural-log log-sum-exp of the attended logits
- * Split-K flash-decoding with a log-sum-exp merge across splits: the grid
- * (S splits per unit) is sized to the co-resident CTA count and launched
- * cooperatively; each split stores its partial (o, m, l) to the workspace
- * tagged with the unit's call epoch (a counter in the workspace header that
- * the unit's first CTA advances once per call), and every split merges a
- * 1/S slice of the unit's outputs as soon as the tagged partials it needs are
- * visible.  The merge order is fixed: results are bitwise reproducible for a
- * given split count.
- * flags    SVL_SELECT_SHARED, SVL_PIN_SPLITS(n).
+ * Split-K flash-decoding with a log-sum-exp merge across splits, S splits
+ * (CTAs) per unit, S from the co-resident CTA count.  While every unit's S
+ * CTAs fit as co-resident thread-block clusters (S <= 16), each unit is one
+ * cluster and the splits push their partials (o, m, l) to the owning CTAs
+ * over distributed shared memory; otherwise the grid is launched
+ * cooperatively, each split stores its partial to the workspace tagged with
+ * the unit's call epoch (a counter in the workspace header that the unit's
+ * first CTA advances once per call), and every split merges a 1/S slice of
+ * the unit's outputs as soon as the tagged partials it needs are visible.
+ * The merge order is fixed: results are bitwise reproducible for a given
+ * split count and merge path.
+ * flags    SVL_SELECT_SHARED, SVL_PIN_SPLITS(n), SVL_IDX_PADDED,
+ *          SVL_DECODE_GRID_MERGE, SVL_DECODE_STATIC_PREFIX (see above).
  *
  * q        device bf16 [B][H][d] contiguous; g = H/Hkv <= 16.
  * K, V     device KV views with identical capacity.
