@@ -127,3 +127,29 @@ def test_decode_planner_batch_sweep_matches_oracle(svl, orc, B):
     assert torch.equal(a, b) and torch.equal(lse_a, lse)
     parity.check_attention(a.cpu().numpy(), lse_a.cpu().numpy(), oo, ol)
     assert ws.flags() == 0
+
+
+@pytest.mark.parametrize("name", ["toy", "nvila-4k"])
+def test_decode_early_gathers_under_a_racing_seq_len_writer(svl, name):
+    """SVL_DECODE_STATIC_PREFIX reads seq_len speculatively before the PDL wait and checks it
+    after the batch loop.  Here the upstream kernel (a fused fresh step, a PDL primary) writes
+    its fp32 output over the very words the decode then reads as seq_len: the early read may
+    see the old value, the checked read sees the fresh step's bits (clamped to the span, device
+    flag raised).  Whatever the race, the result must equal a plain call on the final value."""
+    wl = gen.CONFIGS[name]
+    x = gen.make_decode_inputs(wl, seed=95, device="cuda")
+    idx = svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k).clone()
+    buf = torch.zeros(wl.B, wl.H, wl.d, device="cuda")  # the fresh step's out
+    seq_view = buf.view(-1).view(torch.int32)[:wl.B]    # ... whose first words are the seq_len
+    ws_f, ws_d, ws_r = svl.Workspace(), svl.Workspace(), svl.Workspace()
+    a = torch.empty(wl.B, wl.H, wl.d, device="cuda")
+    b = torch.empty_like(a)
+    for it in range(30):
+        seq_view.copy_(x["seq_len"])
+        svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k, out=buf, ws=ws_f)
+        svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], seq_view, wl.vb, wl.nv, idx,
+                               flags=svl.SVL_DECODE_STATIC_PREFIX, out=a, ws=ws_d)
+        torch.cuda.synchronize()
+        svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], seq_view, wl.vb, wl.nv, idx, out=b, ws=ws_r)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), f"iteration {it}"
