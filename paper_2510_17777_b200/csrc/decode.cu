@@ -453,6 +453,9 @@ __global__ void __launch_bounds__(NTH, 1) decode_kernel(const __grid_constant__ 
     if (!early || !pub_early) break;
     const int L_chk = checked_len();
     if (L_chk == Ls) break;
+#if SVL_EXP_MISS_FLAG  // test build: report a speculation miss in the device flags (bit 16)
+    if (tid == 0) raise_flag(p.flags, 16u);
+#endif
     // the speculation missed (seq_len changed upstream): rerun on the checked value with every
     // row gathered after the wait (the pipeline's buffers are idle: the barrier above)
     pub_early = false;

@@ -129,27 +129,40 @@ def test_decode_planner_batch_sweep_matches_oracle(svl, orc, B):
     assert ws.flags() == 0
 
 
-@pytest.mark.parametrize("name", ["toy", "nvila-4k"])
-def test_decode_early_gathers_under_a_racing_seq_len_writer(svl, name):
+@pytest.mark.parametrize("name,up", [("toy", "fresh"), ("nvila-4k", "fresh"), ("long-video", "decode")])
+def test_decode_early_gathers_under_a_racing_seq_len_writer(svl, name, up):
     """SVL_DECODE_STATIC_PREFIX reads seq_len speculatively before the PDL wait and checks it
-    after the batch loop.  Here the upstream kernel (a fused fresh step, a PDL primary) writes
-    its fp32 output over the very words the decode then reads as seq_len: the early read may
-    see the old value, the checked read sees the fresh step's bits (clamped to the span, device
-    flag raised).  Whatever the race, the result must equal a plain call on the final value."""
+    after the batch loop.  Here the upstream kernel (a fused fresh step or a plain decode, a PDL
+    primary) writes its fp32 output over the very words the decode then reads as seq_len, in a
+    CUDA graph (eager launches leave CPU gaps: nothing would race): the early read sees the old
+    value, the checked read the upstream's bits (clamped to the span, device flag raised), so
+    every replay takes the miss path (a build that flags misses counted 50 of 50:
+    profiles/specmiss_r03.txt).  The result must equal a plain call on the final value."""
     wl = gen.CONFIGS[name]
     x = gen.make_decode_inputs(wl, seed=95, device="cuda")
     idx = svl.retrieve(x["q"], x["K"], x["seq_len"], wl.vb, wl.nv, wl.k).clone()
-    buf = torch.zeros(wl.B, wl.H, wl.d, device="cuda")  # the fresh step's out
+    buf = torch.zeros(wl.B, wl.H, wl.d, device="cuda")  # the upstream's out
     seq_view = buf.view(-1).view(torch.int32)[:wl.B]    # ... whose first words are the seq_len
-    ws_f, ws_d, ws_r = svl.Workspace(), svl.Workspace(), svl.Workspace()
+    ws_u, ws_d, ws_r = svl.Workspace(), svl.Workspace(), svl.Workspace()
     a = torch.empty(wl.B, wl.H, wl.d, device="cuda")
-    b = torch.empty_like(a)
-    for it in range(30):
+
+    def body():
         seq_view.copy_(x["seq_len"])
-        svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k, out=buf, ws=ws_f)
+        if up == "fresh":
+            svl.fresh_decode_step(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, wl.k, out=buf, ws=ws_u)
+        else:
+            svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], x["seq_len"], wl.vb, wl.nv, idx, out=buf, ws=ws_u)
         svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], seq_view, wl.vb, wl.nv, idx,
                                flags=svl.SVL_DECODE_STATIC_PREFIX, out=a, ws=ws_d)
+    body()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            body()
+    for it in range(20):
+        g.replay()
         torch.cuda.synchronize()
-        svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], seq_view, wl.vb, wl.nv, idx, out=b, ws=ws_r)
-        torch.cuda.synchronize()
-        assert torch.equal(a, b), f"iteration {it}"
+        ref, _ = svl.sparse_decode_attn(x["q_dec"], x["K"], x["V"], seq_view, wl.vb, wl.nv, idx, ws=ws_r)
+        assert torch.equal(a, ref), f"replay {it}"
